@@ -1,0 +1,170 @@
+/* brax_b200.h — C ABI of the B200-native batched Brax physics step.
+ *
+ * What it computes: the paper's physics step (arXiv 2106.13281, §3 and Alg. 1,
+ * PAPER.md:60-75):  qp_{t+dt} = Brax_system.step(qp_t, actions),
+ * i.e. `substeps` repetitions of
+ *     kinematic integrator → Σ joints, Σ actuators, Σ colliders (all on the same qp)
+ *     → potential integrator (dp_j + dp_a, dt) → collision integrator (dp_c),
+ * for n independent environments (the paper's vmap over scenes),
+ * with every formula as read in SURVEY.md §8(c) / DESIGN.md "Readings".
+ *
+ * Library: paper_2106_13281_b200/_lib/libbrax_b200.so (sm_100a only).
+ * No CPU fallback exists: every compute entry point launches CUDA kernels.
+ *
+ * Conventions shared by all entry points
+ *  - Return value: brax_status.  On error, brax_last_error_detail() returns a
+ *    thread-local human-readable detail ("line:col: msg", "bodies[3].mass: must
+ *    be > 0", or CUDA's error string).  Nothing is launched when an argument
+ *    check fails.
+ *  - Ownership: the library owns brax_config / brax_system objects until the
+ *    matching *_destroy.  The caller owns every device buffer and the stream.
+ *    brax_step allocates nothing; all scratch is on-chip.
+ *  - Device pointers: every pointer in brax_qp, `action` and brax_step_extras is a
+ *    CUDA device pointer on the system's device, fp32 / u8 / u32 as stated,
+ *    C-contiguous, 16-byte aligned (else BRAX_E_MISALIGNED).
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls are stream-ordered and never synchronise; BRAX_OK means
+ *    "enqueued".  A failed launch returns BRAX_E_CUDA.
+ *  - Thread safety: a brax_system is immutable after creation; concurrent
+ *    brax_step calls on distinct streams are safe.
+ */
+#ifndef BRAX_B200_H_
+#define BRAX_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BRAX_ABI_VERSION 1
+
+typedef enum {
+  BRAX_OK = 0,
+  BRAX_E_INVALID_ARGUMENT = 1,   /* NULL pointer, negative size, partial aliasing, wrong shape */
+  BRAX_E_PARSE = 2,              /* config text: syntax error (detail "line:col: msg") */
+  BRAX_E_VALIDATION = 3,         /* config: semantic error (detail "path: msg") */
+  BRAX_E_CYCLIC_JOINT_GRAPH = 4, /* joints do not form a forest */
+  BRAX_E_UNSUPPORTED_PAIR = 5,   /* collider pair outside the supported set */
+  BRAX_E_MISALIGNED = 6,         /* a device pointer is not 16-byte aligned */
+  BRAX_E_CUDA = 7,               /* CUDA runtime error (no device, launch failure, ...) */
+  BRAX_E_OUT_OF_MEMORY = 8
+} brax_status;
+
+/* Contact-slot types (integer contact indexing).  Part of the ABI:
+ * brax_system_slot_table reports them and tests compare them bit-exactly. */
+typedef enum {
+  BRAX_SLOT_SPHERE_PLANE = 0,
+  BRAX_SLOT_CAPSULE_PLANE = 1,   /* one slot per capsule end (point 0 = c + l·a, 1 = c − l·a) */
+  BRAX_SLOT_BOX_PLANE = 2,       /* 8 corner slots, point k ↔ signs (k&1, k&2, k&4) of (hx, hy, hz) */
+  BRAX_SLOT_SPHERE_SPHERE = 3,
+  BRAX_SLOT_SPHERE_CAPSULE = 4,  /* sphere is A */
+  BRAX_SLOT_CAPSULE_CAPSULE = 5  /* lower collider index is A */
+} brax_slot_type;
+
+/* ---------------------------------------------------------------- config
+ * Text form: the ProtoBuf text subset of the paper's App. A:
+ * top-level dt, substeps, gravity{x y z}, friction, elasticity, baumgarte_erp,
+ * repeated bodies{name mass inertia{} frozen{position{} rotation{} all} colliders{
+ * position{} rotation{} (sphere{radius} | capsule{radius length end} |
+ * box{halfsize{}} | plane{})}}, joints{name parent child stiffness spring_damping
+ * angular_damping limit_stiffness angular_stiffness parent_offset{} child_offset{}
+ * rotation{} reference_rotation{} angle_limit{min max}×dof}, actuators{name joint
+ * strength (torque{} | angle{})}, collide_include{first second},
+ * defaults{qps{name pos{} rot{}}}.  Angles in degrees (Euler, intrinsic X-Y-Z). */
+typedef struct brax_config brax_config;
+
+/* Parse + validate `len` bytes of text (need not be NUL-terminated).
+ * *out receives a new config on BRAX_OK (free with brax_config_destroy).
+ * Errors: BRAX_E_PARSE, BRAX_E_VALIDATION, BRAX_E_CYCLIC_JOINT_GRAPH,
+ * BRAX_E_UNSUPPORTED_PAIR, BRAX_E_INVALID_ARGUMENT. */
+brax_status brax_config_parse(const char *text, size_t len, brax_config **out);
+void brax_config_destroy(brax_config *cfg);
+
+/* Host-only introspection of a parsed config (no GPU needed). */
+brax_status brax_config_counts(const brax_config *cfg, int32_t *n_bodies, int32_t *n_joints, int32_t *act_dim,
+                               int32_t *n_slots);          /* any output may be NULL */
+/* Integer contact-slot table, host [C][7] int32 (see brax_system_slot_table). */
+brax_status brax_config_slot_table(const brax_config *cfg, int32_t *out);
+/* default_qp in fp64 (host): pos [B][3], rot [B][4] (velocities are zero). */
+brax_status brax_config_default_qp(const brax_config *cfg, double *pos, double *rot);
+
+/* ---------------------------------------------------------------- system
+ * The paper's `system`: immutable device-resident static
+ * tables (bodies, joints with their actuators, contact slots, per-body incidence
+ * lists, warp work plan) built from a config.  `cuda_device` selects the GPU.
+ * Errors: BRAX_E_INVALID_ARGUMENT, BRAX_E_CUDA, BRAX_E_OUT_OF_MEMORY. */
+typedef struct brax_system brax_system;
+brax_status brax_system_create(const brax_config *cfg, int cuda_device, brax_system **out);
+void brax_system_destroy(brax_system *sys);
+
+typedef struct {
+  int32_t n_bodies;        /* B: rows per env in every QP array (incl. static bodies) */
+  int32_t n_dynamic;       /* bodies with at least one unfrozen axis */
+  int32_t n_joints;        /* J */
+  int32_t act_dim;         /* A: action width (actuators in config order, dof-major) */
+  int32_t n_contact_slots; /* C */
+  int32_t substeps;        /* S */
+  float dt;                /* step length; substep h = dt / S */
+  int32_t warps_per_block; /* launch shape of the step kernel (32 envs per block) */
+  int32_t n_lint_warnings; /* stability lint (R6) */
+  int32_t smem_bytes;      /* dynamic shared memory per block of the step kernel */
+} brax_system_info;
+brax_status brax_system_get_info(const brax_system *sys, brax_system_info *out);
+
+/* Integer contact-slot table, host buffer [C][7] int32 row-major:
+ * (pair index, brax_slot_type, body A, body B, collider A, collider B, point). */
+brax_status brax_system_slot_table(const brax_system *sys, int32_t *out);
+
+/* Lint warning i (0 <= i < n_lint_warnings) as text; NULL if out of range. */
+const char *brax_system_lint_warning(const brax_system *sys, int32_t i);
+
+/* default_qp: host fp32 buffers of B rows each:
+ * pos [B][3], rot [B][4] (w,x,y,z), vel [B][3], ang [B][3]. */
+brax_status brax_default_qp(const brax_system *sys, float *h_pos, float *h_rot, float *h_vel, float *h_ang);
+
+/* ---------------------------------------------------------------- state
+ * QP: structure of arrays, env-major: pos [n][B][3], rot [n][B][4]
+ * (w,x,y,z), vel [n][B][3], ang [n][B][3]; fp32 device pointers. */
+typedef struct {
+  float *pos, *rot, *vel, *ang;
+} brax_qp;
+
+/* Broadcast default_qp to n_envs envs, then for every non-static body add
+ * v += M_pos ⊙ vel_noise·u, ω += M_rot ⊙ ang_noise·u with u ∈ [−1, 1) from
+ * Philox4x32-10(key = seed, counter = (env, body, field, 0)).
+ * n_envs == 0 is a no-op.  Errors: INVALID_ARGUMENT, MISALIGNED, CUDA. */
+brax_status brax_reset(const brax_system *sys, brax_qp out, int64_t n_envs, uint64_t seed, float vel_noise,
+                       float ang_noise, void *stream);
+
+/* One Brax step of n_envs envs: out = step(in, action).  action: [n][act_dim] fp32
+ * device (may be NULL iff act_dim == 0), held for all substeps.  in == out (all four
+ * pointers equal) is allowed; partial aliasing is BRAX_E_INVALID_ARGUMENT.
+ * Static (fully frozen) bodies are copied through bit for bit. */
+brax_status brax_step(const brax_system *sys, brax_qp in, const float *action, brax_qp out, int64_t n_envs,
+                      void *stream);
+
+typedef struct {
+  uint32_t *status;        /* [n] bit0 non-finite value, bit1 |value| > 1e6; or NULL */
+  uint8_t *contact_active; /* [n][C] number of substeps each slot was active; or NULL */
+} brax_step_extras;
+
+/* brax_step plus optional per-env outputs (NULL extras or NULL members = skip). */
+brax_status brax_step_ex(const brax_system *sys, brax_qp in, const float *action, brax_qp out, int64_t n_envs,
+                         const brax_step_extras *extras, void *stream);
+
+/* Run `n_steps` consecutive steps inside ONE kernel launch (the QP stays on-chip
+ * between steps).  actions: [n_steps][n][act_dim].
+ * Equivalent to n_steps brax_step calls (bitwise, same binary). */
+brax_status brax_rollout(const brax_system *sys, brax_qp in, const float *actions, int64_t n_steps, brax_qp out,
+                         int64_t n_envs, const brax_step_extras *extras, void *stream);
+
+const char *brax_status_string(brax_status s);
+const char *brax_last_error_detail(void);
+int brax_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BRAX_B200_H_ */

@@ -1,0 +1,271 @@
+"""B200-native batched Brax physics step (arXiv 2106.13281, §3 Alg. 1).
+
+Thin ctypes binding over the C ABI in include/brax_b200.h (library
+paper_2106_13281_b200/_lib/libbrax_b200.so, sm_100a).  Argument marshalling
+only: every step of the physics runs in the library's CUDA kernels.  There is
+no CPU fallback — importing fails loudly if the library is missing, and system
+creation fails loudly without a CUDA device.
+
+PyTorch is used for device memory and streams only:
+
+    import torch, paper_2106_13281_b200 as bx
+    sys = bx.System(open("scenes/ant.bxc").read())
+    qp = sys.alloc_qp(8192)                     # dict of fp32 cuda tensors
+    sys.reset(qp, seed=0, vel_noise=0.1, ang_noise=0.1)
+    sys.step(qp, action, qp)                    # in-place is allowed
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+__all__ = [
+    "BraxError", "System", "brax_config_parse", "brax_config_destroy", "brax_config_counts",
+    "brax_config_slot_table", "brax_config_default_qp", "brax_system_create", "brax_system_destroy",
+    "brax_system_get_info", "brax_system_slot_table", "brax_default_qp", "brax_reset", "brax_step",
+    "brax_step_ex", "brax_rollout", "brax_qp", "brax_step_extras", "brax_system_info", "LIB_PATH", "lib",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbrax_b200.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2106_13281_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+lib = C.CDLL(LIB_PATH)
+
+STATUS = ["BRAX_OK", "BRAX_E_INVALID_ARGUMENT", "BRAX_E_PARSE", "BRAX_E_VALIDATION",
+          "BRAX_E_CYCLIC_JOINT_GRAPH", "BRAX_E_UNSUPPORTED_PAIR", "BRAX_E_MISALIGNED", "BRAX_E_CUDA",
+          "BRAX_E_OUT_OF_MEMORY"]
+
+
+class BraxError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        self.name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        self.detail = detail
+        super().__init__(f"{self.name}: {detail}")
+
+
+class brax_qp(C.Structure):
+    _fields_ = [("pos", C.c_void_p), ("rot", C.c_void_p), ("vel", C.c_void_p), ("ang", C.c_void_p)]
+
+
+class brax_step_extras(C.Structure):
+    _fields_ = [("status", C.c_void_p), ("contact_active", C.c_void_p)]
+
+
+class brax_system_info(C.Structure):
+    _fields_ = [("n_bodies", C.c_int32), ("n_dynamic", C.c_int32), ("n_joints", C.c_int32),
+                ("act_dim", C.c_int32), ("n_contact_slots", C.c_int32), ("substeps", C.c_int32),
+                ("dt", C.c_float), ("warps_per_block", C.c_int32), ("n_lint_warnings", C.c_int32),
+                ("smem_bytes", C.c_int32)]
+
+
+_P = C.c_void_p
+_i32p = C.POINTER(C.c_int32)
+_SIGS = {
+    "brax_config_parse": ([C.c_char_p, C.c_size_t, C.POINTER(_P)], C.c_int),
+    "brax_config_destroy": ([_P], None),
+    "brax_config_counts": ([_P, _i32p, _i32p, _i32p, _i32p], C.c_int),
+    "brax_config_slot_table": ([_P, _i32p], C.c_int),
+    "brax_config_default_qp": ([_P, _P, _P], C.c_int),
+    "brax_system_create": ([_P, C.c_int, C.POINTER(_P)], C.c_int),
+    "brax_system_destroy": ([_P], None),
+    "brax_system_get_info": ([_P, C.POINTER(brax_system_info)], C.c_int),
+    "brax_system_slot_table": ([_P, _i32p], C.c_int),
+    "brax_system_lint_warning": ([_P, C.c_int32], C.c_char_p),
+    "brax_default_qp": ([_P, _P, _P, _P, _P], C.c_int),
+    "brax_reset": ([_P, brax_qp, C.c_int64, C.c_uint64, C.c_float, C.c_float, _P], C.c_int),
+    "brax_step": ([_P, brax_qp, _P, brax_qp, C.c_int64, _P], C.c_int),
+    "brax_step_ex": ([_P, brax_qp, _P, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
+    "brax_rollout": ([_P, brax_qp, _P, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
+    "brax_status_string": ([C.c_int], C.c_char_p),
+    "brax_last_error_detail": ([], C.c_char_p),
+    "brax_abi_version": ([], C.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def _check(status: int):
+    if status != 0:
+        raise BraxError(status, lib.brax_last_error_detail().decode())
+
+
+# ---------------------------------------------------------------- same-name wrappers
+def brax_config_parse(text: str) -> int:
+    out = _P()
+    raw = text.encode()
+    _check(lib.brax_config_parse(raw, len(raw), C.byref(out)))
+    return out.value
+
+
+def brax_config_destroy(cfg: int) -> None:
+    lib.brax_config_destroy(cfg)
+
+
+def brax_config_counts(cfg: int):
+    v = [C.c_int32() for _ in range(4)]
+    _check(lib.brax_config_counts(cfg, *[C.byref(x) for x in v]))
+    return tuple(x.value for x in v)  # (n_bodies, n_joints, act_dim, n_slots)
+
+
+def brax_config_slot_table(cfg: int):
+    import numpy as np
+    n_slots = brax_config_counts(cfg)[3]
+    out = np.zeros((n_slots, 7), dtype=np.int32)
+    _check(lib.brax_config_slot_table(cfg, out.ctypes.data_as(_i32p)))
+    return out
+
+
+def brax_config_default_qp(cfg: int):
+    import numpy as np
+    B = brax_config_counts(cfg)[0]
+    pos = np.zeros((B, 3))
+    rot = np.zeros((B, 4))
+    _check(lib.brax_config_default_qp(cfg, pos.ctypes.data, rot.ctypes.data))
+    return pos, rot
+
+
+def brax_system_create(cfg: int, cuda_device: int = 0) -> int:
+    out = _P()
+    _check(lib.brax_system_create(cfg, cuda_device, C.byref(out)))
+    return out.value
+
+
+def brax_system_destroy(sys: int) -> None:
+    lib.brax_system_destroy(sys)
+
+
+def brax_system_get_info(sys: int) -> brax_system_info:
+    info = brax_system_info()
+    _check(lib.brax_system_get_info(sys, C.byref(info)))
+    return info
+
+
+def brax_system_slot_table(sys: int):
+    import numpy as np
+    info = brax_system_get_info(sys)
+    out = np.zeros((info.n_contact_slots, 7), dtype=np.int32)
+    _check(lib.brax_system_slot_table(sys, out.ctypes.data_as(_i32p)))
+    return out
+
+
+def brax_default_qp(sys: int):
+    import numpy as np
+    B = brax_system_get_info(sys).n_bodies
+    arrs = {"pos": np.zeros((B, 3), np.float32), "rot": np.zeros((B, 4), np.float32),
+            "vel": np.zeros((B, 3), np.float32), "ang": np.zeros((B, 3), np.float32)}
+    _check(lib.brax_default_qp(sys, *[arrs[k].ctypes.data for k in ("pos", "rot", "vel", "ang")]))
+    return arrs
+
+
+def _qp(q) -> brax_qp:
+    return brax_qp(*(int(q[k].data_ptr()) for k in ("pos", "rot", "vel", "ang")))
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def brax_reset(sys: int, qp_out, n_envs: int, seed: int, vel_noise: float = 0.0, ang_noise: float = 0.0,
+               stream=None) -> None:
+    _check(lib.brax_reset(sys, _qp(qp_out), n_envs, seed & 0xFFFFFFFFFFFFFFFF, vel_noise, ang_noise,
+                          _stream(stream)))
+
+
+def brax_step(sys: int, qp_in, action, qp_out, n_envs: int, stream=None) -> None:
+    _check(lib.brax_step(sys, _qp(qp_in), None if action is None else action.data_ptr(), _qp(qp_out), n_envs,
+                         _stream(stream)))
+
+
+def _extras(status, contact_active):
+    if status is None and contact_active is None:
+        return None
+    return brax_step_extras(None if status is None else status.data_ptr(),
+                            None if contact_active is None else contact_active.data_ptr())
+
+
+def brax_step_ex(sys: int, qp_in, action, qp_out, n_envs: int, status=None, contact_active=None,
+                 stream=None) -> None:
+    x = _extras(status, contact_active)
+    _check(lib.brax_step_ex(sys, _qp(qp_in), None if action is None else action.data_ptr(), _qp(qp_out), n_envs,
+                            None if x is None else C.byref(x), _stream(stream)))
+
+
+def brax_rollout(sys: int, qp_in, actions, n_steps: int, qp_out, n_envs: int, status=None, contact_active=None,
+                 stream=None) -> None:
+    x = _extras(status, contact_active)
+    _check(lib.brax_rollout(sys, _qp(qp_in), None if actions is None else actions.data_ptr(), n_steps,
+                            _qp(qp_out), n_envs, None if x is None else C.byref(x), _stream(stream)))
+
+
+# ---------------------------------------------------------------- convenience object
+class System:
+    """A config parsed and turned into a device-resident system (owns both handles)."""
+
+    def __init__(self, text: str, device: int = 0):
+        self._cfg = brax_config_parse(text)
+        try:
+            self._sys = brax_system_create(self._cfg, device)
+        except Exception:
+            brax_config_destroy(self._cfg)
+            self._cfg = None
+            raise
+        self.device = device
+        self.info = brax_system_get_info(self._sys)
+
+    def __del__(self):
+        if getattr(self, "_sys", None):
+            brax_system_destroy(self._sys)
+            self._sys = None
+        if getattr(self, "_cfg", None):
+            brax_config_destroy(self._cfg)
+            self._cfg = None
+
+    handle = property(lambda self: self._sys)
+    n_bodies = property(lambda self: self.info.n_bodies)
+    act_dim = property(lambda self: self.info.act_dim)
+    n_slots = property(lambda self: self.info.n_contact_slots)
+    substeps = property(lambda self: self.info.substeps)
+
+    def lint(self):
+        return [lib.brax_system_lint_warning(self._sys, i).decode() for i in range(self.info.n_lint_warnings)]
+
+    def slot_table(self):
+        return brax_system_slot_table(self._sys)
+
+    def default_qp(self):
+        return brax_default_qp(self._sys)
+
+    def alloc_qp(self, n: int):
+        import torch
+        dev = torch.device("cuda", self.device)
+        B = self.n_bodies
+        return {"pos": torch.empty((n, B, 3), device=dev), "rot": torch.empty((n, B, 4), device=dev),
+                "vel": torch.empty((n, B, 3), device=dev), "ang": torch.empty((n, B, 3), device=dev)}
+
+    def reset(self, qp, seed: int = 0, vel_noise: float = 0.0, ang_noise: float = 0.0, stream=None):
+        brax_reset(self._sys, qp, qp["pos"].shape[0], seed, vel_noise, ang_noise, stream)
+        return qp
+
+    def step(self, qp_in, action, qp_out=None, *, status=None, contact_active=None, stream=None):
+        qp_out = qp_in if qp_out is None else qp_out
+        n = qp_in["pos"].shape[0]
+        if status is None and contact_active is None:
+            brax_step(self._sys, qp_in, action, qp_out, n, stream)
+        else:
+            brax_step_ex(self._sys, qp_in, action, qp_out, n, status, contact_active, stream)
+        return qp_out
+
+    def rollout(self, qp_in, actions, qp_out=None, *, n_steps=None, status=None, contact_active=None,
+                stream=None):
+        qp_out = qp_in if qp_out is None else qp_out
+        n = qp_in["pos"].shape[0]
+        T = n_steps if n_steps is not None else actions.shape[0]
+        brax_rollout(self._sys, qp_in, actions, T, qp_out, n, status, contact_active, stream)
+        return qp_out

@@ -1,0 +1,509 @@
+// config.cpp — ProtoBuf-text scene parser, schema mapping and validation.
+//
+// Grammar: the text subset the paper exhibits in App. A:
+//   file := field* ;  field := NAME ':' scalar | NAME ':'? '{' field* '}'
+// '#' comments, ',' and ';' separators are ignored.  Semantic rules (defaults,
+// pair enumeration R19, forest check) follow SPEC.md:290-298 and SURVEY §8(c).
+#include <cmath>
+#include <cstdlib>
+#include <map>
+#include <set>
+#include <sstream>
+
+#include "config.h"
+
+namespace brax {
+namespace {
+
+struct Node {
+  enum Kind { kNum, kStr, kIdent, kMsg } kind = kNum;
+  std::string name;
+  double num = 0;
+  std::string str;
+  std::vector<Node> children;
+  int line = 1, col = 1;
+};
+
+struct Token {
+  enum Kind { kName, kNumber, kString, kPunct, kEof } kind;
+  std::string text;
+  int line, col;
+};
+
+[[noreturn]] void parse_error(int line, int col, const std::string& msg) {
+  std::ostringstream os;
+  os << line << ":" << col << ": " << msg;
+  throw Error(BRAX_E_PARSE, os.str());
+}
+
+std::vector<Token> tokenize(const std::string& s) {
+  std::vector<Token> out;
+  size_t i = 0;
+  int line = 1;
+  size_t line_start = 0;
+  auto isdig = [](char c) { return c >= '0' && c <= '9'; };
+  while (i < s.size()) {
+    char c = s[i];
+    int col = int(i - line_start) + 1;
+    if (c == '\n') { ++i; ++line; line_start = i; continue; }
+    if (c == ' ' || c == '\t' || c == '\r' || c == ',' || c == ';') { ++i; continue; }
+    if (c == '#') { while (i < s.size() && s[i] != '\n') ++i; continue; }
+    if (c == '{' || c == '}' || c == ':') { out.push_back({Token::kPunct, std::string(1, c), line, col}); ++i; continue; }
+    if (c == '"') {
+      size_t j = i + 1;
+      std::string val;
+      while (j < s.size() && s[j] != '"') {
+        if (s[j] == '\n') parse_error(line, col, "unterminated string");
+        if (s[j] == '\\' && j + 1 < s.size()) {
+          char e = s[j + 1];
+          val += (e == 'n') ? '\n' : (e == 't') ? '\t' : e;
+          j += 2;
+        } else {
+          val += s[j++];
+        }
+      }
+      if (j >= s.size()) parse_error(line, col, "unterminated string");
+      out.push_back({Token::kString, val, line, col});
+      i = j + 1;
+      continue;
+    }
+    if (isdig(c) || c == '.' || c == '-' || c == '+') {
+      size_t j = i;
+      if (s[j] == '-' || s[j] == '+') ++j;
+      size_t digits = 0;
+      while (j < s.size() && isdig(s[j])) { ++j; ++digits; }
+      if (j < s.size() && s[j] == '.') {
+        ++j;
+        while (j < s.size() && isdig(s[j])) { ++j; ++digits; }
+      }
+      if (digits == 0) parse_error(line, col, std::string("unexpected character '") + c + "'");
+      if (j < s.size() && (s[j] == 'e' || s[j] == 'E')) {
+        size_t k = j + 1;
+        if (k < s.size() && (s[k] == '-' || s[k] == '+')) ++k;
+        if (k < s.size() && isdig(s[k])) {
+          while (k < s.size() && isdig(s[k])) ++k;
+          j = k;
+        }
+      }
+      out.push_back({Token::kNumber, s.substr(i, j - i), line, col});
+      i = j;
+      continue;
+    }
+    if ((c >= 'a' && c <= 'z') || (c >= 'A' && c <= 'Z') || c == '_') {
+      size_t j = i;
+      while (j < s.size() && ((s[j] >= 'a' && s[j] <= 'z') || (s[j] >= 'A' && s[j] <= 'Z') || s[j] == '_' ||
+                              isdig(s[j])))
+        ++j;
+      out.push_back({Token::kName, s.substr(i, j - i), line, col});
+      i = j;
+      continue;
+    }
+    parse_error(line, col, std::string("unexpected character '") + c + "'");
+  }
+  out.push_back({Token::kEof, "", line, int(s.size() - line_start) + 1});
+  return out;
+}
+
+struct Parser {
+  std::vector<Token> t;
+  size_t i = 0;
+  std::vector<Node> block(bool top) {
+    std::vector<Node> out;
+    for (;;) {
+      const Token& k = t[i];
+      if (k.kind == Token::kEof) {
+        if (!top) parse_error(k.line, k.col, "unexpected end of input: missing '}'");
+        return out;
+      }
+      if (k.kind == Token::kPunct && k.text == "}") {
+        if (top) parse_error(k.line, k.col, "unbalanced '}'");
+        ++i;
+        return out;
+      }
+      if (k.kind != Token::kName) parse_error(k.line, k.col, "expected field name, got '" + k.text + "'");
+      Node n;
+      n.name = k.text;
+      n.line = k.line;
+      n.col = k.col;
+      ++i;
+      const Token* v = &t[i];
+      bool colon = v->kind == Token::kPunct && v->text == ":";
+      if (colon) v = &t[++i];
+      if (v->kind == Token::kPunct && v->text == "{") {
+        ++i;
+        n.kind = Node::kMsg;
+        n.children = block(false);
+      } else if (!colon) {
+        parse_error(v->line, v->col, "expected ':' or '{' after '" + n.name + "'");
+      } else if (v->kind == Token::kNumber) {
+        n.kind = Node::kNum;
+        n.num = std::strtod(v->text.c_str(), nullptr);
+        ++i;
+      } else if (v->kind == Token::kString) {
+        n.kind = Node::kStr;
+        n.str = v->text;
+        ++i;
+      } else if (v->kind == Token::kName) {
+        n.kind = Node::kIdent;
+        n.str = v->text;
+        ++i;
+      } else {
+        parse_error(v->line, v->col, "expected value after ':', got '" + v->text + "'");
+      }
+      out.push_back(std::move(n));
+    }
+  }
+};
+
+[[noreturn]] void invalid(const std::string& path, const std::string& msg, brax_status st = BRAX_E_VALIDATION) {
+  throw Error(st, path + ": " + msg);
+}
+
+// Field access with schema checking.
+struct Fields {
+  std::map<std::string, std::vector<const Node*>> by;
+  std::string path;
+  Fields(const std::vector<Node>& nodes, const std::string& p, std::initializer_list<const char*> allowed)
+      : path(p) {
+    std::set<std::string> ok(allowed.begin(), allowed.end());
+    for (const Node& n : nodes) {
+      if (!ok.count(n.name)) invalid(path + "." + n.name, "unknown field");
+      by[n.name].push_back(&n);
+    }
+  }
+  const Node* one(const std::string& key) const {
+    auto it = by.find(key);
+    if (it == by.end()) return nullptr;
+    if (it->second.size() > 1) invalid(path + "." + key, "field given more than once");
+    return it->second[0];
+  }
+  double num(const std::string& key, double dflt) const {
+    const Node* n = one(key);
+    if (!n) return dflt;
+    if (n->kind != Node::kNum) invalid(path + "." + key, "expected a number");
+    return n->num;
+  }
+  std::string str(const std::string& key, bool* present = nullptr) const {
+    const Node* n = one(key);
+    if (present) *present = n != nullptr;
+    if (!n) return "";
+    if (n->kind != Node::kStr) invalid(path + "." + key, "expected a string");
+    return n->str;
+  }
+  const std::vector<Node>* msg(const std::string& key) const {
+    const Node* n = one(key);
+    if (!n) return nullptr;
+    if (n->kind != Node::kMsg) invalid(path + "." + key, "expected a { } block");
+    return &n->children;
+  }
+  std::vector<const Node*> all(const std::string& key) const {
+    auto it = by.find(key);
+    return it == by.end() ? std::vector<const Node*>{} : it->second;
+  }
+  bool has(const std::string& key) const { return by.count(key) > 0; }
+};
+
+void vec3(const std::vector<Node>* node, const std::string& path, double out[3]) {
+  if (!node) return;
+  for (const Node& n : *node) {
+    if ((n.name != "x" && n.name != "y" && n.name != "z") || n.kind != Node::kNum)
+      invalid(path + "." + n.name, "expected x/y/z numbers");
+    out[n.name[0] - 'x'] = n.num;
+  }
+}
+
+void qmul(const double a[4], const double b[4], double out[4]) {
+  double r[4] = {a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3],
+                 a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2],
+                 a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1],
+                 a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0]};
+  for (int i = 0; i < 4; ++i) out[i] = r[i];
+}
+
+void euler_field(const std::vector<Node>* node, const std::string& path, double q[4]) {
+  double deg[3] = {0, 0, 0};
+  vec3(node, path, deg);
+  euler_deg_to_quat(deg, q);
+}
+
+std::string idx(const char* what, size_t i) { return std::string(what) + "[" + std::to_string(i) + "]"; }
+
+}  // namespace
+
+void euler_deg_to_quat(const double deg[3], double q[4]) {
+  const double k = M_PI / 180.0;
+  double qx[4] = {std::cos(deg[0] * k / 2), std::sin(deg[0] * k / 2), 0, 0};
+  double qy[4] = {std::cos(deg[1] * k / 2), 0, std::sin(deg[1] * k / 2), 0};
+  double qz[4] = {std::cos(deg[2] * k / 2), 0, 0, std::sin(deg[2] * k / 2)};
+  double t[4];
+  qmul(qx, qy, t);
+  qmul(t, qz, q);
+}
+
+Config parse_config(const std::string& text) {
+  Parser p{tokenize(text)};
+  std::vector<Node> root = p.block(true);
+  Fields top(root, "config", {"dt", "substeps", "gravity", "friction", "elasticity", "baumgarte_erp", "bodies",
+                              "joints", "actuators", "collide_include", "defaults"});
+  Config c;
+  c.dt = top.num("dt", 0.01);
+  double sub = top.num("substeps", 1.0);
+  if (!(c.dt > 0)) invalid("config.dt", "must be > 0");
+  if (sub != std::floor(sub) || sub < 1) invalid("config.substeps", "must be a positive integer");
+  c.substeps = int(sub);
+  vec3(top.msg("gravity"), "config.gravity", c.gravity);
+  c.friction = top.num("friction", 1.0);
+  c.elasticity = top.num("elasticity", 0.0);
+  c.baumgarte = top.num("baumgarte_erp", 0.2);
+  if (c.friction < 0) invalid("config.friction", "must be >= 0");
+  if (!(c.elasticity >= 0 && c.elasticity <= 1)) invalid("config.elasticity", "must be in [0, 1]");
+  if (!(c.baumgarte > 0 && c.baumgarte <= 1)) invalid("config.baumgarte_erp", "must be in (0, 1]");
+
+  std::map<std::string, int> body_ix;
+  auto bnodes = top.all("bodies");
+  for (size_t bi = 0; bi < bnodes.size(); ++bi) {
+    std::string path = idx("bodies", bi);
+    if (bnodes[bi]->kind != Node::kMsg) invalid(path, "expected a { } block");
+    Fields bf(bnodes[bi]->children, path, {"name", "mass", "inertia", "frozen", "colliders"});
+    Body b;
+    bool has_name = false;
+    b.name = bf.str("name", &has_name);
+    if (!has_name) invalid(path + ".name", "required");
+    if (body_ix.count(b.name)) invalid(path + ".name", "duplicate body name '" + b.name + "'");
+    body_ix[b.name] = int(bi);
+    b.mass = bf.num("mass", 1.0);
+    if (!(b.mass > 0)) invalid(path + ".mass", "must be > 0");
+    vec3(bf.msg("inertia"), path + ".inertia", b.inertia);
+    for (double v : b.inertia)
+      if (!(v > 0)) invalid(path + ".inertia", "must be > 0");
+    if (const std::vector<Node>* fz = bf.msg("frozen")) {
+      Fields ff(*fz, path + ".frozen", {"position", "rotation", "all"});
+      if (const Node* a = ff.one("all")) {
+        if (a->kind == Node::kIdent && a->str == "true")
+          for (int k = 0; k < 3; ++k) b.frozen_pos[k] = b.frozen_rot[k] = 1;
+      }
+      double fp[3] = {0, 0, 0}, fr[3] = {0, 0, 0};
+      vec3(ff.msg("position"), path + ".frozen.position", fp);
+      vec3(ff.msg("rotation"), path + ".frozen.rotation", fr);
+      for (int k = 0; k < 3; ++k) {
+        if ((fp[k] != 0 && fp[k] != 1) || (fr[k] != 0 && fr[k] != 1))
+          invalid(path + ".frozen", "axis flags must be 0 or 1");
+        b.frozen_pos[k] = std::max(b.frozen_pos[k], fp[k]);
+        b.frozen_rot[k] = std::max(b.frozen_rot[k], fr[k]);
+      }
+    }
+    auto cnodes = bf.all("colliders");
+    for (size_t ci = 0; ci < cnodes.size(); ++ci) {
+      std::string cpath = path + "." + idx("colliders", ci);
+      if (cnodes[ci]->kind != Node::kMsg) invalid(cpath, "expected a { } block");
+      Fields cf(cnodes[ci]->children, cpath, {"position", "rotation", "sphere", "capsule", "box", "plane"});
+      int nshape = cf.has("sphere") + cf.has("capsule") + cf.has("box") + cf.has("plane");
+      if (nshape != 1) invalid(cpath, "exactly one of sphere/capsule/box/plane required");
+      Collider col;
+      col.body = int(bi);
+      vec3(cf.msg("position"), cpath + ".position", col.pos);
+      euler_field(cf.msg("rotation"), cpath + ".rotation", col.rot);
+      if (cf.has("sphere")) {
+        Fields sf(*cf.msg("sphere"), cpath + ".sphere", {"radius"});
+        col.kind = kSphere;
+        col.radius = sf.num("radius", 0);
+        if (!(col.radius > 0)) invalid(cpath + ".sphere.radius", "must be > 0");
+      } else if (cf.has("capsule")) {
+        Fields sf(*cf.msg("capsule"), cpath + ".capsule", {"radius", "length", "end"});
+        col.kind = kCapsule;
+        col.radius = sf.num("radius", 0);
+        col.length = sf.num("length", 0);
+        double end = sf.num("end", 0);
+        if (!(col.radius > 0)) invalid(cpath + ".capsule.radius", "must be > 0");
+        if (!(col.length >= 2 * col.radius)) invalid(cpath + ".capsule.length", "must be >= 2*radius");
+        if (end != 0 && end != 1 && end != -1) invalid(cpath + ".capsule.end", "must be -1, 0 or 1");
+        col.end = int(end);
+      } else if (cf.has("box")) {
+        Fields sf(*cf.msg("box"), cpath + ".box", {"halfsize"});
+        col.kind = kBox;
+        vec3(sf.msg("halfsize"), cpath + ".box.halfsize", col.halfsize);
+        for (double v : col.halfsize)
+          if (!(v > 0)) invalid(cpath + ".box.halfsize", "must be > 0");
+      } else {
+        Fields sf(*cf.msg("plane"), cpath + ".plane", {});
+        col.kind = kPlane;
+      }
+      c.colliders.push_back(col);
+    }
+    c.bodies.push_back(b);
+  }
+  if (c.bodies.empty()) invalid("config.bodies", "no bodies");
+
+  auto dnodes = top.all("defaults");
+  for (size_t di = 0; di < dnodes.size(); ++di) {
+    std::string dpath = idx("defaults", di);
+    Fields df(dnodes[di]->children, dpath, {"qps"});
+    auto qn = df.all("qps");
+    for (size_t qi = 0; qi < qn.size(); ++qi) {
+      std::string qpath = dpath + "." + idx("qps", qi);
+      Fields qf(qn[qi]->children, qpath, {"name", "pos", "rot"});
+      std::string nm = qf.str("name");
+      if (!body_ix.count(nm)) invalid(qpath + ".name", "unknown body '" + nm + "'");
+      Body& b = c.bodies[body_ix[nm]];
+      b.init_pos[0] = b.init_pos[1] = b.init_pos[2] = 0;
+      vec3(qf.msg("pos"), qpath + ".pos", b.init_pos);
+      euler_field(qf.msg("rot"), qpath + ".rot", b.init_rot);
+    }
+  }
+
+  std::map<std::string, int> joint_ix;
+  auto jnodes = top.all("joints");
+  for (size_t ji = 0; ji < jnodes.size(); ++ji) {
+    std::string path = idx("joints", ji);
+    Fields jf(jnodes[ji]->children, path,
+              {"name", "parent", "child", "stiffness", "spring_damping", "angular_damping", "limit_stiffness",
+               "angular_stiffness", "parent_offset", "child_offset", "rotation", "reference_rotation",
+               "angle_limit"});
+    Joint j;
+    bool has_name = false;
+    j.name = jf.str("name", &has_name);
+    if (!has_name) invalid(path + ".name", "required");
+    if (joint_ix.count(j.name)) invalid(path + ".name", "duplicate joint name '" + j.name + "'");
+    joint_ix[j.name] = int(ji);
+    std::string pn = jf.str("parent"), cn = jf.str("child");
+    if (!body_ix.count(pn)) invalid(path + ".parent", "unknown body '" + pn + "'");
+    if (!body_ix.count(cn)) invalid(path + ".child", "unknown body '" + cn + "'");
+    if (pn == cn) invalid(path + ".child", "parent and child must differ");
+    j.parent = body_ix[pn];
+    j.child = body_ix[cn];
+    j.stiffness = jf.num("stiffness", 0);
+    if (!(j.stiffness > 0)) invalid(path + ".stiffness", "must be > 0");
+    j.spring_damping = jf.num("spring_damping", 0);
+    j.angular_damping = jf.num("angular_damping", 0);
+    j.limit_stiffness = jf.num("limit_stiffness", j.stiffness);    // R8
+    j.angular_stiffness = jf.num("angular_stiffness", j.stiffness);
+    vec3(jf.msg("parent_offset"), path + ".parent_offset", j.parent_offset);
+    vec3(jf.msg("child_offset"), path + ".child_offset", j.child_offset);
+    euler_field(jf.msg("rotation"), path + ".rotation", j.rotation);
+    euler_field(jf.msg("reference_rotation"), path + ".reference_rotation", j.reference_rotation);
+    auto lnodes = jf.all("angle_limit");
+    for (size_t li = 0; li < lnodes.size(); ++li) {
+      std::string lpath = path + "." + idx("angle_limit", li);
+      Fields lf(lnodes[li]->children, lpath, {"min", "max"});
+      double lo = lf.num("min", 0), hi = lf.num("max", 0);
+      if (lo > hi) invalid(lpath, "min > max");
+      if (lo < -180 || hi > 180) invalid(lpath, "limits must lie in [-180, 180] degrees (R9)");
+      if (li < 3) {
+        j.lo[li] = lo * M_PI / 180.0;
+        j.hi[li] = hi * M_PI / 180.0;
+      }
+    }
+    if (lnodes.size() > 3) invalid(path + ".angle_limit", "at most 3 (dof <= 3)");
+    j.dof = int(lnodes.size());
+    const char* nonneg[] = {"spring_damping", "angular_damping", "limit_stiffness", "angular_stiffness"};
+    double vals[] = {j.spring_damping, j.angular_damping, j.limit_stiffness, j.angular_stiffness};
+    for (int k = 0; k < 4; ++k)
+      if (vals[k] < 0) invalid(path + "." + nonneg[k], "must be >= 0");
+    c.joints.push_back(j);
+  }
+
+  // forest: every body is the child of at most one joint, no cycles
+  std::vector<int> parent_of(c.bodies.size(), -1);
+  for (size_t ji = 0; ji < c.joints.size(); ++ji) {
+    int ch = c.joints[ji].child;
+    if (parent_of[ch] >= 0) invalid(idx("joints", ji) + ".child", "body is already the child of another joint");
+    parent_of[ch] = c.joints[ji].parent;
+  }
+  for (size_t b = 0; b < c.bodies.size(); ++b) {
+    size_t steps = 0;
+    for (int x = int(b); parent_of[x] >= 0; x = parent_of[x])
+      if (++steps > c.bodies.size()) invalid(idx("bodies", b), "cyclic joint graph", BRAX_E_CYCLIC_JOINT_GRAPH);
+  }
+
+  auto anodes = top.all("actuators");
+  std::set<int> actuated;
+  for (size_t ai = 0; ai < anodes.size(); ++ai) {
+    std::string path = idx("actuators", ai);
+    Fields af(anodes[ai]->children, path, {"name", "joint", "strength", "torque", "angle"});
+    Actuator a;
+    a.name = af.str("name");
+    std::string jn = af.str("joint");
+    if (!joint_ix.count(jn)) invalid(path + ".joint", "unknown joint '" + jn + "'");
+    if (af.has("torque") + af.has("angle") != 1) invalid(path, "exactly one of torque/angle required");
+    a.joint = joint_ix[jn];
+    if (actuated.count(a.joint)) invalid(path + ".joint", "joint already has an actuator");
+    if (c.joints[a.joint].dof == 0) invalid(path + ".joint", "actuated joint must have dof >= 1");
+    actuated.insert(a.joint);
+    a.strength = af.num("strength", 0);
+    a.kind = af.has("torque") ? kTorque : kAngle;
+    a.act_offset = c.act_dim;
+    c.act_dim += c.joints[a.joint].dof;
+    Joint& j = c.joints[a.joint];
+    j.act_kind = a.kind;
+    j.act_strength = a.strength;
+    j.act_offset = a.act_offset;
+    c.actuators.push_back(a);
+  }
+
+  // ---- pairs (naive pairwise collision; enumeration rule R19) ----
+  struct Cand { int i, j; std::string path; };
+  std::vector<Cand> cand;
+  auto inodes = top.all("collide_include");
+  if (!inodes.empty()) {
+    for (size_t ii = 0; ii < inodes.size(); ++ii) {
+      std::string path = idx("collide_include", ii);
+      Fields f(inodes[ii]->children, path, {"first", "second"});
+      std::string a = f.str("first"), b = f.str("second");
+      if (!body_ix.count(a)) invalid(path + ".first", "unknown body '" + a + "'");
+      if (!body_ix.count(b)) invalid(path + ".second", "unknown body '" + b + "'");
+      int ba = body_ix[a], bb = body_ix[b];
+      if (ba == bb) invalid(path, "a body cannot collide with itself");
+      if (c.bodies[ba].is_static() && c.bodies[bb].is_static()) invalid(path, "static-static pair");
+      for (size_t i = 0; i < c.colliders.size(); ++i)
+        if (c.colliders[i].body == ba)
+          for (size_t j = 0; j < c.colliders.size(); ++j)
+            if (c.colliders[j].body == bb) cand.push_back({int(i), int(j), path});
+    }
+  } else {
+    std::set<std::pair<int, int>> jointed;
+    for (const Joint& j : c.joints) {
+      jointed.insert({j.parent, j.child});
+      jointed.insert({j.child, j.parent});
+    }
+    for (size_t i = 0; i < c.colliders.size(); ++i)
+      for (size_t j = i + 1; j < c.colliders.size(); ++j) {
+        int bi = c.colliders[i].body, bj = c.colliders[j].body;
+        if (bi == bj || jointed.count({bi, bj})) continue;
+        if (c.bodies[bi].is_static() && c.bodies[bj].is_static()) continue;
+        cand.push_back({int(i), int(j), "colliders[" + std::to_string(i) + "]x[" + std::to_string(j) + "]"});
+      }
+  }
+  static const char* kind_name[] = {"sphere", "capsule", "box", "plane"};
+  for (const Cand& cd : cand) {
+    int a = cd.i, b = cd.j;
+    int ka = c.colliders[a].kind, kb = c.colliders[b].kind;  // enum order = orientation rank
+    if (ka > kb || (ka == kb && a > b)) { std::swap(a, b); std::swap(ka, kb); }
+    int type = -1;
+    if (kb == kPlane) type = (ka == kSphere) ? BRAX_SLOT_SPHERE_PLANE : (ka == kCapsule) ? BRAX_SLOT_CAPSULE_PLANE
+                                            : (ka == kBox) ? BRAX_SLOT_BOX_PLANE : -1;
+    else if (ka == kSphere && kb == kSphere) type = BRAX_SLOT_SPHERE_SPHERE;
+    else if (ka == kSphere && kb == kCapsule) type = BRAX_SLOT_SPHERE_CAPSULE;
+    else if (ka == kCapsule && kb == kCapsule) type = BRAX_SLOT_CAPSULE_CAPSULE;
+    if (type < 0)
+      invalid(cd.path, std::string("unsupported collider pair ") + kind_name[ka] + "-" + kind_name[kb],
+              BRAX_E_UNSUPPORTED_PAIR);
+    c.pairs.push_back({a, b, type});
+  }
+  for (size_t pi = 0; pi < c.pairs.size(); ++pi) {
+    const Pair& pr = c.pairs[pi];
+    const Collider& A = c.colliders[pr.col_a];
+    int first = 0, count = 1;
+    if (pr.type == BRAX_SLOT_CAPSULE_PLANE) {
+      if (A.end == 0) count = 2;
+      else first = (A.end == 1) ? 0 : 1;
+    } else if (pr.type == BRAX_SLOT_BOX_PLANE) {
+      count = 8;
+    }
+    for (int k = 0; k < count; ++k)
+      c.slots.push_back({int(pi), pr.type, A.body, c.colliders[pr.col_b].body, pr.col_a, pr.col_b, first + k});
+  }
+  if (c.slots.size() > 255) invalid("config", "more than 255 contact slots");
+  return c;
+}
+
+}  // namespace brax

@@ -1,0 +1,330 @@
+// system.cpp — builds the device tables, the warp work plan, default_qp and the
+// stability lint for a parsed config (brax_system_create).
+#include "system.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <sstream>
+
+namespace brax {
+namespace {
+
+void qmul(const double a[4], const double b[4], double o[4]) {
+  double r[4] = {a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3],
+                 a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2],
+                 a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1],
+                 a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0]};
+  std::memcpy(o, r, sizeof r);
+}
+void qconj(const double q[4], double o[4]) { o[0] = q[0]; o[1] = -q[1]; o[2] = -q[2]; o[3] = -q[3]; }
+void qrot(const double q[4], const double v[3], double o[3]) {
+  // v + w·t + u×t, t = 2 u×v
+  double t[3] = {2 * (q[2] * v[2] - q[3] * v[1]), 2 * (q[3] * v[0] - q[1] * v[2]), 2 * (q[1] * v[1] - q[2] * v[0])};
+  double r[3] = {v[0] + q[0] * t[0] + (q[2] * t[2] - q[3] * t[1]),
+                 v[1] + q[0] * t[1] + (q[3] * t[0] - q[1] * t[2]),
+                 v[2] + q[0] * t[2] + (q[1] * t[1] - q[2] * t[0])};
+  std::memcpy(o, r, sizeof r);
+}
+
+template <class T>
+int32_t push_struct(std::vector<uint32_t>& blob, const T& v) {
+  static_assert(sizeof(T) % 4 == 0, "word struct");
+  int32_t off = int32_t(blob.size());
+  blob.resize(blob.size() + sizeof(T) / 4);
+  std::memcpy(blob.data() + off, &v, sizeof(T));
+  return off;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) throw Error(BRAX_E_OUT_OF_MEMORY, std::string(what) + ": out of memory");
+  if (e != cudaSuccess) throw Error(BRAX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+System::~System() {
+  if (d_blob) cudaFree(d_blob);
+  if (d_default_qp) cudaFree(d_default_qp);
+  if (d_masks) cudaFree(d_masks);
+}
+
+void default_qp(const Config& cfg, std::vector<double>& pos, std::vector<double>& rot) {
+  // Roots at their defaults; children placed joint by joint (config order,
+  // repeated until all are placed) so that the joint-frame relative rotation is
+  // E(θ⁰), θ⁰_i = clamp(0, lo_i, hi_i), and the two anchors coincide.
+  const size_t B = cfg.bodies.size();
+  pos.assign(3 * B, 0.0);
+  rot.assign(4 * B, 0.0);
+  std::vector<char> placed(B, 0), is_child(B, 0);
+  for (const Joint& j : cfg.joints) is_child[j.child] = 1;
+  for (size_t b = 0; b < B; ++b)
+    if (!is_child[b]) {
+      std::memcpy(&pos[3 * b], cfg.bodies[b].init_pos, 3 * sizeof(double));
+      std::memcpy(&rot[4 * b], cfg.bodies[b].init_rot, 4 * sizeof(double));
+      placed[b] = 1;
+    }
+  for (bool progress = true; progress;) {
+    progress = false;
+    for (const Joint& j : cfg.joints) {
+      if (!placed[j.parent] || placed[j.child]) continue;
+      double th[3] = {0, 0, 0};
+      for (int i = 0; i < j.dof; ++i) th[i] = std::min(std::max(0.0, j.lo[i]), j.hi[i]) * 180.0 / M_PI;
+      double E[4], Jc[4], t1[4], t2[4], t3[4], qc[4];
+      euler_deg_to_quat(th, E);
+      qconj(j.rotation, Jc);
+      const double* qp = &rot[4 * j.parent];
+      qmul(qp, j.rotation, t1);
+      qmul(t1, E, t2);
+      qmul(t2, Jc, t3);
+      qmul(t3, j.reference_rotation, qc);
+      std::memcpy(&rot[4 * j.child], qc, sizeof qc);
+      double rp[3], rc[3];
+      qrot(qp, j.parent_offset, rp);
+      qrot(qc, j.child_offset, rc);
+      for (int k = 0; k < 3; ++k) pos[3 * j.child + k] = pos[3 * j.parent + k] + rp[k] - rc[k];
+      placed[j.child] = 1;
+      progress = true;
+    }
+  }
+}
+
+System* build_system(const Config& cfg, int device) {
+  std::unique_ptr<System> s(new System());
+  s->cfg = cfg;
+  s->device = device;
+  const int B = int(cfg.bodies.size()), J = int(cfg.joints.size()), C = int(cfg.slots.size());
+  const double h = cfg.dt / cfg.substeps;
+
+  // ---- stability lint (R6) ----
+  for (int ji = 0; ji < J; ++ji) {
+    const Joint& j = cfg.joints[ji];
+    double w = 0;
+    const double* offs[2] = {j.parent_offset, j.child_offset};
+    int bs[2] = {j.parent, j.child};
+    for (int k = 0; k < 2; ++k) {
+      const Body& b = cfg.bodies[bs[k]];
+      if (b.is_static()) continue;
+      double imin = std::min(b.inertia[0], std::min(b.inertia[1], b.inertia[2]));
+      double o2 = offs[k][0] * offs[k][0] + offs[k][1] * offs[k][1] + offs[k][2] * offs[k][2];
+      w += 1.0 / b.mass + o2 / imin;
+    }
+    std::ostringstream os;
+    if (j.stiffness * w * h * h >= 3.6) {
+      os << "joints[" << ji << "]: stiffness*w*h^2 = " << j.stiffness * w * h * h << " >= 3.6";
+      s->lint.push_back(os.str());
+    }
+    if (j.spring_damping * w * h >= 1.8) {
+      std::ostringstream o2s;
+      o2s << "joints[" << ji << "]: spring_damping*w*h = " << j.spring_damping * w * h << " >= 1.8";
+      s->lint.push_back(o2s.str());
+    }
+  }
+
+  // ---- default_qp ----
+  std::vector<double> dpos, drot;
+  default_qp(cfg, dpos, drot);
+  s->dqp_pos.assign(dpos.begin(), dpos.end());
+  s->dqp_rot.assign(drot.begin(), drot.end());
+  s->dqp_vel.assign(3 * B, 0.f);
+  s->dqp_ang.assign(3 * B, 0.f);
+
+  // ---- tables ----
+  std::vector<uint32_t>& blob = s->blob;
+  DHeader& hd = s->hd;
+  hd.B = B;
+  hd.J = J;
+  hd.C = C;
+  hd.A = cfg.act_dim;
+  hd.S = cfg.substeps;
+  hd.h = float(h);
+  hd.beta_over_h = float(cfg.baumgarte / h);
+  hd.mu = float(cfg.friction);
+  hd.e = float(cfg.elasticity);
+  for (int k = 0; k < 3; ++k) hd.g[k] = float(cfg.gravity[k]);
+
+  std::vector<DBody> bodies(B);
+  std::vector<int> dyn;
+  for (int b = 0; b < B; ++b) {
+    const Body& src = cfg.bodies[b];
+    DBody& d = bodies[b];
+    d.inv_mass = float(1.0 / src.mass);
+    for (int k = 0; k < 3; ++k) {
+      d.inv_inertia[k] = float(1.0 / src.inertia[k]);
+      d.mpos[k] = float(1.0 - src.frozen_pos[k]);
+      d.mrot[k] = float(1.0 - src.frozen_rot[k]);
+    }
+    d.is_static = src.is_static() ? 1 : 0;
+    d.rot_frozen = src.rot_frozen() ? 1 : 0;
+    if (!d.is_static) dyn.push_back(b);
+  }
+  s->n_dynamic = int(dyn.size());
+  hd.off_bodies = int32_t(blob.size());
+  for (const DBody& d : bodies) push_struct(blob, d);
+
+  hd.off_joints = int32_t(blob.size());
+  for (const Joint& j : cfg.joints) {
+    DJoint d{};
+    d.parent = j.parent;
+    d.child = j.child;
+    d.dof = j.dof;
+    d.act_kind = j.act_kind;
+    d.act_offset = j.act_offset;
+    double jc[4], rc[4];
+    qconj(j.reference_rotation, rc);
+    qmul(rc, j.rotation, jc);
+    for (int k = 0; k < 3; ++k) {
+      d.o_p[k] = float(j.parent_offset[k]);
+      d.o_c[k] = float(j.child_offset[k]);
+      d.lo[k] = float(j.lo[k]);
+      d.hi[k] = float(j.hi[k]);
+    }
+    for (int k = 0; k < 4; ++k) {
+      d.jp[k] = float(j.rotation[k]);
+      d.jc[k] = float(jc[k]);
+    }
+    d.k = float(j.stiffness);
+    d.c_l = float(j.spring_damping);
+    d.c_a = float(j.angular_damping);
+    d.k_l = float(j.limit_stiffness);
+    d.k_a = float(j.angular_stiffness);
+    d.strength = float(j.act_strength);
+    push_struct(blob, d);
+  }
+
+  hd.off_slots = int32_t(blob.size());
+  for (const Slot& sl : cfg.slots) {
+    DSlot d{};
+    const Collider& A = cfg.colliders[sl.col_a];
+    const Collider& Bc = cfg.colliders[sl.col_b];
+    d.type = sl.type;
+    d.a = sl.a;
+    d.b = sl.b;
+    d.point = sl.point;
+    d.a_static = bodies[sl.a].is_static;
+    d.b_static = bodies[sl.b].is_static;
+    for (int k = 0; k < 3; ++k) {
+      d.ca_pos[k] = float(A.pos[k]);
+      d.cb_pos[k] = float(Bc.pos[k]);
+      d.hs[k] = float(A.halfsize[k]);
+      d.inv_inertia_a[k] = bodies[sl.a].inv_inertia[k];
+      d.inv_inertia_b[k] = bodies[sl.b].inv_inertia[k];
+    }
+    for (int k = 0; k < 4; ++k) {
+      d.ca_rot[k] = float(A.rot[k]);
+      d.cb_rot[k] = float(Bc.rot[k]);
+    }
+    d.ra = float(A.radius);
+    d.rb = float(Bc.radius);
+    d.ella = float(0.5 * A.length - A.radius);
+    d.ellb = float(0.5 * Bc.length - Bc.radius);
+    d.inv_mass_a = bodies[sl.a].inv_mass;
+    d.inv_mass_b = bodies[sl.b].inv_mass;
+    push_struct(blob, d);
+  }
+
+  // ---- warp work plan: W warps per block, lane = env ----
+  int W = std::max(1, std::min(kMaxWarps, int(dyn.size())));
+  if (const char* env = std::getenv("BRAX_WARPS_PER_BLOCK")) {
+    int v = std::atoi(env);
+    if (v >= 1 && v <= kMaxWarps) W = v;
+  }
+  hd.W = W;
+  // items: longest-processing-time-first over estimated costs (joint ≈ 5, contact ≈ 3)
+  std::vector<int> items(J + C);
+  std::iota(items.begin(), items.end(), 0);
+  auto cost = [&](int it) { return it < J ? 5 : 3; };
+  std::stable_sort(items.begin(), items.end(), [&](int a, int b) { return cost(a) > cost(b); });
+  std::vector<std::vector<int>> per_warp(W);
+  std::vector<int> load(W, 0);
+  for (int it : items) {
+    int w = int(std::min_element(load.begin(), load.end()) - load.begin());
+    per_warp[w].push_back(it);
+    load[w] += cost(it);
+  }
+  hd.off_item_begin = int32_t(blob.size());
+  int acc = 0;
+  for (int w = 0; w <= W; ++w) {
+    blob.push_back(uint32_t(acc));
+    if (w < W) acc += int(per_warp[w].size());
+  }
+  hd.off_items = int32_t(blob.size());
+  for (int w = 0; w < W; ++w) {
+    std::sort(per_warp[w].begin(), per_warp[w].end());  // joints first, then slots
+    for (int it : per_warp[w]) blob.push_back(uint32_t(it));
+  }
+  // dynamic bodies round-robin over warps
+  std::vector<std::vector<int>> wb(W);
+  for (size_t i = 0; i < dyn.size(); ++i) wb[i % W].push_back(dyn[i]);
+  hd.off_body_begin = int32_t(blob.size());
+  acc = 0;
+  for (int w = 0; w <= W; ++w) {
+    blob.push_back(uint32_t(acc));
+    if (w < W) acc += int(wb[w].size());
+  }
+  hd.off_bodies_of_warp = int32_t(blob.size());
+  for (int w = 0; w < W; ++w)
+    for (int b : wb[w]) blob.push_back(uint32_t(b));
+  // incidence lists: joints by index (child / parent role), then slots by index (A / B role)
+  std::vector<std::vector<int32_t>> inc(B);
+  for (int j = 0; j < J; ++j) {
+    inc[cfg.joints[j].child].push_back(inc_pack(kIncJointChild, j));
+    inc[cfg.joints[j].parent].push_back(inc_pack(kIncJointParent, j));
+  }
+  for (int c = 0; c < C; ++c) {
+    inc[cfg.slots[c].a].push_back(inc_pack(kIncSlotA, c));
+    inc[cfg.slots[c].b].push_back(inc_pack(kIncSlotB, c));
+  }
+  hd.off_inc_begin = int32_t(blob.size());
+  acc = 0;
+  for (int b = 0; b <= B; ++b) {
+    blob.push_back(uint32_t(acc));
+    if (b < B) acc += int(inc[b].size());
+  }
+  hd.off_inc = int32_t(blob.size());
+  for (int b = 0; b < B; ++b)
+    for (int32_t e : inc[b]) blob.push_back(uint32_t(e));
+  while (blob.size() % 4) blob.push_back(0);
+  hd.blob_words = int32_t(blob.size());
+  auto magic = [](uint32_t d) -> uint32_t { return d ? uint32_t(((uint64_t(1) << 32) + d - 1) / d) : 0; };
+  hd.row_magic[0] = magic(uint32_t(3 * B));
+  hd.row_magic[1] = magic(uint32_t(4 * B));
+  hd.row_magic[2] = magic(uint32_t(std::max(1, cfg.act_dim)));
+  hd.row_magic[3] = 0;
+
+  s->smem_bytes = size_t(hd.blob_words) * 4 +
+                  size_t(kEnvsPerBlock) * 4 * (size_t(B) * kQPFields + size_t(J) * kJointOut +
+                                               size_t(C) * kSlotOut + size_t(hd.A) + size_t(C) + 1);
+  if (s->smem_bytes > 227 * 1024)
+    throw Error(BRAX_E_VALIDATION, "config: system too large for one block's shared memory (" +
+                                       std::to_string(s->smem_bytes) + " bytes)");
+
+  // ---- upload ----
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaMalloc(&s->d_blob, blob.size() * 4), "cudaMalloc(blob)");
+  cuda_check(cudaMemcpy(s->d_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy(blob)");
+  std::vector<float> dq(7 * size_t(B));
+  for (int b = 0; b < B; ++b) {
+    for (int k = 0; k < 3; ++k) dq[3 * b + k] = s->dqp_pos[3 * b + k];
+    for (int k = 0; k < 4; ++k) dq[3 * B + 4 * b + k] = s->dqp_rot[4 * b + k];
+  }
+  cuda_check(cudaMalloc(&s->d_default_qp, dq.size() * 4), "cudaMalloc(default_qp)");
+  cuda_check(cudaMemcpy(s->d_default_qp, dq.data(), dq.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+  s->d_masks_host.assign(7 * size_t(B), 0.f);
+  for (int b = 0; b < B; ++b) {
+    for (int k = 0; k < 3; ++k) {
+      s->d_masks_host[7 * b + k] = bodies[b].mpos[k];
+      s->d_masks_host[7 * b + 3 + k] = bodies[b].mrot[k];
+    }
+    s->d_masks_host[7 * b + 6] = float(bodies[b].is_static);
+  }
+  cuda_check(cudaMalloc(&s->d_masks, s->d_masks_host.size() * 4), "cudaMalloc(masks)");
+  cuda_check(cudaMemcpy(s->d_masks, s->d_masks_host.data(), s->d_masks_host.size() * 4, cudaMemcpyHostToDevice),
+             "cudaMemcpy(masks)");
+  return s.release();
+}
+
+}  // namespace brax

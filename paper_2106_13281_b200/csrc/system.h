@@ -1,0 +1,55 @@
+// system.h — the immutable system object behind brax_system.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "config.h"
+#include "device_tables.h"
+
+namespace brax {
+
+struct StepArgs {
+  const float *pos_in, *rot_in, *vel_in, *ang_in;
+  float *pos_out, *rot_out, *vel_out, *ang_out;
+  const float* actions;        // [n_steps][n][A] (NULL iff A == 0)
+  uint32_t* status;            // [n] or NULL
+  uint8_t* contact_active;     // [n][C] or NULL
+  int64_t n_envs;
+  int64_t n_steps;
+};
+
+struct System {
+  Config cfg;
+  int device = 0;
+  DHeader hd{};
+  std::vector<uint32_t> blob;          // host copy of the table blob
+  uint32_t* d_blob = nullptr;          // device copy
+  std::vector<float> dqp_pos, dqp_rot, dqp_vel, dqp_ang;  // default_qp, fp32, B rows
+  float* d_default_qp = nullptr;       // device: pos[B][3] rot[B][4] (vel/ang are zero)
+  std::vector<float> d_masks_host;     // per body mpos[3] mrot[3] + static flag (reset kernel)
+  float* d_masks = nullptr;
+  std::vector<std::string> lint;
+  int n_dynamic = 0;
+  size_t smem_bytes = 0;
+  ~System();
+};
+
+// Host-side construction: tables, plan, default_qp, lint, then upload.
+System* build_system(const Config& cfg, int device);
+
+// default_qp in double precision (host), B rows.
+void default_qp(const Config& cfg, std::vector<double>& pos, std::vector<double>& rot);
+
+// Kernel launchers (step.cu, reset.cu).  Return cudaSuccess or the launch error.
+cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream);
+cudaError_t launch_reset(const System& sys, float* pos, float* rot, float* vel, float* ang, int64_t n,
+                         uint64_t seed, float vel_noise, float ang_noise, cudaStream_t stream);
+
+}  // namespace brax
+
+struct brax_system {
+  brax::System* impl;
+};

@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA step (through the C ABI) vs the fp64 oracle on identical
+seeded fp32 inputs (SURVEY.md §8(d) parity protocol; tolerances from
+BASELINE.json north_star: ≤ 1e-4 max abs per step, ≤ 1e-3 over 100 steps on
+non-chaotic configs, contact indexing bit-exact outside the R23 band)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+import paper_2106_13281_b200 as bx  # noqa: E402
+
+TOL_STEP = 1e-4
+TOL_100 = 1e-3
+FIELDS = ("pos", "rot", "vel", "ang")
+SCENES = ["ball", "pendulum", "chain2", "ant", "humanoid", "halfcheetah", "grasp", "fetch"]
+_cache = {}
+
+
+def scene(name):
+    if name not in _cache:
+        text = oracle.load_scene(name)
+        _cache[name] = (oracle.Oracle(text), bx.System(text))
+    return _cache[name]
+
+
+def dev(qp):
+    return {k: torch.from_numpy(np.ascontiguousarray(qp[k], dtype=np.float32)).cuda() for k in FIELDS}
+
+
+def host(qp):
+    return {k: qp[k].cpu().numpy() for k in FIELDS}
+
+
+def gpu_step(s, qp32, act32):
+    n = qp32["pos"].shape[0]
+    qd = dev(qp32)
+    out = s.alloc_qp(n)
+    status = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    ca = torch.full((n, max(1, s.n_slots)), 255, dtype=torch.uint8, device="cuda")
+    a = torch.from_numpy(act32).cuda() if s.act_dim else None
+    s.step(qd, a, out, status=status, contact_active=ca if s.n_slots else None)
+    torch.cuda.synchronize()
+    return host(out), status.cpu().numpy().view(np.uint32), ca.cpu().numpy()[:, : s.n_slots]
+
+
+def trajectory_states(o, n, seed, T0):
+    qp = o.reset(n, seed, 0.1, 0.1)
+    if T0:
+        acts = synth.actions(seed + 1, T0, n, o.act_dim)
+        for t in range(T0):
+            qp, _ = o.step(qp, acts[t], threads=8)
+    return synth.to_f32(qp)
+
+
+def max_err(a, b, rows=None):
+    errs = {}
+    for k in FIELDS:
+        x, y = a[k], b[k]
+        if rows is not None:
+            x, y = x[rows], y[rows]
+        errs[k] = float(np.max(np.abs(x.astype(np.float64) - y))) if x.size else 0.0
+    return max(errs.values()), errs
+
+
+@pytest.mark.parametrize("name", SCENES)
+@pytest.mark.parametrize("T0", [0, 10])
+def test_single_step_parity(name, T0):
+    o, s = scene(name)
+    n = 1000 if name != "ball" else 37   # spans many 32-env blocks + a ragged tail
+    qp = trajectory_states(o, n, seed=100 + T0, T0=T0)
+    act = synth.actions(7 + T0, 1, n, o.act_dim)[0]
+    ref, ex = o.step(qp, act, threads=8)
+    got, status, ca = gpu_step(s, qp, act)
+    keep = ~ex["ambiguous"]
+    assert keep.mean() > 0.9, f"too many ambiguous envs: {(~keep).sum()}"
+    err, errs = max_err(got, ref, keep)
+    assert err <= TOL_STEP, errs
+    assert np.array_equal(ca[keep], ex["contact_active"][keep])          # integer indexing bit-exact
+    assert np.array_equal(status, ex["status"])
+    # static bodies are copied through bit for bit
+    for b, body in enumerate(o.sys.bodies):
+        if body.is_static:
+            for k in FIELDS:
+                assert np.array_equal(got[k][:, b], qp[k][:, b])
+
+
+@pytest.mark.parametrize("name,n", [("ant", 8192), ("humanoid", 4096), ("halfcheetah", 4096),
+                                    ("grasp", 2048), ("fetch", 2048)])
+def test_full_size_sampled_parity(name, n):
+    """At BASELINE.json sizes in the bench launch shape: the GPU steps the whole
+    batch, the oracle a sample of 192 envs (envs are independent)."""
+    o, s = scene(name)
+    qp64 = o.reset(n, 5, 0.1, 0.1)
+    kick_v, kick_w = synth.velocity_kicks(6, n, o.n_bodies, 0.5, 0.5)
+    qp64["vel"] += kick_v * np.array([1 - b.is_static for b in o.sys.bodies])[None, :, None]
+    qp64["ang"] += kick_w * np.array([1 - b.is_static for b in o.sys.bodies])[None, :, None]
+    qp = synth.to_f32(qp64)
+    act = synth.actions(8, 1, n, o.act_dim)[0]
+    got, status, ca = gpu_step(s, qp, act)
+    rows = synth.sample_envs(9, n, 192)
+    ref, ex = o.step({k: v[rows] for k, v in qp.items()}, act[rows], threads=8)
+    keep = ~ex["ambiguous"]
+    err, errs = max_err({k: v[rows] for k, v in got.items()}, ref, keep)
+    assert err <= TOL_STEP, errs
+    assert np.array_equal(ca[rows][keep], ex["contact_active"][keep])
+    assert np.all(status == 0)
+
+
+def r24_qualifies(o, qp, acts, T):
+    """R24: the oracle's own trajectory, perturbed by 1e-7 relative, diverges by ≤ 1e-4 after T steps."""
+    a, _ = o.rollout({k: v.astype(np.float64) for k, v in qp.items()}, acts[:T], threads=8)
+    pert = {k: v.astype(np.float64) * (1 + 1e-7) for k, v in qp.items()}
+    b, _ = o.rollout(pert, acts[:T], threads=8)
+    return max(float(np.max(np.abs(a[k] - b[k]))) for k in FIELDS) <= 1e-4
+
+
+@pytest.mark.parametrize("name,n,zero_action", [("ball", 1, True), ("pendulum", 1024, False),
+                                                ("chain2", 1024, False), ("ant", 512, True)])
+def test_100_step_parity(name, n, zero_action):
+    """Free-running GPU vs oracle trajectories, 100 steps, ≤ 1e-3 (R24-qualified configs)."""
+    o, s = scene(name)
+    T = 100
+    qp = synth.to_f32(o.reset(n, 11, 0.1, 0.1))
+    acts = synth.actions(12, T, n, o.act_dim)
+    if zero_action:
+        acts[:] = 0
+    assert r24_qualifies(o, qp, acts, T)
+    o_wide = oracle.Oracle(o.sys, amb_d=1e-3, amb_jn=1e-4)
+    ref, info = o_wide.rollout({k: v.astype(np.float64) for k, v in qp.items()}, acts, threads=8)
+    qd = dev(qp)
+    ad = torch.from_numpy(acts).cuda() if o.act_dim else None
+    for t in range(T):
+        s.step(qd, ad[t] if ad is not None else None, qd)
+    torch.cuda.synchronize()
+    got = host(qd)
+    keep = ~info["ambiguous"] if info["ambiguous"] is not None else np.ones(n, bool)
+    assert keep.mean() > 0.8
+    err, errs = max_err(got, ref, keep)
+    assert err <= TOL_100, errs
+
+
+def test_ball_drop_1000_steps_closed_form():
+    """M1 on the GPU: the rest height r − g h²/β after 1000 steps (fp32 vs closed form)."""
+    o, s = scene("ball")
+    qp = dev(synth.to_f32(o.batch_default_qp(1)))
+    for _ in range(1000):
+        s.step(qp, None, qp)
+    torch.cuda.synchronize()
+    z = float(qp["pos"][0, 1, 2])
+    assert abs(z - (0.5 - 9.8 * 0.01 ** 2 / 0.2)) < 1e-4
+
+
+def test_reset_matches_oracle():
+    o, s = scene("halfcheetah")
+    n = 777
+    qd = s.alloc_qp(n)
+    s.reset(qd, seed=0xDEADBEEF12345, vel_noise=0.1, ang_noise=0.2)
+    torch.cuda.synchronize()
+    ref = o.reset(n, 0xDEADBEEF12345, 0.1, 0.2)
+    err, errs = max_err(host(qd), ref)
+    assert err < 1e-6, errs
+
+
+def test_rollout_equals_repeated_steps_bitwise():
+    o, s = scene("ant")
+    n, T = 300, 7
+    qp = trajectory_states(o, n, 3, 0)
+    acts = torch.from_numpy(synth.actions(4, T, n, o.act_dim)).cuda()
+    a = dev(qp)
+    for t in range(T):
+        s.step(a, acts[t], a)
+    b_in = dev(qp)
+    b_out = s.alloc_qp(n)
+    s.rollout(b_in, acts, b_out)
+    torch.cuda.synchronize()
+    for k in FIELDS:
+        assert torch.equal(a[k], b_out[k])
+
+
+def test_determinism_and_shard_invariance():
+    """Bitwise identical run to run, and env i's result is independent of which
+    sub-range (shard) it is stepped in — the multi-GPU sharding invariant."""
+    o, s = scene("humanoid")
+    n = 999
+    qp = trajectory_states(o, n, 21, 2)
+    act = synth.actions(22, 1, n, o.act_dim)[0]
+    r1, _, _ = gpu_step(s, qp, act)
+    r2, _, _ = gpu_step(s, qp, act)
+    for k in FIELDS:
+        assert np.array_equal(r1[k], r2[k])
+    for lo, hi in [(0, 333), (333, 999), (5, 6), (17, 500)]:
+        part, _, _ = gpu_step(s, {k: v[lo:hi] for k, v in qp.items()}, act[lo:hi])
+        for k in FIELDS:
+            assert np.array_equal(part[k], r1[k][lo:hi])
+
+
+def test_in_place_and_empty():
+    o, s = scene("fetch")
+    n = 64
+    qp = trajectory_states(o, n, 1, 0)
+    act = synth.actions(2, 1, n, o.act_dim)[0]
+    ref, _, _ = gpu_step(s, qp, act)
+    qd = dev(qp)
+    s.step(qd, torch.from_numpy(act).cuda(), qd)
+    torch.cuda.synchronize()
+    for k in FIELDS:
+        assert np.array_equal(host(qd)[k], ref[k])
+    empty = s.alloc_qp(0)
+    bx.brax_step(s.handle, empty, None, empty, 0)   # n_envs == 0 is a no-op
+
+
+def test_argument_errors():
+    o, s = scene("ant")
+    n = 64
+    qd = s.alloc_qp(n)
+    a = torch.zeros((n, 8), device="cuda")
+    bad = dict(qd)
+    bad["pos"] = torch.empty(n * 30 + 1, device="cuda")[1:].view(n, 10, 3)
+    with pytest.raises(bx.BraxError) as e:
+        s.step(bad, a, bad)
+    assert e.value.name == "BRAX_E_MISALIGNED"
+    out = dict(qd)
+    out["vel"] = qd["pos"]
+    with pytest.raises(bx.BraxError) as e:
+        s.step(qd, a, out)
+    assert e.value.name == "BRAX_E_INVALID_ARGUMENT"
+    with pytest.raises(bx.BraxError) as e:
+        s.step(qd, None, qd)
+    assert e.value.name == "BRAX_E_INVALID_ARGUMENT"
+
+
+def test_status_bits_flag_blowup():
+    o, s = scene("ant")
+    n = 40
+    qp = trajectory_states(o, n, 1, 0)
+    qp["vel"][3, 2, 0] = 3e6
+    qp["vel"][5, 2, 0] = np.nan
+    act = np.zeros((n, 8), np.float32)
+    _, status, _ = gpu_step(s, qp, act)
+    assert status[3] & 2 and status[5] & 1
+    assert np.all(status[[i for i in range(n) if i not in (3, 5)]] == 0)
+
+
+def test_slot_table_and_default_qp_on_device_system():
+    for name in SCENES:
+        o, s = scene(name)
+        assert np.array_equal(s.slot_table(), o.sys.slot_table())
+        d = s.default_qp()
+        ref = o.default_qp()
+        for k in FIELDS:
+            assert np.max(np.abs(d[k] - ref[k])) < 1e-6
