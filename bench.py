@@ -142,8 +142,6 @@ def run_reference(args):
         return  # under torchrun only rank 0 runs and prints
     n = args.envs or DEFAULT_ENVS[args.scene]
     sample = min(n, 1024)
-    counts = load_counts(args.scene)
-    del counts
     # warmup W steps, then exactly K timed steps, each a bounded sample of the workload
     oracle_rate(args.scene, sample, 0, max_steps=max(1, args.warmup))
     rate, cores, steps, el = oracle_rate(args.scene, sample, 0, max_steps=args.steps)

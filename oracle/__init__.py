@@ -92,6 +92,8 @@ def _load():
             lib.oracle_step.argtypes = [C.POINTER(_OSys), C.POINTER(_OOpts), C.c_int64, C.c_int64, dp, dp, dp, dp,
                                         dp, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint8)]
             lib.oracle_step.restype = C.c_int
+            lib.oracle_step_f32.argtypes = lib.oracle_step.argtypes
+            lib.oracle_step_f32.restype = C.c_int
             lib.oracle_count_ops.argtypes = [C.POINTER(_OSys), C.POINTER(_OOpts), C.c_int64, C.c_int64, dp, dp, dp,
                                              dp, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
             lib.oracle_count_ops.restype = C.c_int
@@ -186,12 +188,14 @@ class Oracle:
         d = self.default_qp()
         return {k: np.broadcast_to(v, (n,) + v.shape).copy() for k, v in d.items()}
 
-    def step(self, qp, action=None, *, threads: int = 1):
+    def step(self, qp, action=None, *, threads: int = 1, fp32: bool = False):
         """One Brax step (substeps × Alg. 1) on a batch; returns (qp_out, extras).
 
         qp: dict of arrays pos [n,B,3], rot [n,B,4], vel [n,B,3], ang [n,B,3]
         (any float dtype; promoted to fp64).  action: [n, act_dim] or None.
-        extras: contact_active [n,C] u8, status [n] u32, ambiguous [n] bool."""
+        extras: contact_active [n,C] u8, status [n] u32, ambiguous [n] bool.
+        fp32=True runs the same code in fp32 arithmetic: a diagnostic of the fp32
+        rounding floor of the method, never a parity reference."""
         lib = _load()
         out = {k: np.ascontiguousarray(qp[k], dtype=np.float64).copy() for k in ("pos", "rot", "vel", "ang")}
         n = out["pos"].shape[0]
@@ -209,7 +213,8 @@ class Oracle:
         ca_ptr = ca.ctypes.data_as(C.POINTER(C.c_uint8)) if self.n_slots else None
 
         def run(e0, e1):
-            rc = lib.oracle_step(C.byref(self._sys), C.byref(self._opts), e0, e1,
+            fn = lib.oracle_step_f32 if fp32 else lib.oracle_step
+            rc = fn(C.byref(self._sys), C.byref(self._opts), e0, e1,
                                  out["pos"].ctypes.data_as(dp), out["rot"].ctypes.data_as(dp),
                                  out["vel"].ctypes.data_as(dp), out["ang"].ctypes.data_as(dp),
                                  act.ctypes.data_as(dp), ca_ptr,

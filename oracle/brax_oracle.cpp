@@ -61,6 +61,12 @@ inline double xatan2(double y, double x) { return std::atan2(y, x); }
 inline Cnt xatan2(Cnt y, Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::atan2(y.v, x.v)); }
 inline double xasin(double x) { return std::asin(x); }
 inline Cnt xasin(Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::asin(x.v)); }
+// fp32 instantiation (diagnostic only: measures the fp32 rounding floor of the
+// same algorithm; never used as a parity reference)
+inline double val(float x) { return x; }
+inline float xsqrt(float x) { return std::sqrt(x); }
+inline float xatan2(float y, float x) { return std::atan2(y, x); }
+inline float xasin(float x) { return std::asin(x); }
 template <class T> inline T xmax(T a, T b) { return (a < b) ? b : a; }
 template <class T> inline T xmin(T a, T b) { return (b < a) ? b : a; }
 template <class T> inline T xclamp(T x, T lo, T hi) { return xmin(xmax(x, lo), hi); }
@@ -332,7 +338,9 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     T d;
     bool par = false;
     narrowphase<T>(S, sl, st, opt.amb_par, &n, &pt, &d, &par);
-    if (par) out->ambiguous = true;
+    // R23: a near-parallel capsule pair only matters if it can be in contact
+    // (the segment distance is unique; only the contact point is not)
+    if (par && val(d) > -opt.amb_d) out->ambiguous = true;
     if (std::fabs(val(d)) < opt.amb_d) out->ambiguous = true;  // R23 onset band
     if (!(d > T(0.0))) continue;                                 // R16: strict d > 0
 
@@ -449,6 +457,15 @@ int oracle_step(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, double*
                 uint32_t* status, uint8_t* ambiguous) {
   if (!S || !opt || e1 < e0) return 1;
   step_range<double>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous);
+  return 0;
+}
+
+// Diagnostic: the same step in fp32 arithmetic (inputs/outputs fp64 arrays).
+int oracle_step_f32(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, double* pos, double* rot,
+                    double* vel, double* ang, const double* action, uint8_t* contact_active,
+                    uint32_t* status, uint8_t* ambiguous) {
+  if (!S || !opt || e1 < e0) return 1;
+  step_range<float>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous);
   return 0;
 }
 

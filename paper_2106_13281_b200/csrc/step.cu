@@ -255,8 +255,9 @@ __device__ __forceinline__ void contact(const DSlot& S, Row A, Row B, const DHea
 }
 
 // ---- S6 + S7 + S8: gather, potential integrator, collision integrator
+// sJ, sC: this lane's column of the joint / slot outputs.
 __device__ __forceinline__ void integrate(const DBody& bd, Row r, const Tables& T, int b, const float* sJ,
-                                          const float* sC, int lane, const DHeader& H) {
+                                          const float* sC, const DHeader& H) {
   V3 F{0.f, 0.f, 0.f}, Tq{0.f, 0.f, 0.f}, dV{0.f, 0.f, 0.f}, dW{0.f, 0.f, 0.f};
   float cnt = 0.f;
   const int i0 = T.inc_begin[b], i1 = T.inc_begin[b + 1];
@@ -264,7 +265,7 @@ __device__ __forceinline__ void integrate(const DBody& bd, Row r, const Tables& 
     int e = T.inc[i];
     int kind = e >> 16, ix = e & 0xffff;
     if (kind <= kIncJointParent) {
-      const float* o = sJ + ix * kJointOut * 32 + lane;
+      const float* o = sJ + ix * kJointOut * 32;
       V3 f{o[0], o[32], o[64]};
       if (kind == kIncJointChild) {
         F = F + f;
@@ -274,7 +275,7 @@ __device__ __forceinline__ void integrate(const DBody& bd, Row r, const Tables& 
         Tq = Tq + V3{o[192], o[224], o[256]};
       }
     } else {
-      const float* o = sC + ix * kSlotOut * 32 + lane;
+      const float* o = sC + ix * kSlotOut * 32;
       V3 p{o[0], o[32], o[64]};
       cnt += o[288];
       if (kind == kIncSlotA) {
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32) brax_step_kernel(const KArgs k
     if (A > 0) {
       const float* act = a.actions + (step * a.n_envs + e0) * A;
       for (int i = tid; i < nvalid * A; i += blockDim.x) {
-        int env = __umulhi(uint32_t(i), H.row_magic[2]);
+        int env = (A == 1) ? i : int(__umulhi(uint32_t(i), H.row_magic[2]));  // magic(1) would overflow
         int k = i - env * A;
         sA[k * 32 + env] = __ldg(act + i);
       }
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32) brax_step_kernel(const KArgs k
       __syncthreads();
       for (int i = bw0; i < bw1; ++i) {
         int b = T.bodies_of_warp[i];
-        integrate(T.bodies[b], Row{sQ + b * kQPFields * 32 + lane}, T, b, sJ + lane, sC + lane, lane, H);
+        integrate(T.bodies[b], Row{sQ + b * kQPFields * 32 + lane}, T, b, sJ + lane, sC + lane, H);
       }
     }
   }

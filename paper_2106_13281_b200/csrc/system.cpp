@@ -292,7 +292,7 @@ System* build_system(const Config& cfg, int device) {
   auto magic = [](uint32_t d) -> uint32_t { return d ? uint32_t(((uint64_t(1) << 32) + d - 1) / d) : 0; };
   hd.row_magic[0] = magic(uint32_t(3 * B));
   hd.row_magic[1] = magic(uint32_t(4 * B));
-  hd.row_magic[2] = magic(uint32_t(std::max(1, cfg.act_dim)));
+  hd.row_magic[2] = cfg.act_dim > 1 ? magic(uint32_t(cfg.act_dim)) : 0;  // A == 1 is special-cased
   hd.row_magic[3] = 0;
 
   s->smem_bytes = size_t(hd.blob_words) * 4 +

@@ -190,7 +190,7 @@ def grasp():
     for i in range(4):
         incl.append(f'collide_include {{ first: "Dist{i}" second: "Ground" }}')
     out += joints + acts + incl
-    out.append('defaults { qps { name: "Base" pos { z: 0.6 } } qps { name: "Ball" pos { z: 0.1 } } }')
+    out.append('defaults { qps { name: "Base" pos { z: 0.6 } } qps { name: "Ball" pos { z: 0.098775 } } }')
     return "\n".join(out) + "\n"
 
 
@@ -203,7 +203,7 @@ def fetch():
            'bodies { name: "Ground" frozen { all: true } colliders { plane {} } }',
            'bodies { name: "Torso" mass: 5 inertia { x: 1 y: 1 z: 1 }',
            "  colliders { box { halfsize { x: 0.3 y: 0.15 z: 0.1 } } } }",
-           'bodies { name: "Head" mass: 0.5 inertia { x: 0.2 y: 0.2 z: 0.2 }',
+           'bodies { name: "Head" mass: 0.5 inertia { x: 1 y: 1 z: 1 }',
            "  colliders { rotation { y: 90 } capsule { radius: 0.05 length: 0.2 } } }",
            'bodies { name: "Target" mass: 1 inertia { x: 1 y: 1 z: 1 } frozen { all: true } }']
     joints = ['joints { name: "Neck" parent: "Torso" child: "Head" stiffness: 5000 angular_damping: 10\n'
@@ -212,9 +212,9 @@ def fetch():
     acts = ['actuators { name: "Neck" joint: "Neck" strength: 10 torque {} }']
     incl = ['collide_include { first: "Torso" second: "Ground" }']
     for i, (sx, sy) in enumerate(((1, 1), (1, -1), (-1, 1), (-1, -1))):
-        out.append(f'bodies {{ name: "Thigh{i}" mass: 0.5 inertia {{ x: 0.2 y: 0.2 z: 0.2 }}')
+        out.append(f'bodies {{ name: "Thigh{i}" mass: 0.5 inertia {{ x: 1 y: 1 z: 1 }}')
         out.append("  colliders { capsule { radius: 0.04 length: 0.28 } } }")
-        out.append(f'bodies {{ name: "Shin{i}" mass: 0.5 inertia {{ x: 0.2 y: 0.2 z: 0.2 }}')
+        out.append(f'bodies {{ name: "Shin{i}" mass: 0.5 inertia {{ x: 1 y: 1 z: 1 }}')
         out.append("  colliders { capsule { radius: 0.04 length: 0.28 } } }")
         joints.append(f'joints {{ name: "Hip{i}" parent: "Torso" child: "Thigh{i}" stiffness: 5000 angular_damping: 10\n'
                       f"  {vec('parent_offset', (0.25 * sx, 0.12 * sy, -0.1))} child_offset {{ z: 0.1 }} rotation {{ z: 90 }}\n"

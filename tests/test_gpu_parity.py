@@ -130,7 +130,7 @@ def test_100_step_parity(name, n, zero_action):
     if zero_action:
         acts[:] = 0
     assert r24_qualifies(o, qp, acts, T)
-    o_wide = oracle.Oracle(o.sys, amb_d=1e-3, amb_jn=1e-4)
+    o_wide = oracle.Oracle(o.sys, amb_d=1e-4, amb_jn=1e-4)
     ref, info = o_wide.rollout({k: v.astype(np.float64) for k, v in qp.items()}, acts, threads=8)
     qd = dev(qp)
     ad = torch.from_numpy(acts).cuda() if o.act_dim else None

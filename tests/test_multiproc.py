@@ -1,0 +1,78 @@
+"""World-size-2 gloo tests of the N>1 host path (CPU): env sharding, the
+statistics all-reduce, and that sharded stepping reproduces the unsharded
+result exactly (envs are independent)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2106_13281_b200.dist import env_shard, strong_shard
+
+
+def test_shard_ranges_cover_exactly():
+    for world in (1, 2, 3, 8):
+        for n in (0, 1, 7, 8192, 8193):
+            spans = [strong_shard(r, world, n) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+        assert [env_shard(r, world, 8192) for r in range(world)] == [(r * 8192, (r + 1) * 8192) for r in range(world)]
+    with pytest.raises(ValueError):
+        env_shard(2, 2, 10)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_total, out_dir):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    import oracle
+    import synth
+    from paper_2106_13281_b200.dist import allreduce_stats, strong_shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = oracle.Oracle(oracle.load_scene("ant"))
+    qp = o.reset(n_total, 3, 0.1, 0.1)
+    acts = synth.actions(4, 3, n_total, o.act_dim)
+    lo, hi = strong_shard(rank, world, n_total)
+    mine = {k: v[lo:hi] for k, v in qp.items()}
+    blow = 0
+    for t in range(3):
+        mine, ex = o.step(mine, acts[t][lo:hi])
+        blow += int((ex["status"] != 0).sum())
+    steps, blowups, _, ms = allreduce_stats(float((hi - lo) * 3), float(blow), float(10 + rank))
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), lo=lo, hi=hi, steps=steps, blowups=blowups, ms=ms,
+             **{k: v for k, v in mine.items()})
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_equals_unsharded(tmp_path):
+    import oracle
+    import synth
+    n_total, world = 77, 2
+    mp.start_processes(_worker, args=(world, _free_port(), n_total, str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    o = oracle.Oracle(oracle.load_scene("ant"))
+    qp = o.reset(n_total, 3, 0.1, 0.1)
+    acts = synth.actions(4, 3, n_total, o.act_dim)
+    for t in range(3):
+        qp, _ = o.step(qp, acts[t])
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        assert float(d["steps"]) == n_total * 3          # SUM over ranks
+        assert float(d["ms"]) == 10 + world - 1          # MAX over ranks
+        assert float(d["blowups"]) == 0
+        for k in ("pos", "rot", "vel", "ang"):
+            assert np.array_equal(d[k], qp[k][int(d["lo"]):int(d["hi"])])
