@@ -90,6 +90,7 @@ brax_status brax_config_slot_table(const brax_config *cfg, int32_t *out);
 /* default_qp in fp64 (host): pos [B][3], rot [B][4] (velocities are zero). */
 brax_status brax_config_default_qp(const brax_config *cfg, double *pos, double *rot);
 
+
 /* ---------------------------------------------------------------- system
  * The paper's `system`: immutable device-resident static
  * tables (bodies, joints with their actuators, contact slots, per-body incidence

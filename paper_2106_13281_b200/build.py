@@ -1,6 +1,6 @@
 """Builds paper_2106_13281_b200/_lib/libbrax_b200.so with nvcc for sm_100a.
 
-    python -m paper_2106_13281_b200.build        (or __graft_entry__.build())
+    python paper_2106_13281_b200/build.py [-v]     (or __graft_entry__.build())
 
 One shared library: host C++ (parser, system builder, C ABI) + CUDA kernels,
 cudart linked statically, -lineinfo for ncu source correlation.
@@ -26,7 +26,7 @@ def nvcc():
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".h")] + \
+    deps = srcs + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))] + \
         [os.path.join(ROOT, "include", "brax_b200.h")]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
         return OUT

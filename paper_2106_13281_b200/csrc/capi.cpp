@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "brax_b200.h"
@@ -80,7 +81,7 @@ brax_status step_common(const brax_system* sys, brax_qp in, const float* actions
       }
   }
   brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, out.pos, out.rot, out.vel, out.ang, actions,
-                   x ? x->status : nullptr, x ? x->contact_active : nullptr, n_envs, n_steps};
+                   x ? x->status : nullptr, x ? x->contact_active : nullptr, n_envs, n_steps, 0, 0};
   if (a.contact_active && s.hd.C == 0) a.contact_active = nullptr;
   int cur = -1;
   cudaGetDevice(&cur);
@@ -184,7 +185,7 @@ brax_status brax_system_get_info(const brax_system* sys, brax_system_info* out) 
   out->n_contact_slots = s.hd.C;
   out->substeps = s.hd.S;
   out->dt = float(s.cfg.dt);
-  out->warps_per_block = s.hd.W;
+  out->warps_per_block = s.hd.plan[0].W;
   out->n_lint_warnings = int32_t(s.lint.size());
   out->smem_bytes = int32_t(s.smem_bytes);
   return BRAX_OK;

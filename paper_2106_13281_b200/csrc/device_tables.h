@@ -6,58 +6,146 @@
 // of the shared-memory copy; a warp reads one item's struct with warp-uniform
 // (broadcast) addresses.
 #pragma once
+#ifdef __CUDACC_RTC__
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
 #include <stdint.h>
+#endif
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
+#define BRAX_HD __host__ __device__
+#else
+#define BRAX_HD
+#endif
 
 namespace brax {
 
 constexpr int kEnvsPerBlock = 32;  // lane = env; warp = work item
 constexpr int kMaxWarps = 16;      // 512 threads per block at most
-constexpr int kQPFields = 13;      // pos 0-2, rot 3-6 (w,x,y,z), vel 7-9, ang 10-12
-constexpr int kJointOut = 9;       // F (child), T child, T parent
-constexpr int kSlotOut = 10;       // P, rA×P, rB×P, active
+constexpr int kMaxRegs = 80;       // registers per thread of the step kernel
 
-struct DBody {              // 12 words
+// Flag bits (precomputed on the host; warp-uniform tests in the kernel).  An
+// exact-zero offset, identity frame, isotropic inertia or all-free mask makes the
+// corresponding arithmetic an exact identity, which the kernel then skips.
+enum : int32_t {
+  kFlagIso = 1,       // body: isotropic inertia (I_w⁻¹ v = i·v)
+  kFlagFreePos = 2,   // body: no frozen position axis
+  kFlagFreeRot = 4,   // body: no frozen rotation axis
+};
+enum : int32_t {
+  kJZeroOp = 1, kJZeroOc = 2, kJIdentP = 4, kJIdentC = 8, kJNoCl = 16, kJNoCa = 32,
+};
+enum : int32_t {
+  kSZeroPa = 1, kSZeroPb = 2, kSIdentA = 4, kSIdentB = 8, kSIsoA = 16, kSIsoB = 32,
+};
+
+// Every struct is a whole number of 16-byte vectors so the kernel reads it with
+// LDS.128 from the shared-memory copy (the blob offsets are 4-word aligned).
+struct alignas(16) DBody {  // 16 words
   float inv_mass;
   float inv_inertia[3];     // 1 / body-frame diagonal inertia
-  float mpos[3], mrot[3];   // 1 − frozen (App. A `frozen`)
+  float mpos[3];            // 1 − frozen position (App. A `frozen`)
   int32_t is_static;        // all 6 axes frozen: never integrated (R21)
+  float mrot[3];            // 1 − frozen rotation
   int32_t rot_frozen;       // all 3 rotation axes frozen: q untouched
+  int32_t flags, pad0, pad1, pad2;
+};
+struct alignas(16) DJoint {  // 36 words
+  int32_t parent, child, dof, act_kind;
+  int32_t act_offset, flags, pad0, pad1;
+  float o_p[3], k;          // parent anchor offset; stiffness
+  float o_c[3], c_l;        // child anchor offset; linear (spring) damping
+  float jp[4];              // J_p = rotation
+  float jc[4];              // J_c = conj(reference_rotation) ⊗ rotation
+  float lo[3], k_l;         // limits (rad) of the free axes; limit stiffness
+  float hi[3], k_a;         // ... ; alignment stiffness
+  float c_a, strength, pad2, pad3;  // angular damping; actuator strength (act_kind ≥ 0)
+};
+struct alignas(16) DSlot {  // 40 words
+  int32_t type, a, b, point;
+  int32_t a_static, b_static, flags, pad0;
+  float ca_pos[3], ra;      // collider A offset in body A; radius A
+  float ca_rot[4];          // collider A rotation in body A
+  float cb_pos[3], rb;
+  float cb_rot[4];
+  float ell_a, ellb, inv_mass_a, inv_mass_b;  // ell_a: signed capsule-end offset (+ℓ end 0, −ℓ end 1)
+  float corner[3], pad1;    // box: signed half-extent corner of slot `point`
+  float inv_inertia_a[3], pad2;
+  float inv_inertia_b[3], pad3;
 };
 
-struct DJoint {             // 32 words
-  int32_t parent, child, dof, act_kind, act_offset, pad;
-  float o_p[3], o_c[3];     // anchor offsets in the parent / child body frames
-  float jp[4], jc[4];       // joint frames J_p = rotation, J_c = conj(reference_rotation) ⊗ rotation
-  float k, c_l, c_a, k_l, k_a;
-  float lo[3], hi[3];       // limits (rad) of the free axes
-  float strength;           // actuator strength (act_kind ≥ 0)
+// Shared-memory layouts (words): per (item, lane) records, 16-byte aligned,
+// strides chosen so a warp's LDS.128 / STS.128 are bank-conflict free.
+constexpr int kQS = 20;   // QP record: pos 0-2 | rot 4-7 (w,x,y,z) | vel 8-10 | ang 12-14
+constexpr int kJS = 12;   // joint record: F 0-2 | T_child 4-6 | T_parent 8-10
+constexpr int kCS = 12;   // slot record: P 0-2, active 3 | r_A×P 4-6 | r_B×P 8-10
+
+// Incidence entries of the body gather (fixed order: joints by index, then slots
+// by index, R29): (item index << 4) | torque-word offset in the record (4 for the
+// child / A side, 8 for the parent / B side; the side also fixes the sign).
+BRAX_HD inline int32_t inc_pack(int index, bool second_side) { return (index << 4) | (second_side ? 8 : 4); }
+
+// Shared-memory layout of the step kernel (words; every region 16-byte aligned).
+//   [2 mbarriers][tables][QP records B·E·kQS][U][sA A·E][action staging E·A][counts C·E][status E]
+// U holds the joint and slot records during the substeps and the contiguous
+// TMA staging chunks (pos|rot|vel|ang, E·B·13 words) while loading / storing.
+struct SmemLayout {
+  int32_t blob, q, u, a, astg, cnt, stat, total_words;
+};
+BRAX_HD inline int32_t round4(int32_t w) { return (w + 3) & ~3; }
+BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A, int32_t E, int32_t blob_words) {
+  SmemLayout L;
+  L.blob = 4;
+  L.q = L.blob + round4(blob_words);
+  L.u = L.q + B * E * kQS;
+  const int32_t recs = J * E * kJS + C * E * kCS, stg = E * B * 13;
+  L.a = L.u + round4(recs > stg ? recs : stg);
+  L.astg = L.a + round4(A * E);
+  L.cnt = L.astg + round4(A * E);
+  L.stat = L.cnt + round4(C * E);
+  L.total_words = L.stat + round4(E);
+  return L;
+}
+
+// Arguments of one step launch (device pointers; see include/brax_b200.h).
+struct StepArgs {
+  const float *pos_in, *rot_in, *vel_in, *ang_in;
+  float *pos_out, *rot_out, *vel_out, *ang_out;
+  const float* actions;        // [n_steps][n][A] (NULL iff A == 0)
+  uint32_t* status;            // [n] or NULL
+  uint8_t* contact_active;     // [n][C] or NULL
+  int64_t n_envs;
+  int64_t n_steps;
+  int32_t bulk_ok;             // all QP pointers 16-byte aligned: TMA bulk staging for full blocks
+  int32_t act_bulk_ok;         // actions 16-byte aligned and n·A % 4 == 0: TMA bulk action staging
 };
 
-struct DSlot {              // 36 words
-  int32_t type, a, b, point, a_static, b_static;
-  float ca_pos[3], ca_rot[4];  // collider A pose in body A
-  float cb_pos[3], cb_rot[4];  // collider B pose in body B
-  float ra, ella, rb, ellb;    // radii and capsule segment half-lengths ℓ = L/2 − r
-  float hs[3];                 // box half-extents (A), signed by `point`
-  float inv_mass_a, inv_mass_b;
-  float inv_inertia_a[3], inv_inertia_b[3];
-  float pad;
+// A work plan for one lane-group count G (E = 32/G envs per block): each warp's
+// lanes form G groups of E lanes; group g runs item items[step*G + g] on the
+// block's E envs (-1 = idle).  Items sharing a step have the same code class,
+// so the groups do not diverge.
+constexpr int kNumPlans = 3;       // G = 1, 2, 4
+struct DPlan {
+  int32_t G, E, W, log2E;
+  int32_t off_item_begin, off_items;          // per warp: item steps [begin, end); items[step*G + g]
+  int32_t off_body_begin, off_bodies_of_warp;  // per warp: body steps; bodies[step*G + g]
+  int32_t smem_bytes, pad0, pad1, pad2;
 };
-
-// Incidence entry kinds (body gather, fixed order: joints by index, then slots by index).
-enum IncKind { kIncJointChild = 0, kIncJointParent = 1, kIncSlotA = 2, kIncSlotB = 3 };
-__host__ __device__ inline int32_t inc_pack(int kind, int index) { return (kind << 16) | index; }
 
 struct DHeader {            // passed by value as a kernel argument
-  int32_t B, J, C, A, S, W;
+  int32_t B, J, C, A, S;
   float h, beta_over_h, mu, e;
   float g[3];
   int32_t blob_words;       // total words (padded to a multiple of 4)
   int32_t off_bodies, off_joints, off_slots;
-  int32_t off_item_begin, off_items;   // per warp: items (j < J: joint j; J + c: slot c)
-  int32_t off_body_begin, off_bodies_of_warp;
-  int32_t off_inc_begin, off_inc;      // per body: incidence list
+  int32_t off_jinc_begin, off_jinc;    // per body: joint incidence entries
+  int32_t off_cinc_begin, off_cinc;    // per body: contact-slot incidence entries
   uint32_t row_magic[4];    // ⌈2³²/(B·K)⌉ for K = 3, 4 (index 0: K=3, 1: K=4), A (index 2)
+  DPlan plan[kNumPlans];
 };
 
 }  // namespace brax

@@ -92,10 +92,9 @@ void default_qp(const Config& cfg, std::vector<double>& pos, std::vector<double>
   }
 }
 
-System* build_system(const Config& cfg, int device) {
+System* build_host(const Config& cfg) {
   std::unique_ptr<System> s(new System());
   s->cfg = cfg;
-  s->device = device;
   const int B = int(cfg.bodies.size()), J = int(cfg.joints.size()), C = int(cfg.slots.size());
   const double h = cfg.dt / cfg.substeps;
 
@@ -150,21 +149,30 @@ System* build_system(const Config& cfg, int device) {
   std::vector<int> dyn;
   for (int b = 0; b < B; ++b) {
     const Body& src = cfg.bodies[b];
-    DBody& d = bodies[b];
+    DBody d{};
     d.inv_mass = float(1.0 / src.mass);
+    bool free_pos = true, free_rot = true;
     for (int k = 0; k < 3; ++k) {
       d.inv_inertia[k] = float(1.0 / src.inertia[k]);
       d.mpos[k] = float(1.0 - src.frozen_pos[k]);
       d.mrot[k] = float(1.0 - src.frozen_rot[k]);
+      free_pos = free_pos && src.frozen_pos[k] == 0.0;
+      free_rot = free_rot && src.frozen_rot[k] == 0.0;
     }
     d.is_static = src.is_static() ? 1 : 0;
     d.rot_frozen = src.rot_frozen() ? 1 : 0;
+    bool iso = d.inv_inertia[0] == d.inv_inertia[1] && d.inv_inertia[1] == d.inv_inertia[2];
+    d.flags = (iso ? kFlagIso : 0) | (free_pos ? kFlagFreePos : 0) | (free_rot ? kFlagFreeRot : 0);
+    bodies[b] = d;
     if (!d.is_static) dyn.push_back(b);
   }
   s->n_dynamic = int(dyn.size());
+  auto align4 = [&] { while (blob.size() % 4) blob.push_back(0); };
   hd.off_bodies = int32_t(blob.size());
   for (const DBody& d : bodies) push_struct(blob, d);
 
+  auto zero3 = [](const float* p) { return p[0] == 0.f && p[1] == 0.f && p[2] == 0.f; };
+  auto ident = [](const float* q) { return q[0] == 1.f && q[1] == 0.f && q[2] == 0.f && q[3] == 0.f; };
   hd.off_joints = int32_t(blob.size());
   for (const Joint& j : cfg.joints) {
     DJoint d{};
@@ -192,6 +200,8 @@ System* build_system(const Config& cfg, int device) {
     d.k_l = float(j.limit_stiffness);
     d.k_a = float(j.angular_stiffness);
     d.strength = float(j.act_strength);
+    d.flags = (zero3(d.o_p) ? kJZeroOp : 0) | (zero3(d.o_c) ? kJZeroOc : 0) | (ident(d.jp) ? kJIdentP : 0) |
+              (ident(d.jc) ? kJIdentC : 0) | (d.c_l == 0.f ? kJNoCl : 0) | (d.c_a == 0.f ? kJNoCa : 0);
     push_struct(blob, d);
   }
 
@@ -209,9 +219,12 @@ System* build_system(const Config& cfg, int device) {
     for (int k = 0; k < 3; ++k) {
       d.ca_pos[k] = float(A.pos[k]);
       d.cb_pos[k] = float(Bc.pos[k]);
-      d.hs[k] = float(A.halfsize[k]);
       d.inv_inertia_a[k] = bodies[sl.a].inv_inertia[k];
       d.inv_inertia_b[k] = bodies[sl.b].inv_inertia[k];
+    }
+    if (sl.type == BRAX_SLOT_BOX_PLANE) {
+      const int sg[3] = {(sl.point & 1) ? 1 : -1, (sl.point & 2) ? 1 : -1, (sl.point & 4) ? 1 : -1};
+      for (int k = 0; k < 3; ++k) d.corner[k] = float(sg[k] * A.halfsize[k]);
     }
     for (int k = 0; k < 4; ++k) {
       d.ca_rot[k] = float(A.rot[k]);
@@ -219,74 +232,126 @@ System* build_system(const Config& cfg, int device) {
     }
     d.ra = float(A.radius);
     d.rb = float(Bc.radius);
-    d.ella = float(0.5 * A.length - A.radius);
+    float ell_a = float(0.5 * A.length - A.radius);
+    d.ell_a = (sl.type == BRAX_SLOT_CAPSULE_PLANE && sl.point == 1) ? -ell_a : ell_a;
     d.ellb = float(0.5 * Bc.length - Bc.radius);
     d.inv_mass_a = bodies[sl.a].inv_mass;
     d.inv_mass_b = bodies[sl.b].inv_mass;
+    d.flags = (zero3(d.ca_pos) ? kSZeroPa : 0) | (zero3(d.cb_pos) ? kSZeroPb : 0) | (ident(d.ca_rot) ? kSIdentA : 0) |
+              (ident(d.cb_rot) ? kSIdentB : 0) | ((bodies[sl.a].flags & kFlagIso) ? kSIsoA : 0) |
+              ((bodies[sl.b].flags & kFlagIso) ? kSIsoB : 0);
     push_struct(blob, d);
   }
 
-  // ---- warp work plan: W warps per block, lane = env ----
-  int W = std::max(1, std::min(kMaxWarps, int(dyn.size())));
-  if (const char* env = std::getenv("BRAX_WARPS_PER_BLOCK")) {
-    int v = std::atoi(env);
-    if (v >= 1 && v <= kMaxWarps) W = v;
+  align4();
+  // ---- work plans: for G lane groups per warp (E = 32/G envs per block) ----
+  // Items of one code class (joints with equal dof / actuator kind / flags;
+  // contacts with equal type / flags / static sides) are packed G to a step so
+  // a warp's groups never diverge on item kind; steps go to warps by
+  // longest-processing-time-first over estimated costs (joint ≈ 5, contact ≈ 3).
+  const DJoint* djoints = reinterpret_cast<const DJoint*>(blob.data() + hd.off_joints);
+  const DSlot* dslots = reinterpret_cast<const DSlot*>(blob.data() + hd.off_slots);
+  std::vector<std::vector<int>> classes;
+  {
+    std::vector<std::vector<int>> keys;
+    auto add = [&](const std::vector<int>& key, int item) {
+      for (size_t k = 0; k < keys.size(); ++k)
+        if (keys[k] == key) { classes[k].push_back(item); return; }
+      keys.push_back(key);
+      classes.push_back({item});
+    };
+    for (int j = 0; j < J; ++j) add({0, djoints[j].dof, djoints[j].act_kind, djoints[j].flags}, j);
+    for (int c = 0; c < C; ++c)
+      add({1, dslots[c].type, dslots[c].flags, dslots[c].a_static, dslots[c].b_static}, J + c);
   }
-  hd.W = W;
-  // items: longest-processing-time-first over estimated costs (joint ≈ 5, contact ≈ 3)
-  std::vector<int> items(J + C);
-  std::iota(items.begin(), items.end(), 0);
-  auto cost = [&](int it) { return it < J ? 5 : 3; };
-  std::stable_sort(items.begin(), items.end(), [&](int a, int b) { return cost(a) > cost(b); });
-  std::vector<std::vector<int>> per_warp(W);
-  std::vector<int> load(W, 0);
-  for (int it : items) {
-    int w = int(std::min_element(load.begin(), load.end()) - load.begin());
-    per_warp[w].push_back(it);
-    load[w] += cost(it);
+  const int env_w = [] {
+    const char* e = std::getenv("BRAX_WARPS_PER_BLOCK");
+    int v = e ? std::atoi(e) : 0;
+    return (v >= 1 && v <= kMaxWarps) ? v : 0;
+  }();
+  for (int pi = 0; pi < kNumPlans; ++pi) {
+    DPlan& P = hd.plan[pi];
+    const int G = 1 << pi, E = 32 / G;
+    P.G = G;
+    P.E = E;
+    P.log2E = 5 - pi;
+    std::vector<std::vector<int>> steps;  // each: G items (-1 idle)
+    std::vector<int> step_cost;
+    for (const auto& cl : classes)
+      for (size_t k = 0; k < cl.size(); k += G) {
+        std::vector<int> st(G, -1);
+        for (int g = 0; g < G && k + g < cl.size(); ++g) st[g] = cl[k + g];
+        steps.push_back(st);
+        step_cost.push_back(cl[k] < J ? 5 : 3);
+      }
+    const int n_body_steps = (int(dyn.size()) + G - 1) / G;
+    int W = std::max(1, std::max(n_body_steps, (int(steps.size()) + 1) / 2));
+    W = std::min(W, kMaxWarps);
+    if (env_w) W = env_w;
+    P.W = W;
+    std::vector<int> order(steps.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return step_cost[a] > step_cost[b]; });
+    std::vector<std::vector<int>> per_warp(W);
+    std::vector<int> load(W, 0);
+    for (int k : order) {
+      int w = int(std::min_element(load.begin(), load.end()) - load.begin());
+      per_warp[w].push_back(k);
+      load[w] += step_cost[k];
+    }
+    align4();
+    P.off_item_begin = int32_t(blob.size());
+    int acc = 0;
+    for (int w = 0; w <= W; ++w) {
+      blob.push_back(uint32_t(acc));
+      if (w < W) acc += int(per_warp[w].size());
+    }
+    P.off_items = int32_t(blob.size());
+    for (int w = 0; w < W; ++w) {
+      std::sort(per_warp[w].begin(), per_warp[w].end());
+      for (int k : per_warp[w])
+        for (int g = 0; g < G; ++g) blob.push_back(uint32_t(steps[k][g]));
+    }
+    // dynamic bodies, G per step, steps round-robin over warps
+    std::vector<std::vector<int>> wb(W);
+    for (int k = 0; k < n_body_steps; ++k) wb[k % W].push_back(k);
+    P.off_body_begin = int32_t(blob.size());
+    acc = 0;
+    for (int w = 0; w <= W; ++w) {
+      blob.push_back(uint32_t(acc));
+      if (w < W) acc += int(wb[w].size());
+    }
+    P.off_bodies_of_warp = int32_t(blob.size());
+    for (int w = 0; w < W; ++w)
+      for (int k : wb[w])
+        for (int g = 0; g < G; ++g) {
+          size_t i = size_t(k) * G + g;
+          blob.push_back(uint32_t(i < dyn.size() ? dyn[i] : -1));
+        }
   }
-  hd.off_item_begin = int32_t(blob.size());
-  int acc = 0;
-  for (int w = 0; w <= W; ++w) {
-    blob.push_back(uint32_t(acc));
-    if (w < W) acc += int(per_warp[w].size());
-  }
-  hd.off_items = int32_t(blob.size());
-  for (int w = 0; w < W; ++w) {
-    std::sort(per_warp[w].begin(), per_warp[w].end());  // joints first, then slots
-    for (int it : per_warp[w]) blob.push_back(uint32_t(it));
-  }
-  // dynamic bodies round-robin over warps
-  std::vector<std::vector<int>> wb(W);
-  for (size_t i = 0; i < dyn.size(); ++i) wb[i % W].push_back(dyn[i]);
-  hd.off_body_begin = int32_t(blob.size());
-  acc = 0;
-  for (int w = 0; w <= W; ++w) {
-    blob.push_back(uint32_t(acc));
-    if (w < W) acc += int(wb[w].size());
-  }
-  hd.off_bodies_of_warp = int32_t(blob.size());
-  for (int w = 0; w < W; ++w)
-    for (int b : wb[w]) blob.push_back(uint32_t(b));
-  // incidence lists: joints by index (child / parent role), then slots by index (A / B role)
-  std::vector<std::vector<int32_t>> inc(B);
+  // incidence lists: joints by index (child / parent side), then slots by index (A / B side)
+  std::vector<std::vector<int32_t>> jinc(B), cinc(B);
   for (int j = 0; j < J; ++j) {
-    inc[cfg.joints[j].child].push_back(inc_pack(kIncJointChild, j));
-    inc[cfg.joints[j].parent].push_back(inc_pack(kIncJointParent, j));
+    jinc[cfg.joints[j].child].push_back(inc_pack(j, false));
+    jinc[cfg.joints[j].parent].push_back(inc_pack(j, true));
   }
   for (int c = 0; c < C; ++c) {
-    inc[cfg.slots[c].a].push_back(inc_pack(kIncSlotA, c));
-    inc[cfg.slots[c].b].push_back(inc_pack(kIncSlotB, c));
+    cinc[cfg.slots[c].a].push_back(inc_pack(c, false));
+    cinc[cfg.slots[c].b].push_back(inc_pack(c, true));
   }
-  hd.off_inc_begin = int32_t(blob.size());
-  acc = 0;
-  for (int b = 0; b <= B; ++b) {
-    blob.push_back(uint32_t(acc));
-    if (b < B) acc += int(inc[b].size());
-  }
-  hd.off_inc = int32_t(blob.size());
-  for (int b = 0; b < B; ++b)
-    for (int32_t e : inc[b]) blob.push_back(uint32_t(e));
+  auto put_lists = [&](const std::vector<std::vector<int32_t>>& lists, int32_t* off_begin, int32_t* off_list) {
+    *off_begin = int32_t(blob.size());
+    int acc = 0;
+    for (int b = 0; b <= B; ++b) {
+      blob.push_back(uint32_t(acc));
+      if (b < B) acc += int(lists[b].size());
+    }
+    *off_list = int32_t(blob.size());
+    for (int b = 0; b < B; ++b)
+      for (int32_t e : lists[b]) blob.push_back(uint32_t(e));
+  };
+  put_lists(jinc, &hd.off_jinc_begin, &hd.off_jinc);
+  put_lists(cinc, &hd.off_cinc_begin, &hd.off_cinc);
   while (blob.size() % 4) blob.push_back(0);
   hd.blob_words = int32_t(blob.size());
   auto magic = [](uint32_t d) -> uint32_t { return d ? uint32_t(((uint64_t(1) << 32) + d - 1) / d) : 0; };
@@ -295,15 +360,28 @@ System* build_system(const Config& cfg, int device) {
   hd.row_magic[2] = cfg.act_dim > 1 ? magic(uint32_t(cfg.act_dim)) : 0;  // A == 1 is special-cased
   hd.row_magic[3] = 0;
 
-  s->smem_bytes = size_t(hd.blob_words) * 4 +
-                  size_t(kEnvsPerBlock) * 4 * (size_t(B) * kQPFields + size_t(J) * kJointOut +
-                                               size_t(C) * kSlotOut + size_t(hd.A) + size_t(C) + 1);
-  if (s->smem_bytes > 227 * 1024)
+  for (int pi = 0; pi < kNumPlans; ++pi) {
+    DPlan& P = hd.plan[pi];
+    P.smem_bytes = smem_layout(B, J, C, hd.A, P.E, hd.blob_words).total_words * 4;
+  }
+  s->smem_bytes = size_t(hd.plan[0].smem_bytes);
+  if (size_t(hd.plan[0].smem_bytes) > 227 * 1024)
     throw Error(BRAX_E_VALIDATION, "config: system too large for one block's shared memory (" +
                                        std::to_string(s->smem_bytes) + " bytes)");
 
+  return s.release();
+}
+
+System* build_system(const Config& cfg, int device) {
+  std::unique_ptr<System> s(build_host(cfg));
+  s->device = device;
+  std::vector<uint32_t>& blob = s->blob;
+  const int B = s->hd.B;
+  std::vector<DBody> bodies(B);
+  std::memcpy(bodies.data(), blob.data() + s->hd.off_bodies, sizeof(DBody) * B);
   // ---- upload ----
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
   cuda_check(cudaMalloc(&s->d_blob, blob.size() * 4), "cudaMalloc(blob)");
   cuda_check(cudaMemcpy(s->d_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy(blob)");
   std::vector<float> dq(7 * size_t(B));

@@ -11,16 +11,6 @@
 
 namespace brax {
 
-struct StepArgs {
-  const float *pos_in, *rot_in, *vel_in, *ang_in;
-  float *pos_out, *rot_out, *vel_out, *ang_out;
-  const float* actions;        // [n_steps][n][A] (NULL iff A == 0)
-  uint32_t* status;            // [n] or NULL
-  uint8_t* contact_active;     // [n][C] or NULL
-  int64_t n_envs;
-  int64_t n_steps;
-};
-
 struct System {
   Config cfg;
   int device = 0;
@@ -33,15 +23,22 @@ struct System {
   float* d_masks = nullptr;
   std::vector<std::string> lint;
   int n_dynamic = 0;
+  int num_sms = 0;                     // of `device` (launch heuristics)
   size_t smem_bytes = 0;
   ~System();
 };
 
-// Host-side construction: tables, plan, default_qp, lint, then upload.
+// Host-side construction: tables, plan, default_qp, lint (no GPU needed).
+System* build_host(const Config& cfg);
+// build_host + upload to `device`.
 System* build_system(const Config& cfg, int device);
 
 // default_qp in double precision (host), B rows.
 void default_qp(const Config& cfg, std::vector<double>& pos, std::vector<double>& rot);
+
+
+// Lane-group plan index chosen for a launch of n_envs envs (step.cu).
+int choose_plan(const System& sys, int64_t n_envs);
 
 // Kernel launchers (step.cu, reset.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream);

