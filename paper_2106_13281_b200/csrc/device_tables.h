@@ -26,7 +26,6 @@ namespace brax {
 
 constexpr int kEnvsPerBlock = 32;  // lane = env; warp = work item
 constexpr int kMaxWarps = 16;      // 512 threads per block at most
-constexpr int kMaxRegs = 80;       // registers per thread of the step kernel
 
 // Flag bits (precomputed on the host; warp-uniform tests in the kernel).  An
 // exact-zero offset, identity frame, isotropic inertia or all-free mask makes the
@@ -128,9 +127,9 @@ struct StepArgs {
 // lanes form G groups of E lanes; group g runs item items[step*G + g] on the
 // block's E envs (-1 = idle).  Items sharing a step have the same code class,
 // so the groups do not diverge.
-constexpr int kNumPlans = 3;       // G = 1, 2, 4
+constexpr int kNumPlans = 6;       // (G, V) = (1,1) (2,1) (4,1) (1,2) (2,2) (4,2)
 struct DPlan {
-  int32_t G, E, W, log2E;
+  int32_t G, V, E, W;  // lane groups per warp, envs per lane, envs per block E = 32·V/G, warps
   int32_t off_item_begin, off_items;          // per warp: item steps [begin, end); items[step*G + g]
   int32_t off_body_begin, off_bodies_of_warp;  // per warp: body steps; bodies[step*G + g]
   int32_t smem_bytes, pad0, pad1, pad2;

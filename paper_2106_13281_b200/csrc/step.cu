@@ -14,9 +14,9 @@
 //     brax_rollout), and written back once.
 //   * per-body sums are gathers over static incidence lists in a fixed order
 //     (joints by index, then contact slots by index): no atomics.
-//   * per substep: phase 1 kinematic integrator (body warps) | barrier |
-//     phase 2 joints+actuators and contacts (item warps) | barrier |
-//     phase 3 gather + potential + collision integrators (body warps).
+//   * per substep: phase 1 joints+actuators and contacts (item warps) | barrier |
+//     phase 2 gather + potential + collision integrators, fused with the next
+//     substep's kinematic integrator (body warps) | barrier.
 // The static tables are staged into shared memory and read with broadcast
 // LDS.128; the code is shared by all warps, which keeps the instruction
 // footprint small (a per-system specialised variant with the
@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "step_device.cuh"
@@ -43,7 +44,11 @@ struct KArgs {
 };
 
 // Register budget: 80 per thread keeps 2 blocks of up to 12 warps resident per SM.
-__global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ KArgs ka) {
+// S = float: one env per lane; F2: two envs per lane.  R: register budget per
+// thread (instantiated for several budgets; launch_step picks the largest that
+// keeps two blocks resident per SM).
+template <class S, int R>
+__global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka) {
   extern __shared__ __align__(16) uint32_t smem[];
   const DHeader& H = ka.hd;
   const DPlan& P = H.plan[ka.plan];
@@ -58,11 +63,13 @@ __global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ K
   float* stg = reinterpret_cast<float*>(smem + L.u);  // aliases sJ/sC outside the substeps
   float* sA = reinterpret_cast<float*>(smem + L.a);
   float* sAstg = reinterpret_cast<float*>(smem + L.astg);
-  int* sCnt = reinterpret_cast<int*>(smem + L.cnt);
+  float* sCnt = reinterpret_cast<float*>(smem + L.cnt);
   uint32_t* sStat = smem + L.stat;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grp = lane >> P.log2E, el = lane & (E - 1);  // lane group, env slot within the block
+  const int LG = 32 / G;                                 // lanes per group
+  const int grp = lane / LG, el = lane - grp * LG;       // lane group; first env slot of this lane
+  const int o2q = LG * kQS, o2j = LG * kJS, o2c = LG * kCS;  // second env (S = F2): + LG slots
   const int64_t e0 = int64_t(blockIdx.x) * E;
   const int nvalid = (a.n_envs - e0 < E) ? int(a.n_envs - e0) : E;
   const bool bulk = a.bulk_ok && nvalid == E;          // block-uniform
@@ -97,7 +104,7 @@ __global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ K
   if (!bulk) load_block(a, sQ, sStat, B, E, e0, nvalid);  // ragged tail / unaligned: per-row loads
   mbar_wait(&bars[0], 0);
   if (bulk) stg_to_records(stg, sQ, B, E, E);
-  if (tid < E) sStat[tid] = 0u;
+  for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
   __syncthreads();
 
   const DBody* bodies = reinterpret_cast<const DBody*>(sBlob + H.off_bodies);
@@ -115,8 +122,12 @@ __global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ K
   const float* sCe = sC + el * kCS;
   const int it0 = item_begin[warp], it1 = item_begin[warp + 1];
   const int bw0 = body_begin[warp], bw1 = body_begin[warp + 1];
-  const V3 g{H.g[0], H.g[1], H.g[2]};
 
+  // S2 of the first substep; every later S2 is fused into the previous substep's integrate()
+  for (int i = bw0; i < bw1; ++i) {
+    int b = bodies_of_warp[i * G];
+    if (b >= 0) kinematic<S>(bodies[b], Row<S>{sQ + (b * E + el) * kQS, o2q}, H.h);
+  }
   for (int64_t step = 0; step < a.n_steps; ++step) {
     if (act_bulk) {  // this step's actions arrived in sAstg [E][A]; transpose to sA [A][E]
       mbar_wait(&bars[1], uint32_t(step & 1));
@@ -129,13 +140,12 @@ __global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ K
     }  // sA is read in phase 2, after a barrier
     for (int it = it0; it < it1; ++it) {
       int item = items[it * G];
-      if (item >= J) sCnt[(item - J) * E + el] = 0;
+      if (item >= J) {
+        sCnt[(item - J) * E + el] = 0.f;
+        if (LG != E) sCnt[(item - J) * E + el + LG] = 0.f;
+      }
     }
     for (int s = 0; s < H.S; ++s) {
-      for (int i = bw0; i < bw1; ++i) {
-        int b = bodies_of_warp[i * G];
-        if (b >= 0) kinematic(bodies[b], row(sQ, b, el, E), H.h);
-      }
       __syncthreads();
       if (act_bulk && s == 0 && tid == 0 && step + 1 < a.n_steps) {  // prefetch next step's actions
         mbar_expect_tx(&bars[1], act_bytes);
@@ -146,29 +156,33 @@ __global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ K
         if (item < 0) continue;
         if (item < J) {
           const DJoint& jt = joints[item];
-          joint(jt, row(sQ, jt.parent, el, E), row(sQ, jt.child, el, E), sA + el, E,
-                sJ + (item * E + el) * kJS);
+          joint<S>(jt, Row<S>{sQ + (jt.parent * E + el) * kQS, o2q}, Row<S>{sQ + (jt.child * E + el) * kQS, o2q},
+                   sA + el, E, LG, sJ + (item * E + el) * kJS, o2j);
         } else {
           int c = item - J;
           const DSlot& sl = slots[c];
-          contact(sl, row(sQ, sl.a, el, E), row(sQ, sl.b, el, E), 1.f + H.e, H.beta_over_h, H.mu,
-                  sC + (c * E + el) * kCS, sCnt + c * E + el);
+          float* cp = sCnt + c * E + el;
+          S cnt = Lanes<S>::ld(cp, LG);
+          contact<S>(sl, Row<S>{sQ + (sl.a * E + el) * kQS, o2q}, Row<S>{sQ + (sl.b * E + el) * kQS, o2q},
+                     1.f + H.e, H.beta_over_h, H.mu, sC + (c * E + el) * kCS, o2c, cnt);
+          store_count(cp, LG, cnt);
         }
       }
       __syncthreads();
       for (int i = bw0; i < bw1; ++i) {
         int b = bodies_of_warp[i * G];
         if (b < 0) continue;
-        Acc acc;
+        Acc<S> acc;
         for (int k = jinc_begin[b]; k < jinc_begin[b + 1]; ++k) {
           int e = jinc[k];
-          acc.joint(sJe + (e >> 4) * (E * kJS), e);
+          acc.joint(sJe + (e >> 4) * (E * kJS), o2j, e);
         }
         for (int k = cinc_begin[b]; k < cinc_begin[b + 1]; ++k) {
           int e = cinc[k];
-          acc.slot(sCe + (e >> 4) * (E * kCS), e);
+          acc.slot(sCe + (e >> 4) * (E * kCS), o2c, e);
         }
-        integrate(bodies[b], row(sQ, b, el, E), acc, H.h, g);
+        const bool kin = !(step + 1 == a.n_steps && s + 1 == H.S);  // fused S2 of the next substep
+        integrate<S>(bodies[b], Row<S>{sQ + (b * E + el) * kQS, o2q}, acc, H.h, H.g, kin);
       }
     }
   }
@@ -195,7 +209,7 @@ __global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ K
   }
   if (a.status) {
     __syncthreads();
-    if (tid < nvalid) a.status[e0 + tid] = sStat[tid];
+    for (int i = tid; i < nvalid; i += blockDim.x) a.status[e0 + i] = sStat[i];
   }
 }
 
@@ -205,27 +219,55 @@ __global__ void __maxnreg__(kMaxRegs) brax_step_kernel(const __grid_constant__ K
 // alone would leave the SMs with few independent env groups to overlap their
 // per-substep barriers; G = 1 once the grid fills the GPU.
 int choose_plan(const System& sys, int64_t n_envs) {
-  if (const char* e = std::getenv("BRAX_LANE_GROUPS")) {
-    int g = std::atoi(e);
-    if (g == 1) return 0;
-    if (g == 2) return 1;
-    if (g == 4) return 2;
+  if (const char* e = std::getenv("BRAX_PLAN")) {  // "G,V" override (experiments)
+    int g = 0, v = 0;
+    if (std::sscanf(e, "%d,%d", &g, &v) == 2)
+      for (int i = 0; i < kNumPlans; ++i)
+        if (sys.hd.plan[i].G == g && sys.hd.plan[i].V == v) return i;
   }
   int sms = sys.num_sms > 0 ? sys.num_sms : 148;
   int64_t blocks32 = (n_envs + 31) / 32;
-  if (blocks32 >= 6 * sms) return 0;
-  if (blocks32 >= 3 * sms) return 1;
-  return 2;
+  // measured (profiles/): G = 2 helps only while 32-env blocks leave SMs idle
+  return blocks32 < sms ? 1 : 0;
 }
+
+// Register budget per thread: as many as possible while the SM still holds the
+// number of blocks the grid can use (B200: 148 SMs, 64 K registers = 4 SMSPs x
+// 16 K, 228 KB shared memory, 64 warps).  Measured (profiles/): more registers
+// buy ILP for latency-bound small batches, occupancy wins for large ones.
+int choose_regs(const System& sys, const DPlan& P, int64_t grid) {
+  if (const char* e = std::getenv("BRAX_MAXREG")) return std::atoi(e);
+  const int sms = sys.num_sms > 0 ? sys.num_sms : 148;
+  const int64_t want = (grid + sms - 1) / sms;
+  const int by_smem = (228 * 1024) / (P.smem_bytes + 1024);
+  const int by_warps = 64 / P.W;
+  int blocks = int(want < 8 ? want : 8);
+  blocks = blocks < by_smem ? blocks : by_smem;
+  blocks = blocks < by_warps ? blocks : by_warps;
+  blocks = blocks < 1 ? 1 : blocks;
+  const int warps_per_smsp = (blocks * P.W + 3) / 4;
+  return (16384 / (warps_per_smsp * 32)) & ~7;
+}
+
+namespace {
+template <class S, int R>
+cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(brax_step_kernel<S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  brax_step_kernel<S, R><<<grid, block, smem, stream>>>(ka);
+  return cudaGetLastError();
+}
+}  // namespace
 
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream) {
   if (a.n_envs <= 0 || a.n_steps <= 0) return cudaSuccess;
-  static bool attr_set[64] = {};
-  if (sys.device >= 0 && sys.device < 64 && !attr_set[sys.device]) {
-    cudaError_t e = cudaFuncSetAttribute(brax_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set[sys.device] = true;
-  }
   KArgs ka{a, sys.d_blob, sys.hd, choose_plan(sys, a.n_envs)};
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
@@ -234,8 +276,18 @@ cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t strea
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
   const DPlan& P = sys.hd.plan[ka.plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
-  brax_step_kernel<<<grid, block, size_t(P.smem_bytes), stream>>>(ka);
-  return cudaGetLastError();
+  const size_t smem = size_t(P.smem_bytes);
+  const int regs = choose_regs(sys, P, int64_t(grid.x));
+  if (P.V == 2) {
+    if (regs >= 128) return launch_variant<F2, 128>(ka, grid, block, smem, stream);
+    if (regs >= 96) return launch_variant<F2, 96>(ka, grid, block, smem, stream);
+    return launch_variant<F2, 80>(ka, grid, block, smem, stream);
+  }
+  if (regs >= 128) return launch_variant<float, 128>(ka, grid, block, smem, stream);
+  if (regs >= 112) return launch_variant<float, 112>(ka, grid, block, smem, stream);
+  if (regs >= 96) return launch_variant<float, 96>(ka, grid, block, smem, stream);
+  if (regs >= 80) return launch_variant<float, 80>(ka, grid, block, smem, stream);
+  return launch_variant<float, 64>(ka, grid, block, smem, stream);
 }
 
 }  // namespace brax

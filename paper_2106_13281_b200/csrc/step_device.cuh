@@ -2,8 +2,14 @@
 //
 // Formulas: Alg. 1 of the paper with SURVEY.md §8(c).1 /
 // DESIGN.md "Readings"; see the per-function citations.  Shared-memory
-// records are float4-aligned (device_tables.h: kQS, kJS, kCS) so state,
-// parameters and per-item outputs move with LDS.128 / STS.128.
+// records are float4-aligned (device_tables.h: kQS, kJS, kCS) so state and
+// per-item outputs move with LDS.128 / STS.128.
+//
+// The physics is templated on the per-lane scalar S: `float` (one env per
+// lane) or `F2` (two envs per lane: every parameter load, branch and address
+// computation then serves two envs, and the two independent dependency chains
+// double the instruction-level parallelism).  Conditions that differ between
+// envs (contact activity, clamps, signs) are selects, never branches.
 #pragma once
 #include <stdint.h>
 
@@ -12,173 +18,272 @@
 namespace brax {
 namespace dev {
 
-struct V3 { float x, y, z; };
-struct Q4 { float w, x, y, z; };
+// ---- per-lane scalar types -----------------------------------------------------
+struct F2 { float x, y; };
+struct B2 { bool x, y; };
 
-__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-__device__ __forceinline__ V3 operator*(float s, V3 a) { return {s * a.x, s * a.y, s * a.z}; }
-__device__ __forceinline__ V3 had(V3 a, V3 b) { return {a.x * b.x, a.y * b.y, a.z * b.z}; }
-__device__ __forceinline__ float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ F2 operator*(F2 a, F2 b) { return {a.x * b.x, a.y * b.y}; }
+__device__ __forceinline__ F2 operator-(F2 a) { return {-a.x, -a.y}; }
+__device__ __forceinline__ F2 operator+(F2 a, float b) { return {a.x + b, a.y + b}; }
+__device__ __forceinline__ F2 operator+(float a, F2 b) { return {a + b.x, a + b.y}; }
+__device__ __forceinline__ F2 operator-(F2 a, float b) { return {a.x - b, a.y - b}; }
+__device__ __forceinline__ F2 operator-(float a, F2 b) { return {a - b.x, a - b.y}; }
+__device__ __forceinline__ F2 operator*(float a, F2 b) { return {a * b.x, a * b.y}; }
+__device__ __forceinline__ F2 operator*(F2 a, float b) { return {a.x * b, a.y * b}; }
+
+__device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ F2 vmin(F2 a, F2 b) { return {fminf(a.x, b.x), fminf(a.y, b.y)}; }
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ F2 vmax(F2 a, F2 b) { return {fmaxf(a.x, b.x), fmaxf(a.y, b.y)}; }
+__device__ __forceinline__ float vabs(float a) { return fabsf(a); }
+__device__ __forceinline__ F2 vabs(F2 a) { return {fabsf(a.x), fabsf(a.y)}; }
+__device__ __forceinline__ float vsqrt(float a) { return sqrtf(a); }
+__device__ __forceinline__ F2 vsqrt(F2 a) { return {sqrtf(a.x), sqrtf(a.y)}; }
+__device__ __forceinline__ float vrsqrt(float a) { return rsqrtf(a); }
+__device__ __forceinline__ F2 vrsqrt(F2 a) { return {rsqrtf(a.x), rsqrtf(a.y)}; }
+__device__ __forceinline__ float vdiv(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ F2 vdiv(F2 a, F2 b) { return {__fdividef(a.x, b.x), __fdividef(a.y, b.y)}; }
+__device__ __forceinline__ float vcopysign(float a, float b) { return copysignf(a, b); }
+__device__ __forceinline__ F2 vcopysign(F2 a, F2 b) { return {copysignf(a.x, b.x), copysignf(a.y, b.y)}; }
+__device__ __forceinline__ bool lt(float a, float b) { return a < b; }
+__device__ __forceinline__ B2 lt(F2 a, F2 b) { return {a.x < b.x, a.y < b.y}; }
+__device__ __forceinline__ bool gt(float a, float b) { return a > b; }
+__device__ __forceinline__ B2 gt(F2 a, F2 b) { return {a.x > b.x, a.y > b.y}; }
+__device__ __forceinline__ float sel(bool m, float a, float b) { return m ? a : b; }
+__device__ __forceinline__ F2 sel(B2 m, F2 a, F2 b) { return {m.x ? a.x : b.x, m.y ? a.y : b.y}; }
+__device__ __forceinline__ bool both(bool m, bool n) { return m && n; }
+__device__ __forceinline__ B2 both(B2 m, B2 n) { return {m.x && n.x, m.y && n.y}; }
+__device__ __forceinline__ bool any(bool m) { return m; }
+__device__ __forceinline__ bool any(B2 m) { return m.x || m.y; }
+__device__ __forceinline__ float as_count(bool m) { return m ? 1.f : 0.f; }
+__device__ __forceinline__ F2 as_count(B2 m) { return {m.x ? 1.f : 0.f, m.y ? 1.f : 0.f}; }
+template <class S> __device__ __forceinline__ S bc(float f);
+template <> __device__ __forceinline__ float bc<float>(float f) { return f; }
+template <> __device__ __forceinline__ F2 bc<F2>(float f) { return {f, f}; }
+template <class S> __device__ __forceinline__ S clampv(S x, float lo, float hi) {
+  return vmin(vmax(x, bc<S>(lo)), bc<S>(hi));
+}
+
+template <class S> struct V3T { S x, y, z; };
+template <class S> struct Q4T { S w, x, y, z; };
+template <class S> __device__ __forceinline__ V3T<S> operator+(V3T<S> a, V3T<S> b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+template <class S> __device__ __forceinline__ V3T<S> operator-(V3T<S> a, V3T<S> b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+template <class S> __device__ __forceinline__ V3T<S> operator*(S s, V3T<S> a) { return {s * a.x, s * a.y, s * a.z}; }
+template <class S> __device__ __forceinline__ V3T<S> scale(float s, V3T<S> a) { return {s * a.x, s * a.y, s * a.z}; }
+template <class S> __device__ __forceinline__ V3T<S> had(const float* m, V3T<S> a) { return {m[0] * a.x, m[1] * a.y, m[2] * a.z}; }
+template <class S> __device__ __forceinline__ S dot(V3T<S> a, V3T<S> b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+template <class S> __device__ __forceinline__ V3T<S> cross(V3T<S> a, V3T<S> b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
-__device__ __forceinline__ Q4 qmul(Q4 a, Q4 b) {
+template <class S> __device__ __forceinline__ V3T<S> bc3(const float* p) { return {bc<S>(p[0]), bc<S>(p[1]), bc<S>(p[2])}; }
+template <class S> __device__ __forceinline__ Q4T<S> bcq(const float* p) {
+  return {bc<S>(p[0]), bc<S>(p[1]), bc<S>(p[2]), bc<S>(p[3])};
+}
+template <class S> __device__ __forceinline__ V3T<S> sel3(decltype(lt(S(), S())) m, V3T<S> a, V3T<S> b) {
+  return {sel(m, a.x, b.x), sel(m, a.y, b.y), sel(m, a.z, b.z)};
+}
+template <class S> __device__ __forceinline__ Q4T<S> qmul(Q4T<S> a, Q4T<S> b) {
   return {a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
           a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x, a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w};
 }
-__device__ __forceinline__ Q4 qconj(Q4 q) { return {q.w, -q.x, -q.y, -q.z}; }
+template <class S> __device__ __forceinline__ Q4T<S> qconj(Q4T<S> q) { return {q.w, -q.x, -q.y, -q.z}; }
 // rotate(q, v) = v + w·t + u×t, t = 2u×v
-__device__ __forceinline__ V3 rotate(Q4 q, V3 v) {
-  V3 u{q.x, q.y, q.z};
-  V3 t = 2.f * cross(u, v);
+template <class S> __device__ __forceinline__ V3T<S> rotate(Q4T<S> q, V3T<S> v) {
+  V3T<S> u{q.x, q.y, q.z};
+  V3T<S> t = scale(2.f, cross(u, v));
   return v + q.w * t + cross(u, t);
 }
+// rotate(q, ẑ): the third column of R(q)
+template <class S> __device__ __forceinline__ V3T<S> rotate_z(Q4T<S> q) {
+  return {2.f * (q.x * q.z + q.w * q.y), 2.f * (q.y * q.z - q.w * q.x), 1.f - 2.f * (q.x * q.x + q.y * q.y)};
+}
 // I_w⁻¹(q)·v = rotate(q, inv_rotate(q, v) ⊙ I_b⁻¹)   (R4); isotropic: i·v exactly
-__device__ __forceinline__ V3 iw(Q4 q, const float* inv_i, bool iso, V3 v) {
-  if (iso) return inv_i[0] * v;
-  return rotate(q, had(rotate(qconj(q), v), V3{inv_i[0], inv_i[1], inv_i[2]}));
+template <class S> __device__ __forceinline__ V3T<S> iw(Q4T<S> q, const float* inv_i, bool iso, V3T<S> v) {
+  if (iso) return scale(inv_i[0], v);
+  return rotate(q, had(inv_i, rotate(qconj(q), v)));
 }
-__device__ __forceinline__ V3 v3(const float* p) { return {p[0], p[1], p[2]}; }
-__device__ __forceinline__ Q4 q4(const float* p) {
-  float4 v = *reinterpret_cast<const float4*>(p);
-  return {v.x, v.y, v.z, v.w};
-}
-__device__ __forceinline__ float clampf(float x, float lo, float hi) { return fminf(fmaxf(x, lo), hi); }
 
 // atan2 for fp32: range reduction to [0, 1] and a degree-8 polynomial in a²
 // (least-squares/minimax fit of atan(a)/a; max error ≈ 1.0e-7 rad in fp32).
-__device__ __forceinline__ float atan2_f(float y, float x) {
-  float ax = fabsf(x), ay = fabsf(y);
-  float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  float a = (mx > 0.f) ? __fdividef(mn, mx) : 0.f;
-  float s = a * a;
-  float p = 0.002456719521433115f;
-  p = fmaf(p, s, -0.014401338994503021f);
-  p = fmaf(p, s, 0.03978119418025017f);
-  p = fmaf(p, s, -0.07234854996204376f);
-  p = fmaf(p, s, 0.1049894466996193f);
-  p = fmaf(p, s, -0.14161229133605957f);
-  p = fmaf(p, s, 0.19985906779766083f);
-  p = fmaf(p, s, -0.33332598209381104f);
-  p = fmaf(p, s, 0.9999998807907104f);
-  float r = p * a;
-  r = (ay > ax) ? 1.5707963267948966f - r : r;
-  r = (x < 0.f) ? 3.141592653589793f - r : r;
-  return copysignf(r, y);
+template <class S> __device__ __forceinline__ S atan2_f(S y, S x) {
+  S ax = vabs(x), ay = vabs(y);
+  S mx = vmax(ax, ay), mn = vmin(ax, ay);
+  S a = sel(gt(mx, bc<S>(0.f)), vdiv(mn, mx), bc<S>(0.f));
+  S s = a * a;
+  S p = bc<S>(0.002456719521433115f);
+  p = p * s + -0.014401338994503021f;
+  p = p * s + 0.03978119418025017f;
+  p = p * s + -0.07234854996204376f;
+  p = p * s + 0.1049894466996193f;
+  p = p * s + -0.14161229133605957f;
+  p = p * s + 0.19985906779766083f;
+  p = p * s + -0.33332598209381104f;
+  p = p * s + 0.9999998807907104f;
+  S r = p * a;
+  r = sel(gt(ay, ax), 1.5707963267948966f - r, r);
+  r = sel(lt(x, bc<S>(0.f)), 3.141592653589793f - r, r);
+  return vcopysign(r, y);
 }
 // asin(x) = atan2(x, √((1−x)(1+x))), x already clamped to [−1, 1]
-__device__ __forceinline__ float asin_f(float x) { return atan2_f(x, sqrtf((1.f - x) * (1.f + x))); }
+template <class S> __device__ __forceinline__ S asin_f(S x) { return atan2_f(x, vsqrt((1.f - x) * (1.f + x))); }
 
-// QP record of one (body, lane) in shared memory: pos | rot | vel | ang, float4 each
-struct Row {
-  float* p;  // = sQ + (b*E + env) * kQS
-  __device__ __forceinline__ V3 pos() const { float4 v = *reinterpret_cast<float4*>(p); return {v.x, v.y, v.z}; }
-  __device__ __forceinline__ Q4 rot() const { float4 v = *reinterpret_cast<float4*>(p + 4); return {v.x, v.y, v.z, v.w}; }
-  __device__ __forceinline__ V3 vel() const { float4 v = *reinterpret_cast<float4*>(p + 8); return {v.x, v.y, v.z}; }
-  __device__ __forceinline__ V3 ang() const { float4 v = *reinterpret_cast<float4*>(p + 12); return {v.x, v.y, v.z}; }
-  __device__ __forceinline__ void set_pos(V3 v) const { *reinterpret_cast<float4*>(p) = make_float4(v.x, v.y, v.z, 0.f); }
-  __device__ __forceinline__ void set_rot(Q4 q) const { *reinterpret_cast<float4*>(p + 4) = make_float4(q.w, q.x, q.y, q.z); }
-  __device__ __forceinline__ void set_vel(V3 v) const { *reinterpret_cast<float4*>(p + 8) = make_float4(v.x, v.y, v.z, 0.f); }
-  __device__ __forceinline__ void set_ang(V3 v) const { *reinterpret_cast<float4*>(p + 12) = make_float4(v.x, v.y, v.z, 0.f); }
+// ---- shared-memory access for V = 1 or 2 envs per lane ---------------------------
+// A lane of a group of L lanes handles env slot `el` and (S = F2) `el + L`; the
+// second env's record sits `o2` words after the first's.
+__device__ __forceinline__ float ld1(const float* p, int) { return *p; }
+__device__ __forceinline__ F2 ld2(const float* p, int o2) { return {p[0], p[o2]}; }
+template <class S> struct Lanes;
+template <> struct Lanes<float> {
+  static __device__ __forceinline__ float4 ld4(const float* p, int) { return *reinterpret_cast<const float4*>(p); }
+  static __device__ __forceinline__ V3T<float> ld3(const float* p, int o2) {
+    float4 a = ld4(p, o2);
+    return {a.x, a.y, a.z};
+  }
+  static __device__ __forceinline__ Q4T<float> ldq(const float* p, int o2) {
+    float4 a = ld4(p, o2);
+    return {a.x, a.y, a.z, a.w};
+  }
+  static __device__ __forceinline__ void st3(float* p, int, V3T<float> v, float w = 0.f) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.x, v.y, v.z, w);
+  }
+  static __device__ __forceinline__ void stq(float* p, int, Q4T<float> q) {
+    *reinterpret_cast<float4*>(p) = make_float4(q.w, q.x, q.y, q.z);
+  }
+  static __device__ __forceinline__ float ld(const float* p, int) { return *p; }
+  static __device__ __forceinline__ float w4(const float* p, int) { return p[3]; }
 };
-// record of body b for env-slot `el` of a block holding E envs
-__device__ __forceinline__ Row row(float* sQ, int b, int el, int E) { return Row{sQ + (b * E + el) * kQS}; }
+template <> struct Lanes<F2> {
+  static __device__ __forceinline__ V3T<F2> ld3(const float* p, int o2) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + o2);
+    return {{a.x, b.x}, {a.y, b.y}, {a.z, b.z}};
+  }
+  static __device__ __forceinline__ Q4T<F2> ldq(const float* p, int o2) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + o2);
+    return {{a.x, b.x}, {a.y, b.y}, {a.z, b.z}, {a.w, b.w}};
+  }
+  static __device__ __forceinline__ void st3(float* p, int o2, V3T<F2> v, F2 w = {0.f, 0.f}) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.x.x, v.y.x, v.z.x, w.x);
+    *reinterpret_cast<float4*>(p + o2) = make_float4(v.x.y, v.y.y, v.z.y, w.y);
+  }
+  static __device__ __forceinline__ void stq(float* p, int o2, Q4T<F2> q) {
+    *reinterpret_cast<float4*>(p) = make_float4(q.w.x, q.x.x, q.y.x, q.z.x);
+    *reinterpret_cast<float4*>(p + o2) = make_float4(q.w.y, q.x.y, q.y.y, q.z.y);
+  }
+  static __device__ __forceinline__ F2 ld(const float* p, int o2) { return {p[0], p[o2]}; }
+  static __device__ __forceinline__ F2 w4(const float* p, int o2) { return {p[3], p[o2 + 3]}; }
+};
+
+// QP record of one (body, env) in shared memory: pos | rot | vel | ang, float4 each
+template <class S> struct Row {
+  float* p;  // = sQ + (b*E + env) * kQS
+  int o2;    // second env's record (S = F2): + L·kQS words
+  __device__ __forceinline__ V3T<S> pos() const { return Lanes<S>::ld3(p, o2); }
+  __device__ __forceinline__ Q4T<S> rot() const { return Lanes<S>::ldq(p + 4, o2); }
+  __device__ __forceinline__ V3T<S> vel() const { return Lanes<S>::ld3(p + 8, o2); }
+  __device__ __forceinline__ V3T<S> ang() const { return Lanes<S>::ld3(p + 12, o2); }
+  __device__ __forceinline__ void set_pos(V3T<S> v) const { Lanes<S>::st3(p, o2, v); }
+  __device__ __forceinline__ void set_rot(Q4T<S> q) const { Lanes<S>::stq(p + 4, o2, q); }
+  __device__ __forceinline__ void set_vel(V3T<S> v) const { Lanes<S>::st3(p + 8, o2, v); }
+  __device__ __forceinline__ void set_ang(V3T<S> v) const { Lanes<S>::st3(p + 12, o2, v); }
+};
 
 // ---- S2: kinematic integrator (R3, R21) -------------------------
-__device__ __forceinline__ void kinematic(const DBody& bd, Row r, float h) {
-  V3 v = r.vel();
-  if (!(bd.flags & kFlagFreePos)) v = had(v3(bd.mpos), v);
-  r.set_pos(r.pos() + h * v);
+template <class S> __device__ __forceinline__ void kinematic(const DBody& bd, Row<S> r, float h) {
+  V3T<S> v = r.vel();
+  if (!(bd.flags & kFlagFreePos)) v = had(bd.mpos, v);
+  r.set_pos(r.pos() + scale(h, v));
   if (!bd.rot_frozen) {
-    V3 w = r.ang();
-    if (!(bd.flags & kFlagFreeRot)) w = had(v3(bd.mrot), w);
-    Q4 q = r.rot();
-    Q4 dq = qmul(Q4{0.f, w.x, w.y, w.z}, q);
-    float hh = 0.5f * h;
-    q = Q4{q.w + hh * dq.w, q.x + hh * dq.x, q.y + hh * dq.y, q.z + hh * dq.z};
-    float n2 = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
-    float inv = rsqrtf(n2);
+    V3T<S> w = r.ang();
+    if (!(bd.flags & kFlagFreeRot)) w = had(bd.mrot, w);
+    Q4T<S> q = r.rot();
+    Q4T<S> dq = qmul(Q4T<S>{bc<S>(0.f), w.x, w.y, w.z}, q);
+    const float hh = 0.5f * h;
+    q = Q4T<S>{q.w + hh * dq.w, q.x + hh * dq.x, q.y + hh * dq.y, q.z + hh * dq.z};
+    S n2 = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    S inv = vrsqrt(n2);
     inv = inv * (1.5f - 0.5f * n2 * inv * inv);  // one Newton step: ≈ correctly rounded 1/√n2
-    r.set_rot(Q4{q.w * inv, q.x * inv, q.y * inv, q.z * inv});
+    r.set_rot(Q4T<S>{q.w * inv, q.x * inv, q.y * inv, q.z * inv});
   }
 }
 
 // ---- S3 + S4: joint spring/limits with its actuator (R5, R7-R12)
-// act: this env's column of the block's actions sA[k][env] (stride E).
+// act: this env's column of the block's actions sA[k][env] (row stride E, second env + L).
 // out: this (joint, env) record: F on child | T child | T parent.
-// Zero offsets / identity frames are computed through (exact results, no
-// branches: better ILP); only the optional damping term and the actuator are
-// guarded, by flags that are uniform across a warp's lane groups.
-__device__ __forceinline__ void joint(const DJoint& J, Row P, Row C, const float* act, int E, float* out) {
-  Q4 qp = P.rot(), qc = C.rot();
-  V3 rp = rotate(qp, v3(J.o_p));
-  V3 rc = rotate(qc, v3(J.o_c));
-  V3 dx = (P.pos() - C.pos()) + (rp - rc);
-  V3 wp = P.ang(), wc = C.ang();
-  V3 f = J.k * dx;
-  if (!(J.flags & kJNoCl)) f = f + J.c_l * ((P.vel() + cross(wp, rp)) - (C.vel() + cross(wc, rc)));
-  Q4 fp = qmul(qp, q4(J.jp));
-  Q4 fc = qmul(qc, q4(J.jc));
-  Q4 qr = qmul(qconj(fp), fc);
-  float sg = (qr.w < 0.f) ? -1.f : 1.f;  // canonicalise q_r to w >= 0 (R25)
-  qr = Q4{sg * qr.w, sg * qr.x, sg * qr.y, sg * qr.z};
-  float R02 = 2.f * (qr.x * qr.z + qr.w * qr.y);
-  float R12 = 2.f * (qr.y * qr.z - qr.w * qr.x);
-  float R22 = 1.f - 2.f * (qr.x * qr.x + qr.y * qr.y);
-  float R01 = 2.f * (qr.x * qr.y - qr.w * qr.z);
-  float R00 = 1.f - 2.f * (qr.y * qr.y + qr.z * qr.z);
-  float th[3] = {atan2_f(-R12, R22), asin_f(clampf(R02, -1.f, 1.f)), atan2_f(-R01, R00)};
-  float tau[3];
+template <class S>
+__device__ __forceinline__ void joint(const DJoint& J, Row<S> P, Row<S> C, const float* act, int E, int L,
+                                      float* out, int o2) {
+  Q4T<S> qp = P.rot(), qc = C.rot();
+  V3T<S> rp = rotate(qp, bc3<S>(J.o_p));
+  V3T<S> rc = rotate(qc, bc3<S>(J.o_c));
+  V3T<S> dx = (P.pos() - C.pos()) + (rp - rc);
+  V3T<S> wp = P.ang(), wc = C.ang();
+  V3T<S> f = scale(J.k, dx);
+  if (!(J.flags & kJNoCl))
+    f = f + scale(J.c_l, (P.vel() + cross(wp, rp)) - (C.vel() + cross(wc, rc)));
+  Q4T<S> fp = qmul(qp, bcq<S>(J.jp));
+  Q4T<S> fc = qmul(qc, bcq<S>(J.jc));
+  Q4T<S> qr = qmul(qconj(fp), fc);
+  S sg = sel(lt(qr.w, bc<S>(0.f)), bc<S>(-1.f), bc<S>(1.f));  // canonicalise q_r to w >= 0 (R25)
+  qr = Q4T<S>{sg * qr.w, sg * qr.x, sg * qr.y, sg * qr.z};
+  S R02 = 2.f * (qr.x * qr.z + qr.w * qr.y);
+  S R12 = 2.f * (qr.y * qr.z - qr.w * qr.x);
+  S R22 = 1.f - 2.f * (qr.x * qr.x + qr.y * qr.y);
+  S R01 = 2.f * (qr.x * qr.y - qr.w * qr.z);
+  S R00 = 1.f - 2.f * (qr.y * qr.y + qr.z * qr.z);
+  S th[3] = {atan2_f(-R12, R22), asin_f(clampv(R02, -1.f, 1.f)), atan2_f(-R01, R00)};
+  S tau[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const bool free_axis = i < J.dof;
-    tau[i] = free_axis ? J.k_l * (clampf(th[i], J.lo[i], J.hi[i]) - th[i]) : -(J.k_a * th[i]);
+    if (i < J.dof) tau[i] = J.k_l * (clampv(th[i], J.lo[i], J.hi[i]) - th[i]);
+    else tau[i] = -(J.k_a * th[i]);
   }
   if (J.act_kind >= 0) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       if (i < J.dof) {
-        float a = act[(J.act_offset + i) * E];
-        tau[i] += (J.act_kind == 0) ? J.strength * clampf(a, -1.f, 1.f)
-                                    : J.strength * (clampf(a, J.lo[i], J.hi[i]) - th[i]);
+        S a = Lanes<S>::ld(act + (J.act_offset + i) * E, L);
+        tau[i] = tau[i] + ((J.act_kind == 0) ? J.strength * clampv(a, -1.f, 1.f)
+                                             : J.strength * (clampv(a, J.lo[i], J.hi[i]) - th[i]));
       }
     }
   }
-  V3 twd = rotate(fp, V3{tau[0], tau[1], tau[2]});
-  if (!(J.flags & kJNoCa)) twd = twd + J.c_a * (wp - wc);
-  V3 tc = twd + cross(rc, f);
-  V3 tp = twd + cross(rp, f);
-  float4* o = reinterpret_cast<float4*>(out);
-  o[0] = make_float4(f.x, f.y, f.z, 0.f);
-  o[1] = make_float4(tc.x, tc.y, tc.z, 0.f);
-  o[2] = make_float4(-tp.x, -tp.y, -tp.z, 0.f);
+  V3T<S> twd = rotate(fp, V3T<S>{tau[0], tau[1], tau[2]});
+  if (!(J.flags & kJNoCa)) twd = twd + scale(J.c_a, wp - wc);
+  V3T<S> tc = twd + cross(rc, f);
+  V3T<S> tp = twd + cross(rp, f);
+  Lanes<S>::st3(out, o2, f);
+  Lanes<S>::st3(out + 4, o2, tc);
+  Lanes<S>::st3(out + 8, o2, V3T<S>{-tp.x, -tp.y, -tp.z});
 }
 
-// Closest points between segments (Ericson, Real-Time Collision Detection §5.1.9).
-__device__ __forceinline__ void seg_seg(V3 p1, V3 q1, V3 p2, V3 q2, V3& c1, V3& c2) {
-  V3 d1 = q1 - p1, d2 = q2 - p2, r = p1 - p2;
-  float a = dot(d1, d1), e = dot(d2, d2), f = dot(d2, r);
-  float s = 0.f, t = 0.f;
-  if (a <= 0.f && e <= 0.f) {
-  } else if (a <= 0.f) {
-    t = clampf(f / e, 0.f, 1.f);
+// Closest points between segments (Ericson, Real-Time Collision Detection §5.1.9),
+// with the per-env branches written as selects.  Degenerate (zero-length)
+// segments are a parameter property (uniform): a = |d1|², e = |d2|² > 0 unless ℓ = 0.
+template <class S>
+__device__ __forceinline__ void seg_seg(V3T<S> p1, V3T<S> q1, V3T<S> p2, V3T<S> q2, bool degA, bool degB,
+                                        V3T<S>& c1, V3T<S>& c2) {
+  V3T<S> d1 = q1 - p1, d2 = q2 - p2, r = p1 - p2;
+  S a = dot(d1, d1), e = dot(d2, d2), f = dot(d2, r);
+  const S zero = bc<S>(0.f);
+  S s = zero, t = zero;
+  if (degA && degB) {
+  } else if (degA) {
+    t = clampv(vdiv(f, e), 0.f, 1.f);
   } else {
-    float c = dot(d1, r);
-    if (e <= 0.f) {
-      s = clampf(-c / a, 0.f, 1.f);
+    S c = dot(d1, r);
+    if (degB) {
+      s = clampv(vdiv(-c, a), 0.f, 1.f);
     } else {
-      float b = dot(d1, d2);
-      float denom = a * e - b * b;
-      s = (denom == 0.f) ? 0.f : clampf((b * f - c * e) / denom, 0.f, 1.f);
-      t = (b * s + f) / e;
-      if (t < 0.f) {
-        t = 0.f;
-        s = clampf(-c / a, 0.f, 1.f);
-      } else if (t > 1.f) {
-        t = 1.f;
-        s = clampf((b - c) / a, 0.f, 1.f);
-      }
+      S b = dot(d1, d2);
+      S denom = a * e - b * b;
+      s = sel(gt(vabs(denom), zero), clampv(vdiv(b * f - c * e, denom), 0.f, 1.f), zero);
+      t = vdiv(b * s + f, e);
+      S s_lo = clampv(vdiv(-c, a), 0.f, 1.f), s_hi = clampv(vdiv(b - c, a), 0.f, 1.f);
+      auto tl = lt(t, zero), th = gt(t, bc<S>(1.f));
+      s = sel(tl, s_lo, sel(th, s_hi, s));
+      t = sel(tl, zero, sel(th, bc<S>(1.f), t));
     }
   }
   c1 = p1 + s * d1;
@@ -187,130 +292,160 @@ __device__ __forceinline__ void seg_seg(V3 p1, V3 q1, V3 p2, V3 q2, V3& c1, V3& 
 
 // ---- S5: contact slot, velocity-level impulse + Baumgarte (R13-R19)
 // out: this (slot, env) record: P, active | r_A×P | r_B×P; cnt: substeps active.
-__device__ __forceinline__ void contact(const DSlot& S, Row A, Row B, float opl_e, float beta_over_h, float mu,
-                                        float* out, int* cnt) {
-  const int fl = S.flags;
-  Q4 qa = A.rot(), qb = B.rot();
-  V3 xa = A.pos(), xb = B.pos();
-  V3 cA = (fl & kSZeroPa) ? xa : xa + rotate(qa, v3(S.ca_pos));
-  V3 cB = (fl & kSZeroPb) ? xb : xb + rotate(qb, v3(S.cb_pos));
-  Q4 qA = (fl & kSIdentA) ? qa : qmul(qa, q4(S.ca_rot));
-  Q4 qB = (fl & kSIdentB) ? qb : qmul(qb, q4(S.cb_rot));
-  const V3 zhat{0.f, 0.f, 1.f};
-  V3 n, pt;
-  float d;
-  if (S.type <= 2) {  // sphere / capsule end / box corner vs plane: plane is B
-    n = rotate(qB, zhat);
-    if (S.type == 2) {
-      V3 c = cA + rotate(qA, v3(S.corner));
+template <class S>
+__device__ __forceinline__ void contact(const DSlot& SL, Row<S> A, Row<S> B, float opl_e, float beta_over_h,
+                                        float mu, float* out, int o2, S& cnt) {
+  const int fl = SL.flags;
+  Q4T<S> qa = A.rot(), qb = B.rot();
+  V3T<S> xa = A.pos(), xb = B.pos();
+  V3T<S> cA = (fl & kSZeroPa) ? xa : xa + rotate(qa, bc3<S>(SL.ca_pos));
+  V3T<S> cB = (fl & kSZeroPb) ? xb : xb + rotate(qb, bc3<S>(SL.cb_pos));
+  Q4T<S> qA = (fl & kSIdentA) ? qa : qmul(qa, bcq<S>(SL.ca_rot));
+  Q4T<S> qB = (fl & kSIdentB) ? qb : qmul(qb, bcq<S>(SL.cb_rot));
+  const S zero = bc<S>(0.f);
+  V3T<S> n, pt;
+  S d;
+  if (SL.type <= 2) {  // sphere / capsule end / box corner vs plane: plane is B
+    n = rotate_z(qB);
+    if (SL.type == 2) {
+      V3T<S> c = cA + rotate(qA, bc3<S>(SL.corner));
       d = -dot(c - cB, n);
       pt = c;
     } else {
-      V3 c = (S.type == 1) ? cA + S.ell_a * rotate(qA, zhat) : cA;
-      d = S.ra - dot(c - cB, n);
-      pt = c - S.ra * n;
+      V3T<S> c = (SL.type == 1) ? cA + scale(SL.ell_a, rotate_z(qA)) : cA;
+      d = SL.ra - dot(c - cB, n);
+      pt = c - scale(SL.ra, n);
     }
   } else {
-    V3 pa = cA, pb = cB;
-    if (S.type == 4) {  // sphere (A) – capsule (B)
-      V3 axb = rotate(qB, zhat);
-      V3 e0 = cB + S.ellb * axb, e1 = cB - S.ellb * axb;
-      V3 seg = e0 - e1;
-      float L2 = dot(seg, seg);
-      float t = (L2 > 0.f) ? clampf(dot(cA - e1, seg) / L2, 0.f, 1.f) : 0.f;
-      pb = e1 + t * seg;
-    } else if (S.type == 5) {  // capsule – capsule
-      V3 axa = rotate(qA, zhat), axb = rotate(qB, zhat);
-      seg_seg(cA + S.ell_a * axa, cA - S.ell_a * axa, cB + S.ellb * axb, cB - S.ellb * axb, pa, pb);
+    V3T<S> pa = cA, pb = cB;
+    if (SL.type == 4) {  // sphere (A) – capsule (B)
+      V3T<S> axb = rotate_z(qB);
+      V3T<S> e0 = cB + scale(SL.ellb, axb), e1 = cB - scale(SL.ellb, axb);
+      V3T<S> seg = e0 - e1;
+      if (SL.ellb > 0.f) pb = e1 + clampv(vdiv(dot(cA - e1, seg), dot(seg, seg)), 0.f, 1.f) * seg;
+      else pb = e1;
+    } else if (SL.type == 5) {  // capsule – capsule
+      V3T<S> axa = rotate_z(qA), axb = rotate_z(qB);
+      seg_seg(cA + scale(SL.ell_a, axa), cA - scale(SL.ell_a, axa), cB + scale(SL.ellb, axb),
+              cB - scale(SL.ellb, axb), !(SL.ell_a > 0.f), !(SL.ellb > 0.f), pa, pb);
     }
-    V3 delta = pa - pb;
-    float dist = sqrtf(dot(delta, delta));
-    n = (dist > 0.f) ? (1.f / dist) * delta : zhat;
-    d = S.ra + S.rb - dist;
-    pt = 0.5f * ((pa - S.ra * n) + (pb + S.rb * n));
+    V3T<S> delta = pa - pb;
+    S dist2 = dot(delta, delta);
+    auto nz = gt(dist2, zero);
+    S idist = sel(nz, vrsqrt(dist2), zero);
+    S dist = dist2 * idist;
+    V3T<S> zhat{zero, zero, bc<S>(1.f)};
+    n = sel3<S>(nz, idist * delta, zhat);  // R16: ẑ when the centres coincide
+    d = (SL.ra + SL.rb) - dist;
+    pt = scale(0.5f, (pa - scale(SL.ra, n)) + (pb + scale(SL.rb, n)));
   }
-  bool active = false;
-  V3 P{0.f, 0.f, 0.f}, ta{0.f, 0.f, 0.f}, tb{0.f, 0.f, 0.f};
-  if (d > 0.f) {
-    V3 rA = pt - xa, rB = pt - xb;
-    V3 u = (A.vel() + cross(A.ang(), rA)) - (B.vel() + cross(B.ang(), rB));
-    float un = dot(u, n);
+  auto pen = gt(d, zero);  // R16: strict d > 0
+  V3T<S> P{zero, zero, zero}, ta{zero, zero, zero}, tb{zero, zero, zero};
+  S active = zero;
+  if (any(pen)) {
+    V3T<S> rA = pt - xa, rB = pt - xb;
+    V3T<S> u = (A.vel() + cross(A.ang(), rA)) - (B.vel() + cross(B.ang(), rB));
+    S un = dot(u, n);
     const bool isa = fl & kSIsoA, isb = fl & kSIsoB;
-    auto eff = [&](V3 dir) {  // k(dir) = Σ_X not static [1/m_X + (r_X×dir)·I_w⁻¹(r_X×dir)]
-      float k = 0.f;
-      if (!S.a_static) {
-        V3 rn = cross(rA, dir);
-        k = k + S.inv_mass_a + dot(rn, iw(qa, S.inv_inertia_a, isa, rn));
+    auto eff = [&](V3T<S> dir) {  // k(dir) = Σ_X not static [1/m_X + (r_X×dir)·I_w⁻¹(r_X×dir)]
+      S k = zero;
+      if (!SL.a_static) {
+        V3T<S> rn = cross(rA, dir);
+        k = k + SL.inv_mass_a + dot(rn, iw(qa, SL.inv_inertia_a, isa, rn));
       }
-      if (!S.b_static) {
-        V3 rn = cross(rB, dir);
-        k = k + S.inv_mass_b + dot(rn, iw(qb, S.inv_inertia_b, isb, rn));
+      if (!SL.b_static) {
+        V3T<S> rn = cross(rB, dir);
+        k = k + SL.inv_mass_b + dot(rn, iw(qb, SL.inv_inertia_b, isb, rn));
       }
       return k;
     };
-    float kn = eff(n);
-    float jn = fmaxf(0.f, __fdividef(-opl_e * un + beta_over_h * d, kn));
-    if (jn > 0.f) {
-      active = true;
-      V3 ut = u - un * n;
-      float st2 = dot(ut, ut);
-      P = jn * n;
-      if (st2 > 0.f) {
-        float ist = rsqrtf(st2);
-        float st = st2 * ist;
-        V3 th = ist * ut;
-        float jt = fminf(__fdividef(st, eff(th)), mu * jn);
-        P = P - jt * th;
-      }
+    S jn = vmax(zero, vdiv(-opl_e * un + beta_over_h * d, eff(n)));
+    auto act = both(pen, gt(jn, zero));  // R15
+    if (any(act)) {
+      jn = sel(act, jn, zero);
+      V3T<S> ut = u - un * n;
+      S st2 = dot(ut, ut);
+      auto sl = gt(st2, zero);  // R16: j_t = 0 when s_t = 0
+      S ist = sel(sl, vrsqrt(st2), zero);
+      S st = st2 * ist;
+      V3T<S> th = ist * ut;
+      S kt = sel(sl, eff(th), bc<S>(1.f));
+      S jt = vmin(vdiv(st, kt), mu * jn);
+      P = jn * n - jt * th;
       ta = cross(rA, P);
       tb = cross(rB, P);
+      active = as_count(act);
     }
   }
-  float4* o = reinterpret_cast<float4*>(out);
-  o[0] = make_float4(P.x, P.y, P.z, active ? 1.f : 0.f);
-  o[1] = make_float4(ta.x, ta.y, ta.z, 0.f);
-  o[2] = make_float4(tb.x, tb.y, tb.z, 0.f);
-  *cnt += active ? 1 : 0;
+  Lanes<S>::st3(out, o2, P, active);
+  Lanes<S>::st3(out + 4, o2, ta);
+  Lanes<S>::st3(out + 8, o2, tb);
+  cnt = cnt + active;
+}
+
+__device__ __forceinline__ void store_count(float* p, int, float c) { *p = c; }
+__device__ __forceinline__ void store_count(float* p, int o2, F2 c) {
+  p[0] = c.x;
+  p[o2] = c.y;
 }
 
 // ---- S6: per-body accumulation over the static incidence lists (fixed order) --
 // e = (item << 4) | t with t = 4 (child / A side: sign +1) or 8 (parent / B side:
 // sign −1); rec: this env's record of the item; the torque vector sits at word t.
-struct Acc {
-  V3 F{0.f, 0.f, 0.f}, T{0.f, 0.f, 0.f}, dV{0.f, 0.f, 0.f}, dW{0.f, 0.f, 0.f};
-  float cnt = 0.f;
-  __device__ __forceinline__ void joint(const float* rec, int e) {
-    float4 f = *reinterpret_cast<const float4*>(rec), t = *reinterpret_cast<const float4*>(rec + (e & 15));
-    float sg = (e & 8) ? -1.f : 1.f;
-    F = V3{fmaf(sg, f.x, F.x), fmaf(sg, f.y, F.y), fmaf(sg, f.z, F.z)};
-    T = T + V3{t.x, t.y, t.z};
+template <class S> struct Acc {
+  V3T<S> F, T, dV, dW;
+  S cnt;
+  __device__ __forceinline__ Acc() {
+    const S z = bc<S>(0.f);
+    F = T = dV = dW = V3T<S>{z, z, z};
+    cnt = z;
   }
-  __device__ __forceinline__ void slot(const float* rec, int e) {
-    float4 p = *reinterpret_cast<const float4*>(rec), t = *reinterpret_cast<const float4*>(rec + (e & 15));
-    float sg = (e & 8) ? -1.f : 1.f;
-    dV = V3{fmaf(sg, p.x, dV.x), fmaf(sg, p.y, dV.y), fmaf(sg, p.z, dV.z)};
-    dW = V3{fmaf(sg, t.x, dW.x), fmaf(sg, t.y, dW.y), fmaf(sg, t.z, dW.z)};
-    cnt += p.w;
+  __device__ __forceinline__ void joint(const float* rec, int o2, int e) {
+    const float sg = (e & 8) ? -1.f : 1.f;
+    F = F + scale(sg, Lanes<S>::ld3(rec, o2));
+    T = T + Lanes<S>::ld3(rec + (e & 15), o2);
+  }
+  __device__ __forceinline__ void slot(const float* rec, int o2, int e) {
+    const float sg = (e & 8) ? -1.f : 1.f;
+    dV = dV + scale(sg, Lanes<S>::ld3(rec, o2));
+    dW = dW + scale(sg, Lanes<S>::ld3(rec + (e & 15), o2));
+    cnt = cnt + Lanes<S>::w4(rec, o2);
   }
 };
 
-// ---- S7 + S8: potential integrator then collision integrator (R14, R21)
-__device__ __forceinline__ void integrate(const DBody& bd, Row r, const Acc& acc, float h, V3 g) {
+// ---- S7 + S8: potential integrator then collision integrator (R14, R21),
+// fused (kin = true) with the next substep's S2 kinematic integrator of the same
+// body: same arithmetic as kinematic(), with v and ω still in registers.
+template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Row<S> r, const Acc<S>& acc, float h,
+                                                             const float* g, bool kin) {
   const bool iso = bd.flags & kFlagIso, fp = bd.flags & kFlagFreePos, fr = bd.flags & kFlagFreeRot;
-  Q4 q = r.rot();
-  V3 v = r.vel() + h * (bd.inv_mass * acc.F + g);
-  V3 w = r.ang() + h * iw(q, bd.inv_inertia, iso, acc.T);
-  if (!fp) v = had(v3(bd.mpos), v);
-  if (!fr) w = had(v3(bd.mrot), w);
-  if (acc.cnt > 0.f) {
-    float ic = __fdividef(1.f, acc.cnt);  // R14: mean over the body's active contacts
+  Q4T<S> q = r.rot();
+  V3T<S> v = r.vel() + scale(h, scale(bd.inv_mass, acc.F) + bc3<S>(g));
+  V3T<S> w = r.ang() + scale(h, iw(q, bd.inv_inertia, iso, acc.T));
+  if (!fp) v = had(bd.mpos, v);
+  if (!fr) w = had(bd.mrot, w);
+  auto hit = gt(acc.cnt, bc<S>(0.f));
+  if (any(hit)) {
+    S ic = sel(hit, vdiv(bc<S>(1.f), acc.cnt), bc<S>(0.f));  // R14: mean over the body's active contacts
     v = v + (bd.inv_mass * ic) * acc.dV;
     w = w + ic * iw(q, bd.inv_inertia, iso, acc.dW);
-    if (!fp) v = had(v3(bd.mpos), v);
-    if (!fr) w = had(v3(bd.mrot), w);
+    if (!fp) v = had(bd.mpos, v);
+    if (!fr) w = had(bd.mrot, w);
   }
   r.set_vel(v);
   r.set_ang(w);
+  if (kin) {  // next substep's kinematic integrator (v, ω already masked)
+    r.set_pos(r.pos() + scale(h, v));
+    if (!bd.rot_frozen) {
+      Q4T<S> dq = qmul(Q4T<S>{bc<S>(0.f), w.x, w.y, w.z}, q);
+      const float hh = 0.5f * h;
+      Q4T<S> qn{q.w + hh * dq.w, q.x + hh * dq.x, q.y + hh * dq.y, q.z + hh * dq.z};
+      S n2 = qn.w * qn.w + qn.x * qn.x + qn.y * qn.y + qn.z * qn.z;
+      S inv = vrsqrt(n2);
+      inv = inv * (1.5f - 0.5f * n2 * inv * inv);
+      r.set_rot(Q4T<S>{qn.w * inv, qn.x * inv, qn.y * inv, qn.z * inv});
+    }
+  }
 }
 
 // ---- S1 / S9: staging of one QP field [n][B][K] <-> sQ record words foff..foff+K-1.
@@ -432,7 +567,7 @@ __device__ __forceinline__ void load_actions(const StepArgs& a, float* sA, int A
 }
 
 // S9: status bits and contact counts (after a barrier)
-__device__ __forceinline__ void block_extras(const StepArgs& a, const float* sQ, const int* sCnt, uint32_t* sStat,
+__device__ __forceinline__ void block_extras(const StepArgs& a, const float* sQ, const float* sCnt, uint32_t* sStat,
                                              int B, int C, int E, int64_t e0, int nvalid) {
   if (a.status) {
     for (int i = threadIdx.x; i < B * E; i += blockDim.x) {

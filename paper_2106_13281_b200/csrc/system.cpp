@@ -271,10 +271,10 @@ System* build_host(const Config& cfg) {
   }();
   for (int pi = 0; pi < kNumPlans; ++pi) {
     DPlan& P = hd.plan[pi];
-    const int G = 1 << pi, E = 32 / G;
+    const int G = 1 << (pi % 3), V = 1 + pi / 3, E = 32 * V / G;
     P.G = G;
+    P.V = V;
     P.E = E;
-    P.log2E = 5 - pi;
     std::vector<std::vector<int>> steps;  // each: G items (-1 idle)
     std::vector<int> step_cost;
     for (const auto& cl : classes)

@@ -24,7 +24,7 @@ p.add_argument("--warps", default="0", help="0 = library default")
 p.add_argument("--steps", type=int, default=200)
 p.add_argument("--rollout", type=int, default=0, help="steps per launch via brax_rollout (0 = brax_step)")
 p.add_argument("--substeps", type=int, default=0, help="override the scene's substeps (staging-cost study)")
-p.add_argument("--groups", default="0", help="lane groups per warp G (1, 2, 4; 0 = library heuristic)")
+p.add_argument("--groups", default="0", help="plans 'G:V' (lane groups, envs per lane) or G; 0 = library heuristic")
 a = p.parse_args()
 with open(os.path.join(ROOT, "profiles", "algorithmic_counts.json")) as f:
     counts = json.load(f)["scenes"]
@@ -39,11 +39,11 @@ for scene in a.scenes.split(","):
         else:
             os.environ.pop("BRAX_WARPS_PER_BLOCK", None)
         s = bx.System(text)
-        for n, G in [(int(x), int(g)) for x in a.envs.split(",") for g in a.groups.split(",")]:
-            if G:
-                os.environ["BRAX_LANE_GROUPS"] = str(G)
+        for n, G in [(int(x), g) for x in a.envs.split(",") for g in a.groups.split(",")]:
+            if G != "0":
+                os.environ["BRAX_PLAN"] = G.replace(":", ",") if ":" in G else f"{G},1"
             else:
-                os.environ.pop("BRAX_LANE_GROUPS", None)
+                os.environ.pop("BRAX_PLAN", None)
             qp = s.alloc_qp(n)
             s.reset(qp, 0, 0.1, 0.1)
             T = a.steps
