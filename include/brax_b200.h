@@ -118,6 +118,14 @@ brax_status brax_system_get_info(const brax_system *sys, brax_system_info *out);
  * (pair index, brax_slot_type, body A, body B, collider A, collider B, point). */
 brax_status brax_system_slot_table(const brax_system *sys, int32_t *out);
 
+/* Tracing: when enabled, every subsequent step launch adds, per block, the SM
+ * cycles thread 0 spent in [0] the prologue (tables + QP staging), [1] joints,
+ * actuators and contacts, [2] the body integrators, [3] the epilogue (write-back);
+ * brax_system_phase_cycles reads the sums (synchronising) and resets them.
+ * Not thread-safe with concurrent launches of the same system. */
+brax_status brax_system_set_tracing(brax_system *sys, int enable);
+brax_status brax_system_phase_cycles(brax_system *sys, uint64_t out[4]);
+
 /* Lint warning i (0 <= i < n_lint_warnings) as text; NULL if out of range. */
 const char *brax_system_lint_warning(const brax_system *sys, int32_t i);
 

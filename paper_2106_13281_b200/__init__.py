@@ -73,6 +73,8 @@ _SIGS = {
     "brax_system_get_info": ([_P, C.POINTER(brax_system_info)], C.c_int),
     "brax_system_slot_table": ([_P, _i32p], C.c_int),
     "brax_system_lint_warning": ([_P, C.c_int32], C.c_char_p),
+    "brax_system_set_tracing": ([_P, C.c_int], C.c_int),
+    "brax_system_phase_cycles": ([_P, C.POINTER(C.c_uint64)], C.c_int),
     "brax_default_qp": ([_P, _P, _P, _P, _P], C.c_int),
     "brax_reset": ([_P, brax_qp, C.c_int64, C.c_uint64, C.c_float, C.c_float, _P], C.c_int),
     "brax_step": ([_P, brax_qp, _P, brax_qp, C.c_int64, _P], C.c_int),
@@ -235,6 +237,15 @@ class System:
 
     def lint(self):
         return [lib.brax_system_lint_warning(self._sys, i).decode() for i in range(self.info.n_lint_warnings)]
+
+    def set_tracing(self, enable: bool = True):
+        _check(lib.brax_system_set_tracing(self._sys, int(enable)))
+
+    def phase_cycles(self):
+        """(prologue, joints+contacts, integrators, epilogue) SM cycles summed over blocks since the last call."""
+        out = (C.c_uint64 * 4)()
+        _check(lib.brax_system_phase_cycles(self._sys, out))
+        return tuple(int(x) for x in out)
 
     def slot_table(self):
         return brax_system_slot_table(self._sys)

@@ -81,7 +81,7 @@ brax_status step_common(const brax_system* sys, brax_qp in, const float* actions
       }
   }
   brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, out.pos, out.rot, out.vel, out.ang, actions,
-                   x ? x->status : nullptr, x ? x->contact_active : nullptr, n_envs, n_steps, 0, 0};
+                   x ? x->status : nullptr, x ? x->contact_active : nullptr, n_envs, n_steps, 0, 0, nullptr};
   if (a.contact_active && s.hd.C == 0) a.contact_active = nullptr;
   int cur = -1;
   cudaGetDevice(&cur);
@@ -195,6 +195,23 @@ brax_status brax_system_slot_table(const brax_system* sys, int32_t* out) {
   if (!sys) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
   brax_config tmp{sys->impl->cfg};
   return brax_config_slot_table(&tmp, out);
+}
+
+brax_status brax_system_set_tracing(brax_system* sys, int enable) {
+  if (!sys) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
+  sys->impl->trace = enable != 0;
+  return BRAX_OK;
+}
+
+brax_status brax_system_phase_cycles(brax_system* sys, uint64_t out[4]) {
+  if (!sys || !out) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
+  cudaSetDevice(sys->impl->device);
+  unsigned long long h[4];
+  cudaError_t e = cudaMemcpy(h, sys->impl->d_phase_cycles, sizeof h, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(sys->impl->d_phase_cycles, 0, sizeof h);
+  if (e != cudaSuccess) return cuda_status(e, "brax_system_phase_cycles");
+  for (int k = 0; k < 4; ++k) out[k] = h[k];
+  return BRAX_OK;
 }
 
 const char* brax_system_lint_warning(const brax_system* sys, int32_t i) {

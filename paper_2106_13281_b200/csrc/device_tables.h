@@ -121,6 +121,7 @@ struct StepArgs {
   int64_t n_steps;
   int32_t bulk_ok;             // all QP pointers 16-byte aligned: TMA bulk staging for full blocks
   int32_t act_bulk_ok;         // actions 16-byte aligned and n·A % 4 == 0: TMA bulk action staging
+  unsigned long long* phase_cycles;  // [4] per-phase SM cycles summed over blocks (tracing), or NULL
 };
 
 // A work plan for one lane-group count G (E = 32/G envs per block): each warp's

@@ -67,6 +67,17 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   uint32_t* sStat = smem + L.stat;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // tracing (brax_system_phase_cycles): thread 0 times prologue / joints+contacts /
+  // integrate / epilogue with clock64 (uniform branch; off unless requested)
+  const bool trace = a.phase_cycles != nullptr && tid == 0;
+  long long tr_mark = trace ? clock64() : 0, tr[4] = {0, 0, 0, 0};
+  auto lap = [&](int k) {
+    if (trace) {
+      long long t = clock64();
+      tr[k] += t - tr_mark;
+      tr_mark = t;
+    }
+  };
   const int LG = 32 / G;                                 // lanes per group
   const int grp = lane / LG, el = lane - grp * LG;       // lane group; first env slot of this lane
   const int o2q = LG * kQS, o2j = LG * kJS, o2c = LG * kCS;  // second env (S = F2): + LG slots
@@ -106,6 +117,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   if (bulk) stg_to_records(stg, sQ, B, E, E);
   for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
   __syncthreads();
+  lap(0);
 
   const DBody* bodies = reinterpret_cast<const DBody*>(sBlob + H.off_bodies);
   const DJoint* joints = reinterpret_cast<const DJoint*>(sBlob + H.off_joints);
@@ -147,6 +159,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     }
     for (int s = 0; s < H.S; ++s) {
       __syncthreads();
+      lap(2);
       if (act_bulk && s == 0 && tid == 0 && step + 1 < a.n_steps) {  // prefetch next step's actions
         mbar_expect_tx(&bars[1], act_bytes);
         tma_load(sAstg, a.actions + ((step + 1) * a.n_envs + e0) * A, act_bytes, &bars[1]);
@@ -169,14 +182,17 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         }
       }
       __syncthreads();
+      lap(1);
       for (int i = bw0; i < bw1; ++i) {
         int b = bodies_of_warp[i * G];
         if (b < 0) continue;
         Acc<S> acc;
+#pragma unroll 4
         for (int k = jinc_begin[b]; k < jinc_begin[b + 1]; ++k) {
           int e = jinc[k];
           acc.joint(sJe + (e >> 4) * (E * kJS), o2j, e);
         }
+#pragma unroll 4
         for (int k = cinc_begin[b]; k < cinc_begin[b + 1]; ++k) {
           int e = cinc[k];
           acc.slot(sCe + (e >> 4) * (E * kCS), o2c, e);
@@ -186,6 +202,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       }
     }
   }
+  lap(2);
   __syncthreads();
   // S9: status bits, contact counts, and the single write-back of the QP (TMA bulk for full blocks)
   block_extras(a, sQ, sCnt, sStat, B, C, E, e0, nvalid);
@@ -211,6 +228,10 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     __syncthreads();
     for (int i = tid; i < nvalid; i += blockDim.x) a.status[e0 + i] = sStat[i];
   }
+  if (trace) {
+    lap(3);
+    for (int k = 0; k < 4; ++k) atomicAdd(&a.phase_cycles[k], (unsigned long long)tr[k]);
+  }
 }
 
 }  // namespace
@@ -227,8 +248,12 @@ int choose_plan(const System& sys, int64_t n_envs) {
   }
   int sms = sys.num_sms > 0 ? sys.num_sms : 148;
   int64_t blocks32 = (n_envs + 31) / 32;
-  // measured (profiles/): G = 2 helps only while 32-env blocks leave SMs idle
-  return blocks32 < sms ? 1 : 0;
+  // measured (profiles/): lane groups help only while the smaller blocks still
+  // fit one per SM (the batch is too small to fill the GPU with 32-env blocks)
+  if (4 * blocks32 <= sms) return 2;
+  if (2 * blocks32 <= sms) return 1;
+  if (blocks32 >= 4 * sms) return 3;  // large batches: two envs per lane (G = 1, V = 2)
+  return 0;
 }
 
 // Register budget per thread: as many as possible while the SM still holds the
@@ -274,6 +299,7 @@ cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t strea
                  al16(a.rot_out) && al16(a.vel_out) && al16(a.ang_out);
   ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * sys.hd.A) % 4 == 0);
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
+  ka.a.phase_cycles = sys.trace ? sys.d_phase_cycles : nullptr;
   const DPlan& P = sys.hd.plan[ka.plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(P.smem_bytes);
@@ -287,7 +313,8 @@ cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t strea
   if (regs >= 112) return launch_variant<float, 112>(ka, grid, block, smem, stream);
   if (regs >= 96) return launch_variant<float, 96>(ka, grid, block, smem, stream);
   if (regs >= 80) return launch_variant<float, 80>(ka, grid, block, smem, stream);
-  return launch_variant<float, 64>(ka, grid, block, smem, stream);
+  if (regs >= 64) return launch_variant<float, 64>(ka, grid, block, smem, stream);
+  return launch_variant<float, 56>(ka, grid, block, smem, stream);
 }
 
 }  // namespace brax

@@ -127,7 +127,10 @@ template <class S> __device__ __forceinline__ S atan2_f(S y, S x) {
   return vcopysign(r, y);
 }
 // asin(x) = atan2(x, √((1−x)(1+x))), x already clamped to [−1, 1]
-template <class S> __device__ __forceinline__ S asin_f(S x) { return atan2_f(x, vsqrt((1.f - x) * (1.f + x))); }
+template <class S> __device__ __forceinline__ S asin_f(S x) {
+  S c2 = (1.f - x) * (1.f + x);  // ≥ 0; √ via rsqrt (no IEEE slow-path call), exact 0 at |x| = 1
+  return atan2_f(x, sel(gt(c2, bc<S>(0.f)), c2 * vrsqrt(c2), bc<S>(0.f)));
+}
 
 // ---- shared-memory access for V = 1 or 2 envs per lane ---------------------------
 // A lane of a group of L lanes handles env slot `el` and (S = F2) `el + L`; the
@@ -212,18 +215,24 @@ template <class S> __device__ __forceinline__ void kinematic(const DBody& bd, Ro
 // act: this env's column of the block's actions sA[k][env] (row stride E, second env + L).
 // out: this (joint, env) record: F on child | T child | T parent.
 template <class S>
-__device__ __forceinline__ void joint(const DJoint& J, Row<S> P, Row<S> C, const float* act, int E, int L,
+__device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, const float* act, int E, int L,
                                       float* out, int o2) {
+  // the parameter record, read with LDS.128 (struct fields at fixed float4 slots)
+  const float4* J4 = reinterpret_cast<const float4*>(&Jm);
+  const int4 h0 = *reinterpret_cast<const int4*>(&Jm), h1 = reinterpret_cast<const int4*>(&Jm)[1];
+  const int dof = h0.z, act_kind = h0.w, act_offset = h1.x, flags = h1.y;
+  const float4 op_k = J4[2], oc_cl = J4[3], jp = J4[4], jc = J4[5], lo_kl = J4[6], hi_ka = J4[7], ca_s = J4[8];
+  const float lo[3] = {lo_kl.x, lo_kl.y, lo_kl.z}, hi[3] = {hi_ka.x, hi_ka.y, hi_ka.z};
   Q4T<S> qp = P.rot(), qc = C.rot();
-  V3T<S> rp = rotate(qp, bc3<S>(J.o_p));
-  V3T<S> rc = rotate(qc, bc3<S>(J.o_c));
+  V3T<S> rp = rotate(qp, V3T<S>{bc<S>(op_k.x), bc<S>(op_k.y), bc<S>(op_k.z)});
+  V3T<S> rc = rotate(qc, V3T<S>{bc<S>(oc_cl.x), bc<S>(oc_cl.y), bc<S>(oc_cl.z)});
   V3T<S> dx = (P.pos() - C.pos()) + (rp - rc);
   V3T<S> wp = P.ang(), wc = C.ang();
-  V3T<S> f = scale(J.k, dx);
-  if (!(J.flags & kJNoCl))
-    f = f + scale(J.c_l, (P.vel() + cross(wp, rp)) - (C.vel() + cross(wc, rc)));
-  Q4T<S> fp = qmul(qp, bcq<S>(J.jp));
-  Q4T<S> fc = qmul(qc, bcq<S>(J.jc));
+  V3T<S> f = scale(op_k.w, dx);
+  if (!(flags & kJNoCl))
+    f = f + scale(oc_cl.w, (P.vel() + cross(wp, rp)) - (C.vel() + cross(wc, rc)));
+  Q4T<S> fp = qmul(qp, Q4T<S>{bc<S>(jp.x), bc<S>(jp.y), bc<S>(jp.z), bc<S>(jp.w)});
+  Q4T<S> fc = qmul(qc, Q4T<S>{bc<S>(jc.x), bc<S>(jc.y), bc<S>(jc.z), bc<S>(jc.w)});
   Q4T<S> qr = qmul(qconj(fp), fc);
   S sg = sel(lt(qr.w, bc<S>(0.f)), bc<S>(-1.f), bc<S>(1.f));  // canonicalise q_r to w >= 0 (R25)
   qr = Q4T<S>{sg * qr.w, sg * qr.x, sg * qr.y, sg * qr.z};
@@ -236,21 +245,21 @@ __device__ __forceinline__ void joint(const DJoint& J, Row<S> P, Row<S> C, const
   S tau[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    if (i < J.dof) tau[i] = J.k_l * (clampv(th[i], J.lo[i], J.hi[i]) - th[i]);
-    else tau[i] = -(J.k_a * th[i]);
+    if (i < dof) tau[i] = lo_kl.w * (clampv(th[i], lo[i], hi[i]) - th[i]);
+    else tau[i] = -(hi_ka.w * th[i]);
   }
-  if (J.act_kind >= 0) {
+  if (act_kind >= 0) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      if (i < J.dof) {
-        S a = Lanes<S>::ld(act + (J.act_offset + i) * E, L);
-        tau[i] = tau[i] + ((J.act_kind == 0) ? J.strength * clampv(a, -1.f, 1.f)
-                                             : J.strength * (clampv(a, J.lo[i], J.hi[i]) - th[i]));
+      if (i < dof) {
+        S a = Lanes<S>::ld(act + (act_offset + i) * E, L);
+        tau[i] = tau[i] + ((act_kind == 0) ? ca_s.y * clampv(a, -1.f, 1.f)
+                                           : ca_s.y * (clampv(a, lo[i], hi[i]) - th[i]));
       }
     }
   }
   V3T<S> twd = rotate(fp, V3T<S>{tau[0], tau[1], tau[2]});
-  if (!(J.flags & kJNoCa)) twd = twd + scale(J.c_a, wp - wc);
+  if (!(flags & kJNoCa)) twd = twd + scale(ca_s.x, wp - wc);
   V3T<S> tc = twd + cross(rc, f);
   V3T<S> tp = twd + cross(rp, f);
   Lanes<S>::st3(out, o2, f);

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -11,6 +12,12 @@
 #include <sstream>
 
 namespace brax {
+// the kernel reads these records with 16-byte vector loads at fixed slots
+static_assert(sizeof(DBody) == 64 && sizeof(DJoint) == 144 && sizeof(DSlot) == 160, "record sizes");
+static_assert(offsetof(DJoint, o_p) == 32 && offsetof(DJoint, o_c) == 48 && offsetof(DJoint, jp) == 64 &&
+                  offsetof(DJoint, jc) == 80 && offsetof(DJoint, lo) == 96 && offsetof(DJoint, hi) == 112 &&
+                  offsetof(DJoint, c_a) == 128,
+              "DJoint float4 slots");
 namespace {
 
 void qmul(const double a[4], const double b[4], double o[4]) {
@@ -50,6 +57,7 @@ System::~System() {
   if (d_blob) cudaFree(d_blob);
   if (d_default_qp) cudaFree(d_default_qp);
   if (d_masks) cudaFree(d_masks);
+  if (d_phase_cycles) cudaFree(d_phase_cycles);
 }
 
 void default_qp(const Config& cfg, std::vector<double>& pos, std::vector<double>& rot) {
@@ -285,7 +293,10 @@ System* build_host(const Config& cfg) {
         step_cost.push_back(cl[k] < J ? 5 : 3);
       }
     const int n_body_steps = (int(dyn.size()) + G - 1) / G;
-    int W = std::max(1, std::max(n_body_steps, (int(steps.size()) + 1) / 2));
+    // G = 1 (large batches, throughput-bound): ~2 item steps per warp; G > 1 (small
+    // batches, latency-bound): one item step per warp (measured, profiles/)
+    int W = G == 1 ? std::max(1, std::max(n_body_steps, (int(steps.size()) + 1) / 2))
+                   : std::max(1, std::max(n_body_steps, int(steps.size())));
     W = std::min(W, kMaxWarps);
     if (env_w) W = env_w;
     P.W = W;
@@ -399,6 +410,8 @@ System* build_system(const Config& cfg, int device) {
     }
     s->d_masks_host[7 * b + 6] = float(bodies[b].is_static);
   }
+  cuda_check(cudaMalloc(&s->d_phase_cycles, 4 * sizeof(unsigned long long)), "cudaMalloc(phase_cycles)");
+  cuda_check(cudaMemset(s->d_phase_cycles, 0, 4 * sizeof(unsigned long long)), "cudaMemset");
   cuda_check(cudaMalloc(&s->d_masks, s->d_masks_host.size() * 4), "cudaMalloc(masks)");
   cuda_check(cudaMemcpy(s->d_masks, s->d_masks_host.data(), s->d_masks_host.size() * 4, cudaMemcpyHostToDevice),
              "cudaMemcpy(masks)");

@@ -24,6 +24,8 @@ struct System {
   std::vector<std::string> lint;
   int n_dynamic = 0;
   int num_sms = 0;                     // of `device` (launch heuristics)
+  bool trace = false;                  // per-phase cycle tracing (brax_system_set_tracing)
+  unsigned long long* d_phase_cycles = nullptr;  // device [4]
   size_t smem_bytes = 0;
   ~System();
 };
