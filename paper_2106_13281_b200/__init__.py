@@ -222,12 +222,14 @@ class System:
         self.info = brax_system_get_info(self._sys)
 
     def __del__(self):
-        if getattr(self, "_sys", None):
-            brax_system_destroy(self._sys)
-            self._sys = None
-        if getattr(self, "_cfg", None):
-            brax_config_destroy(self._cfg)
-            self._cfg = None
+        try:
+            if getattr(self, "_sys", None):
+                brax_system_destroy(self._sys)
+            if getattr(self, "_cfg", None):
+                brax_config_destroy(self._cfg)
+        except Exception:  # noqa: BLE001 — interpreter shutdown: the library may already be gone
+            pass
+        self._sys = self._cfg = None
 
     handle = property(lambda self: self._sys)
     n_bodies = property(lambda self: self.info.n_bodies)

@@ -89,11 +89,19 @@ template <class S> __device__ __forceinline__ Q4T<S> qmul(Q4T<S> a, Q4T<S> b) {
           a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x, a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w};
 }
 template <class S> __device__ __forceinline__ Q4T<S> qconj(Q4T<S> q) { return {q.w, -q.x, -q.y, -q.z}; }
-// rotate(q, v) = v + w·t + u×t, t = 2u×v
+// c + a×b with the products fused into the accumulation (2 FFMA per component)
+template <class S> __device__ __forceinline__ V3T<S> cross_add(V3T<S> a, V3T<S> b, V3T<S> c) {
+  return {a.y * b.z + (c.x - a.z * b.y), a.z * b.x + (c.y - a.x * b.z), a.x * b.y + (c.z - a.y * b.x)};
+}
+// rotate(q, v) = v + w·t + u×t, t = 2u×v, evaluated as v + (2w)·c + (2u)×c with
+// c = u×v: 7 FMUL + 12 FFMA instead of 9 FMUL + 9 FFMA + 3 FADD.
 template <class S> __device__ __forceinline__ V3T<S> rotate(Q4T<S> q, V3T<S> v) {
   V3T<S> u{q.x, q.y, q.z};
-  V3T<S> t = scale(2.f, cross(u, v));
-  return v + q.w * t + cross(u, t);
+  V3T<S> c = cross(u, v);
+  S w2 = 2.f * q.w;
+  V3T<S> u2{2.f * q.x, 2.f * q.y, 2.f * q.z};
+  V3T<S> r{w2 * c.x + v.x, w2 * c.y + v.y, w2 * c.z + v.z};
+  return cross_add(u2, c, r);
 }
 // rotate(q, ẑ): the third column of R(q)
 template <class S> __device__ __forceinline__ V3T<S> rotate_z(Q4T<S> q) {
@@ -230,7 +238,7 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
   V3T<S> wp = P.ang(), wc = C.ang();
   V3T<S> f = scale(op_k.w, dx);
   if (!(flags & kJNoCl))
-    f = f + scale(oc_cl.w, (P.vel() + cross(wp, rp)) - (C.vel() + cross(wc, rc)));
+    f = f + scale(oc_cl.w, cross_add(wp, rp, P.vel()) - cross_add(wc, rc, C.vel()));
   Q4T<S> fp = qmul(qp, Q4T<S>{bc<S>(jp.x), bc<S>(jp.y), bc<S>(jp.z), bc<S>(jp.w)});
   Q4T<S> fc = qmul(qc, Q4T<S>{bc<S>(jc.x), bc<S>(jc.y), bc<S>(jc.z), bc<S>(jc.w)});
   Q4T<S> qr = qmul(qconj(fp), fc);
@@ -260,8 +268,8 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
   }
   V3T<S> twd = rotate(fp, V3T<S>{tau[0], tau[1], tau[2]});
   if (!(flags & kJNoCa)) twd = twd + scale(ca_s.x, wp - wc);
-  V3T<S> tc = twd + cross(rc, f);
-  V3T<S> tp = twd + cross(rp, f);
+  V3T<S> tc = cross_add(rc, f, twd);
+  V3T<S> tp = cross_add(rp, f, twd);
   Lanes<S>::st3(out, o2, f);
   Lanes<S>::st3(out + 4, o2, tc);
   Lanes<S>::st3(out + 8, o2, V3T<S>{-tp.x, -tp.y, -tp.z});
@@ -302,41 +310,54 @@ __device__ __forceinline__ void seg_seg(V3T<S> p1, V3T<S> q1, V3T<S> p2, V3T<S> 
 // ---- S5: contact slot, velocity-level impulse + Baumgarte (R13-R19)
 // out: this (slot, env) record: P, active | r_A×P | r_B×P; cnt: substeps active.
 template <class S>
-__device__ __forceinline__ void contact(const DSlot& SL, Row<S> A, Row<S> B, float opl_e, float beta_over_h,
+__device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, float opl_e, float beta_over_h,
                                         float mu, float* out, int o2, S& cnt) {
-  const int fl = SL.flags;
+  // the parameter record, read with LDS.128 at its fixed float4 slots
+  const float4* S4 = reinterpret_cast<const float4*>(&SLm);
+  const int4 h0 = *reinterpret_cast<const int4*>(&SLm), h1 = reinterpret_cast<const int4*>(&SLm)[1];
+  const int type = h0.x, a_static = h1.x, b_static = h1.y, fl = h1.z;
+  const float4 ca = S4[2], cb = S4[4], ells = S4[6];  // ca_pos|ra, cb_pos|rb, ell_a ellb 1/m_a 1/m_b
+  const float ra = ca.w, rb = cb.w;
   Q4T<S> qa = A.rot(), qb = B.rot();
   V3T<S> xa = A.pos(), xb = B.pos();
-  V3T<S> cA = (fl & kSZeroPa) ? xa : xa + rotate(qa, bc3<S>(SL.ca_pos));
-  V3T<S> cB = (fl & kSZeroPb) ? xb : xb + rotate(qb, bc3<S>(SL.cb_pos));
-  Q4T<S> qA = (fl & kSIdentA) ? qa : qmul(qa, bcq<S>(SL.ca_rot));
-  Q4T<S> qB = (fl & kSIdentB) ? qb : qmul(qb, bcq<S>(SL.cb_rot));
+  V3T<S> cA = (fl & kSZeroPa) ? xa : xa + rotate(qa, V3T<S>{bc<S>(ca.x), bc<S>(ca.y), bc<S>(ca.z)});
+  V3T<S> cB = (fl & kSZeroPb) ? xb : xb + rotate(qb, V3T<S>{bc<S>(cb.x), bc<S>(cb.y), bc<S>(cb.z)});
+  Q4T<S> qA = qa, qB = qb;
+  if (!(fl & kSIdentA)) {
+    const float4 r = S4[3];
+    qA = qmul(qa, Q4T<S>{bc<S>(r.x), bc<S>(r.y), bc<S>(r.z), bc<S>(r.w)});
+  }
+  if (!(fl & kSIdentB)) {
+    const float4 r = S4[5];
+    qB = qmul(qb, Q4T<S>{bc<S>(r.x), bc<S>(r.y), bc<S>(r.z), bc<S>(r.w)});
+  }
   const S zero = bc<S>(0.f);
   V3T<S> n, pt;
   S d;
-  if (SL.type <= 2) {  // sphere / capsule end / box corner vs plane: plane is B
+  if (type <= 2) {  // sphere / capsule end / box corner vs plane: plane is B
     n = rotate_z(qB);
-    if (SL.type == 2) {
-      V3T<S> c = cA + rotate(qA, bc3<S>(SL.corner));
+    if (type == 2) {
+      const float4 k = S4[7];
+      V3T<S> c = cA + rotate(qA, V3T<S>{bc<S>(k.x), bc<S>(k.y), bc<S>(k.z)});
       d = -dot(c - cB, n);
       pt = c;
     } else {
-      V3T<S> c = (SL.type == 1) ? cA + scale(SL.ell_a, rotate_z(qA)) : cA;
-      d = SL.ra - dot(c - cB, n);
-      pt = c - scale(SL.ra, n);
+      V3T<S> c = (type == 1) ? cA + scale(ells.x, rotate_z(qA)) : cA;
+      d = ra - dot(c - cB, n);
+      pt = c - scale(ra, n);
     }
   } else {
     V3T<S> pa = cA, pb = cB;
-    if (SL.type == 4) {  // sphere (A) – capsule (B)
+    if (type == 4) {  // sphere (A) – capsule (B)
       V3T<S> axb = rotate_z(qB);
-      V3T<S> e0 = cB + scale(SL.ellb, axb), e1 = cB - scale(SL.ellb, axb);
+      V3T<S> e0 = cB + scale(ells.y, axb), e1 = cB - scale(ells.y, axb);
       V3T<S> seg = e0 - e1;
-      if (SL.ellb > 0.f) pb = e1 + clampv(vdiv(dot(cA - e1, seg), dot(seg, seg)), 0.f, 1.f) * seg;
+      if (ells.y > 0.f) pb = e1 + clampv(vdiv(dot(cA - e1, seg), dot(seg, seg)), 0.f, 1.f) * seg;
       else pb = e1;
-    } else if (SL.type == 5) {  // capsule – capsule
+    } else if (type == 5) {  // capsule – capsule
       V3T<S> axa = rotate_z(qA), axb = rotate_z(qB);
-      seg_seg(cA + scale(SL.ell_a, axa), cA - scale(SL.ell_a, axa), cB + scale(SL.ellb, axb),
-              cB - scale(SL.ellb, axb), !(SL.ell_a > 0.f), !(SL.ellb > 0.f), pa, pb);
+      seg_seg(cA + scale(ells.x, axa), cA - scale(ells.x, axa), cB + scale(ells.y, axb), cB - scale(ells.y, axb),
+              !(ells.x > 0.f), !(ells.y > 0.f), pa, pb);
     }
     V3T<S> delta = pa - pb;
     S dist2 = dot(delta, delta);
@@ -345,26 +366,28 @@ __device__ __forceinline__ void contact(const DSlot& SL, Row<S> A, Row<S> B, flo
     S dist = dist2 * idist;
     V3T<S> zhat{zero, zero, bc<S>(1.f)};
     n = sel3<S>(nz, idist * delta, zhat);  // R16: ẑ when the centres coincide
-    d = (SL.ra + SL.rb) - dist;
-    pt = scale(0.5f, (pa - scale(SL.ra, n)) + (pb + scale(SL.rb, n)));
+    d = (ra + rb) - dist;
+    pt = scale(0.5f, (pa - scale(ra, n)) + (pb + scale(rb, n)));
   }
   auto pen = gt(d, zero);  // R16: strict d > 0
   V3T<S> P{zero, zero, zero}, ta{zero, zero, zero}, tb{zero, zero, zero};
   S active = zero;
   if (any(pen)) {
     V3T<S> rA = pt - xa, rB = pt - xb;
-    V3T<S> u = (A.vel() + cross(A.ang(), rA)) - (B.vel() + cross(B.ang(), rB));
+    V3T<S> u = cross_add(A.ang(), rA, A.vel()) - cross_add(B.ang(), rB, B.vel());
     S un = dot(u, n);
     const bool isa = fl & kSIsoA, isb = fl & kSIsoB;
+    const float4 iia4 = S4[8], iib4 = S4[9];
+    const float iia[3] = {iia4.x, iia4.y, iia4.z}, iib[3] = {iib4.x, iib4.y, iib4.z};
     auto eff = [&](V3T<S> dir) {  // k(dir) = Σ_X not static [1/m_X + (r_X×dir)·I_w⁻¹(r_X×dir)]
       S k = zero;
-      if (!SL.a_static) {
+      if (!a_static) {
         V3T<S> rn = cross(rA, dir);
-        k = k + SL.inv_mass_a + dot(rn, iw(qa, SL.inv_inertia_a, isa, rn));
+        k = k + ells.z + dot(rn, iw(qa, iia, isa, rn));
       }
-      if (!SL.b_static) {
+      if (!b_static) {
         V3T<S> rn = cross(rB, dir);
-        k = k + SL.inv_mass_b + dot(rn, iw(qb, SL.inv_inertia_b, isb, rn));
+        k = k + ells.w + dot(rn, iw(qb, iib, isb, rn));
       }
       return k;
     };
