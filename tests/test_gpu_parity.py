@@ -17,7 +17,7 @@ import paper_2106_13281_b200 as bx  # noqa: E402
 TOL_STEP = 1e-4
 TOL_100 = 1e-3
 FIELDS = ("pos", "rot", "vel", "ang")
-SCENES = ["ball", "pendulum", "chain2", "ant", "humanoid", "halfcheetah", "grasp", "fetch"]
+SCENES = ["ball", "pendulum", "chain2", "ant", "humanoid", "halfcheetah", "grasp", "fetch", "coverage"]
 _cache = {}
 
 
@@ -90,7 +90,7 @@ def test_single_step_parity(name, T0):
 
 
 @pytest.mark.parametrize("name,n", [("ant", 8192), ("humanoid", 4096), ("halfcheetah", 4096),
-                                    ("grasp", 2048), ("fetch", 2048)])
+                                    ("grasp", 2048), ("fetch", 2048), ("coverage", 3000)])
 def test_full_size_sampled_parity(name, n):
     """At BASELINE.json sizes in the bench launch shape: the GPU steps the whole
     batch, the oracle a sample of 192 envs (envs are independent)."""
@@ -256,3 +256,29 @@ def test_slot_table_and_default_qp_on_device_system():
         ref = o.default_qp()
         for k in FIELDS:
             assert np.max(np.abs(d[k] - ref[k])) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["ant", "humanoid", "grasp", "coverage"])
+def test_every_launch_plan_matches_oracle(name):
+    """The launch heuristics pick the lane-group count G, envs per lane V and the
+    register budget per call; every combination must give the oracle's answer."""
+    import os
+    o, s = scene(name)
+    n = 333
+    qp = trajectory_states(o, n, seed=41, T0=3)
+    act = synth.actions(42, 1, n, o.act_dim)[0]
+    ref, ex = o.step(qp, act, threads=8)
+    keep = ~ex["ambiguous"]
+    try:
+        for plan in ("1,1", "2,1", "4,1", "1,2", "2,2", "4,2"):
+            for regs in ("56", "96", "128"):
+                os.environ["BRAX_PLAN"] = plan
+                os.environ["BRAX_MAXREG"] = regs
+                got, status, ca = gpu_step(s, qp, act)
+                err, errs = max_err(got, ref, keep)
+                assert err <= TOL_STEP, (plan, regs, errs)
+                assert np.array_equal(ca[keep], ex["contact_active"][keep]), (plan, regs)
+                assert np.array_equal(status, ex["status"]), (plan, regs)
+    finally:
+        os.environ.pop("BRAX_PLAN", None)
+        os.environ.pop("BRAX_MAXREG", None)

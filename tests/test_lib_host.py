@@ -12,7 +12,7 @@ import oracle
 import paper_2106_13281_b200 as bx
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SCENES = ["ball", "appA", "pendulum", "chain2", "ant", "humanoid", "halfcheetah", "grasp", "fetch"]
+SCENES = ["ball", "appA", "pendulum", "chain2", "ant", "humanoid", "halfcheetah", "grasp", "fetch", "coverage"]
 
 
 def declared_functions():

@@ -166,6 +166,31 @@ joints { name: "J" parent: "P" child: "C" stiffness: 1000 limit_stiffness: 300
         assert abs(q["ang"][0, 1, 0] - w) < 1e-12
 
 
+def test_angle_actuator_servo_recurrence():
+    """ANGLE actuator (R12): τ = s·(clamp(a, lo, hi) − θ) about the free axis; with wide
+    limits and no other torque: θ_{n+1} = θ_n + 2·atan(ω_n h/2), ω_{n+1} = ω_n +
+    (s·(a − θ_{n+1}) + k_l·(clamp(θ_{n+1}, lo, hi) − θ_{n+1}))·h/I; the target a is
+    clamped to the limits."""
+    txt = """dt: 0.01
+bodies { name: "P" frozen { all: true } }
+bodies { name: "C" mass: 1 inertia { x: 0.5 y: 0.5 z: 0.5 } }
+joints { name: "J" parent: "P" child: "C" stiffness: 1000 angle_limit { min: -90 max: 60 } }
+actuators { name: "J" joint: "J" strength: 20 angle {} }"""
+    o = oracle.Oracle(txt)
+    for target in (0.4, 2.0):  # 2.0 rad is beyond the 60° limit: clamped to π/3
+        q = o.batch_default_qp(1)
+        th, w = 0.0, 0.0
+        tgt = min(target, math.radians(60))
+        for _ in range(200):
+            q, _ = o.step(q, np.array([[target]]))
+            th = th + 2 * math.atan(w * 0.01 / 2)
+            lim = min(max(th, math.radians(-90)), math.radians(60)) - th  # soft limit (R7, R8)
+            w = w + ((20 * (tgt - th) + 1000 * lim) / 0.5) * 0.01
+            r = q["rot"][0, 1]
+            assert abs(2 * math.atan2(r[1], r[0]) - th) < 1e-11
+            assert abs(q["ang"][0, 1, 0] - w) < 1e-11
+
+
 def test_app_a_pendulum_period():
     """Small-angle period of the App. A pendulum:
     T = 2π√((I + mL²)/(mgL)) = 2.8384 s; within 1e-3 relative at h = 0.01."""
@@ -422,6 +447,35 @@ collide_include { first: "C" second: "S" }"""
     pb = _seg_points(pos[1], _quat_to_axis(rot[1]), 0.4, k)
     dmin = np.linalg.norm(pb - pos[0][None, :], axis=1).min()
     assert abs(d - (0.3 - dmin)) < 1e-9
+
+
+def test_sphere_sphere_geometry():
+    """Sphere–sphere: d = r_A + r_B − |c_A − c_B|, n from B to A, contact point at the
+    midpoint of the two surface points (R18); coincident centres → n = ẑ (R16)."""
+    txt = """dt: 0.01
+bodies { name: "A" colliders { position { x: 0.1 } sphere { radius: 0.3 } } }
+bodies { name: "B" colliders { sphere { radius: 0.2 } } }"""
+    o = oracle.Oracle(txt)
+    assert o.sys.slot_table().tolist() == [[0, 3, 0, 1, 0, 1, 0]]
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        pos = rng.uniform(-0.3, 0.3, (2, 3))
+        rot = rng.normal(size=(2, 4))
+        rot /= np.linalg.norm(rot, axis=1, keepdims=True)
+        ca = pos[0] + _rotate(rot[0], [0.1, 0, 0])
+        cb = pos[1]
+        dist = np.linalg.norm(ca - cb)
+        d, n, pt, _ = o.slot_geometry(0, pos, rot)
+        assert abs(d - (0.5 - dist)) < 1e-12
+        assert np.allclose(n, (ca - cb) / dist, atol=1e-12)
+        assert np.allclose(pt, 0.5 * ((ca - 0.3 * n) + (cb + 0.2 * n)), atol=1e-12)
+    d, n, pt, _ = o.slot_geometry(0, np.array([[-0.1, 0, 0], [0, 0, 0.0]]), np.array([[1.0, 0, 0, 0]] * 2))
+    assert abs(d - 0.5) < 1e-12 and np.allclose(n, [0, 0, 1])
+
+
+def _rotate(q, v):
+    from scipy.spatial.transform import Rotation
+    return Rotation.from_quat([q[1], q[2], q[3], q[0]]).apply(v)
 
 
 def test_sphere_plane_examples():

@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 import synth  # noqa: E402
 
-SCENES = ["ball", "pendulum", "chain2", "ant", "humanoid", "halfcheetah", "grasp", "fetch"]
+SCENES = ["ball", "pendulum", "chain2", "ant", "humanoid", "halfcheetah", "grasp", "fetch", "coverage"]
 
 
 def count(name, n=64, burn=30, measure=20, seed=0):
