@@ -1,0 +1,131 @@
+"""NEXT-3: the "astronaut" conservation diagnostic of Fig. 5 (PAPER.md:251-258,
+:264), run on the GPU step kernel.
+
+Protocol (paper, after Erez et al.): the humanoid with damping, collisions and
+gravity disabled; (momentum) limbs randomly actuated for 1 s with ≈ 0.5 N·m
+per actuator per step; (energy) actuators disabled, every body part given a
+random 1 m/s kick, energy drift measured after 1 s; averaged over 128 seeds,
+single precision.  Fidelity axis: the substep length h (dt fixed, substeps
+1, 2, 4, 8).
+
+Quantities (host-side analysis of the GPU's QP, fp64):
+  P = Σ m v;  L = Σ (x × m v + I_w ω) about the origin (isotropic inertia, R4);
+  E = Σ ½ m|v|² + ½ ω·I_w ω + Σ_joints ½ k |Δx|² (anchor springs; the angular
+      alignment/limit springs are reported separately as they are not
+      potential-derived for d ≥ 2, R7).
+    python tools/astronaut.py [--seeds 128] [--json out.json]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import re
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def astronaut_text(substeps: int, strength: float) -> str:
+    """humanoid.bxc with gravity, damping and colliders removed, torque actuators of `strength`."""
+    with open(os.path.join(ROOT, "scenes", "humanoid.bxc")) as f:
+        t = f.read()
+    t = re.sub(r"gravity \{[^}]*\}", "gravity { }", t)
+    t = re.sub(r"angular_damping: [0-9.]+", "angular_damping: 0", t)
+    t = re.sub(r"\n  colliders \{[^\n]*\} \}", " }", t)       # each body's one-line collider block
+    t = re.sub(r"collide_include \{[^}]*\}\n", "", t)
+    t = re.sub(r'bodies \{ name: "Ground" frozen \{ all: true \} colliders \{ plane \{\} \} \}\n', "", t)
+    t = re.sub(r"strength: [0-9.]+", f"strength: {strength}", t)
+    t = re.sub(r"^substeps: *\d+", f"substeps: {substeps}", t, flags=re.M)
+    assert "colliders" not in t and "collide_include" not in t
+    return t
+
+
+def quat_rotate(q, v):
+    w, u = q[..., :1], q[..., 1:]
+    t = 2.0 * np.cross(u, v)
+    return v + w * t + np.cross(u, t)
+
+
+def invariants(o_sys, qp):
+    """P, L (about the origin), kinetic energy and anchor-spring energy per env (fp64)."""
+    m = np.array([b.mass for b in o_sys.bodies])[None, :, None]
+    I = np.array([b.inertia for b in o_sys.bodies])[None]
+    x, q, v, w = (qp[k].astype(np.float64) for k in ("pos", "rot", "vel", "ang"))
+    P = (m * v).sum(1)
+    # I_w ω = R (I ⊙ Rᵀ ω)
+    wb = quat_rotate(q * np.array([1, -1, -1, -1]), w)
+    Iw = quat_rotate(q, I * wb)
+    L = (np.cross(x, m * v) + Iw).sum(1)
+    ke = 0.5 * (m[..., 0] * (v * v).sum(-1)).sum(1) + 0.5 * (w * Iw).sum(-1).sum(1)
+    pe = np.zeros(x.shape[0])
+    for j in o_sys.joints:
+        ap = x[:, j.parent] + quat_rotate(q[:, j.parent], j.parent_offset)
+        ac = x[:, j.child] + quat_rotate(q[:, j.child], j.child_offset)
+        pe += 0.5 * j.stiffness * ((ap - ac) ** 2).sum(-1)
+    return P, L, ke + pe
+
+
+def run(seeds=128, substeps_list=(1, 2, 4, 8), horizon_s=1.0):
+    import torch
+
+    import oracle
+    import paper_2106_13281_b200 as bx
+    import synth
+    out = []
+    for S in substeps_list:
+        text_mom = astronaut_text(S, 0.5)
+        text_en = astronaut_text(S, 0.0)
+        sys_m = bx.System(text_mom)
+        sys_e = bx.System(text_en)
+        o = oracle.parse_system(text_mom)  # host-side constants for the analysis only
+        dt = o.dt
+        steps = int(round(horizon_s / dt))
+        # momentum: random ±0.5 N·m torques every step
+        qp = sys_m.alloc_qp(seeds)
+        sys_m.reset(qp, seed=S, vel_noise=0.1, ang_noise=0.1)
+        acts = torch.from_numpy(synth.actions(100 + S, steps, seeds, sys_m.act_dim)).cuda()
+        q0 = {k: v.cpu().numpy() for k, v in qp.items()}
+        for t in range(steps):
+            sys_m.step(qp, acts[t], qp)
+        torch.cuda.synchronize()
+        q1 = {k: v.cpu().numpy() for k, v in qp.items()}
+        P0, L0, _ = invariants(o, q0)
+        P1, L1, _ = invariants(o, q1)
+        # energy: no actuation, 1 m/s random kick of every body (random unit directions)
+        qe = sys_e.alloc_qp(seeds)
+        sys_e.reset(qe, seed=S, vel_noise=0.0, ang_noise=0.0)
+        rng = np.random.Generator(np.random.PCG64(200 + S))
+        kick = rng.normal(size=qe["vel"].shape)
+        kick /= np.linalg.norm(kick, axis=-1, keepdims=True)
+        qe["vel"].copy_(torch.from_numpy(kick.astype(np.float32)))
+        e0 = {k: v.cpu().numpy() for k, v in qe.items()}
+        zero = torch.zeros((steps, seeds, sys_e.act_dim), device="cuda")
+        for t in range(steps):
+            sys_e.step(qe, zero[t], qe)
+        torch.cuda.synchronize()
+        e1 = {k: v.cpu().numpy() for k, v in qe.items()}
+        _, _, E0 = invariants(o, e0)
+        _, _, E1 = invariants(o, e1)
+        out.append({"substeps": S, "h": dt / S, "steps": steps, "seeds": seeds,
+                    "linear_momentum_drift": float(np.mean(np.linalg.norm(P1 - P0, axis=-1))),
+                    "angular_momentum_drift": float(np.mean(np.linalg.norm(L1 - L0, axis=-1))),
+                    "energy_drift": float(np.mean(np.abs(E1 - E0))),
+                    "energy_rel_drift": float(np.mean(np.abs(E1 - E0) / np.abs(E0)))})
+    return out
+
+
+if __name__ == "__main__":
+    p = argparse.ArgumentParser()
+    p.add_argument("--seeds", type=int, default=128)
+    p.add_argument("--json", default=None)
+    a = p.parse_args()
+    res = run(a.seeds)
+    for r in res:
+        print(json.dumps(r))
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump(res, f, indent=1)
