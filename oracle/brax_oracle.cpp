@@ -16,8 +16,8 @@
 // joint / slot at a time, in the paper's order; no blocking, fusion or
 // reordering.  The scalar type is a template parameter so that the same code
 // also runs with an op-counting type (SURVEY §8(d) counting convention:
-// add/sub/mul = 1 flop, div/sqrt = 4 flops + 1 MUFU, atan2/asin = 20 flops +
-// 1 MUFU; comparisons, min/max and clamps are not counted).
+// add/sub/mul = 1 flop, div/sqrt = 4 flops + 1 MUFU, atan2/asin/sin/cos = 20
+// flops + 1 MUFU; comparisons, min/max and clamps are not counted).
 //
 // Parity pins: tests/test_oracle_pins.py (closed forms, invariants, brute force).
 // Parity unpinned beyond invariants: whole-scene trajectories (ant, humanoid,
@@ -60,6 +60,10 @@ inline Cnt xsqrt(Cnt x) { g_flops += 4; g_mufu += 1; return Cnt(std::sqrt(x.v));
 inline double xatan2(double y, double x) { return std::atan2(y, x); }
 inline Cnt xatan2(Cnt y, Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::atan2(y.v, x.v)); }
 inline double xasin(double x) { return std::asin(x); }
+inline double xsin(double x) { return std::sin(x); }
+inline double xcos(double x) { return std::cos(x); }
+inline Cnt xsin(Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::sin(x.v)); }
+inline Cnt xcos(Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::cos(x.v)); }
 inline Cnt xasin(Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::asin(x.v)); }
 // fp32 instantiation (diagnostic only: measures the fp32 rounding floor of the
 // same algorithm; never used as a parity reference)
@@ -67,6 +71,8 @@ inline double val(float x) { return x; }
 inline float xsqrt(float x) { return std::sqrt(x); }
 inline float xatan2(float y, float x) { return std::atan2(y, x); }
 inline float xasin(float x) { return std::asin(x); }
+inline float xsin(float x) { return std::sin(x); }
+inline float xcos(float x) { return std::cos(x); }
 template <class T> inline T xmax(T a, T b) { return (a < b) ? b : a; }
 template <class T> inline T xmin(T a, T b) { return (b < a) ? b : a; }
 template <class T> inline T xclamp(T x, T lo, T hi) { return xmin(xmax(x, lo), hi); }
@@ -319,7 +325,15 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
         else tau[i] = tau[i] + T(J.act_strength) * (xclamp(a, T(J.lo[i]), T(J.hi[i])) - th[i]);
       }
     }
-    V3<T> tw = rotate(fp, v3(tau[0], tau[1], tau[2]));
+    // torque component i acts about the i-th rotation axis of the intrinsic X-Y-Z
+    // decomposition, in the parent joint frame (R7 as amended in DESIGN.md):
+    //   a0 = x,  a1 = Rx(θ0)·y = (0, cos θ0, sin θ0),
+    //   a2 = Rx(θ0)·Ry(θ1)·z = (sin θ1, −sin θ0 cos θ1, cos θ0 cos θ1)
+    const T c0 = xcos(th[0]), s0 = xsin(th[0]), c1 = xcos(th[1]), s1 = xsin(th[1]);
+    V3<T> a1 = v3(T(0.0), c0, s0);
+    V3<T> a2 = v3(s1, -(s0 * c1), c0 * c1);
+    V3<T> tj = v3(tau[0], T(0.0), T(0.0)) + tau[1] * a1 + tau[2] * a2;
+    V3<T> tw = rotate(fp, tj);
     V3<T> td = T(J.c_a) * (P.w - C.w);
     F[J.child] = F[J.child] + f;
     Tq[J.child] = Tq[J.child] + ((tw + td) + cross(rc, f));

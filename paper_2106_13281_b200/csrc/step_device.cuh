@@ -266,7 +266,14 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
       }
     }
   }
-  V3T<S> twd = rotate(fp, V3T<S>{tau[0], tau[1], tau[2]});
+  // torque component i about the i-th rotation axis of R = Rx(θ0)Ry(θ1)Rz(θ2) in the
+  // parent joint frame (R7 as amended): a0 = x; a1 = Rx(θ0)y =
+  // (0, R22, −R12)/cos θ1; a2 = Rx(θ0)Ry(θ1)z = (R02, R12, R22), the third column of R.
+  S c2 = R12 * R12 + R22 * R22;  // cos² θ1
+  S ic = sel(gt(c2, bc<S>(0.f)), vrsqrt(c2), bc<S>(0.f));
+  S t1 = tau[1] * ic;
+  V3T<S> tj{tau[0] + tau[2] * R02, t1 * R22 + tau[2] * R12, tau[2] * R22 - t1 * R12};
+  V3T<S> twd = rotate(fp, tj);
   if (!(flags & kJNoCa)) twd = twd + scale(ca_s.x, wp - wc);
   V3T<S> tc = cross_add(rc, f, twd);
   V3T<S> tp = cross_add(rp, f, twd);

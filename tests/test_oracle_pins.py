@@ -166,6 +166,56 @@ joints { name: "J" parent: "P" child: "C" stiffness: 1000 limit_stiffness: 300
         assert abs(q["ang"][0, 1, 0] - w) < 1e-12
 
 
+def test_alignment_torque_about_the_rotated_euler_axis():
+    """R7 (as amended): the alignment spring of axis 1 acts about
+    a1 = Rx(θ0)·ŷ.  A hinge at angle θ0 = 0.5 (free, inside its limits) with an
+    alignment error α about that rotated axis therefore rotates about the fixed
+    axis a1 only: α follows the scalar recurrence α_{n+1} = α_n + 2·atan(ω_n h/2),
+    ω_{n+1} = ω_n − (k_a/I)·α_{n+1}·h, and θ0 stays 0.5."""
+    txt = """dt: 0.01
+bodies { name: "P" frozen { all: true } }
+bodies { name: "C" mass: 1 inertia { x: 2 y: 2 z: 2 } }
+joints { name: "J" parent: "P" child: "C" stiffness: 1000 angular_stiffness: 400
+  angle_limit { min: -60 max: 60 } }"""
+    o = oracle.Oracle(txt)
+    th0, alpha = 0.5, 0.03
+    a1 = np.array([0.0, math.cos(th0), math.sin(th0)])
+    qx = np.array([math.cos(th0 / 2), math.sin(th0 / 2), 0, 0])
+    qa = np.array([math.cos(alpha / 2), *(math.sin(alpha / 2) * a1)])  # rotation about a1 by α
+    qc = oracle.system.qmul(qa, qx)                                    # = Rx(θ0)·Ry(α)
+    q = qp1(o, rot=[[1, 0, 0, 0], qc])
+    al, w = alpha, 0.0
+    for _ in range(200):
+        q, _ = o.step(q)
+        al = al + 2 * math.atan(w * 0.01 / 2)
+        w = w - (400 / 2) * al * 0.01
+        r = q["rot"][0, 1]
+        # relative rotation back to the hinge: conj(qx) = rotation about a1 by the current α
+        rel = oracle.system.qmul(r, oracle.system.qconj(qx))
+        assert abs(2 * math.atan2(np.dot(rel[1:], a1), rel[0]) - al) < 1e-10
+        assert np.allclose(q["ang"][0, 1], w * a1, atol=1e-10)
+
+
+def test_undamped_energy_drift_shrinks_with_h():
+    """Fig. 5 energy protocol in fp64: the undamped, gravity- and
+    contact-free humanoid kicked at 1 m/s keeps its energy to O(h), and the drift
+    after 1 s shrinks as the substep halves."""
+    import sys as _sys
+    _sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    import astronaut
+    drifts = []
+    for S in (2, 4, 8):
+        o = oracle.Oracle(astronaut.astronaut_text(S, 0.0))
+        qp = o.batch_default_qp(8)
+        kick = np.random.default_rng(0).normal(size=qp["vel"].shape)
+        qp["vel"] = kick / np.linalg.norm(kick, axis=-1, keepdims=True)
+        E0 = astronaut.invariants(o.sys, qp)[2]
+        for _ in range(67):
+            qp, _ = o.step(qp, np.zeros((8, o.act_dim)))
+        drifts.append(np.abs(astronaut.invariants(o.sys, qp)[2] - E0).mean() / E0.mean())
+    assert drifts[0] < 0.15 and drifts[1] < drifts[0] and drifts[2] < drifts[1], drifts
+
+
 def test_angle_actuator_servo_recurrence():
     """ANGLE actuator (R12): τ = s·(clamp(a, lo, hi) − θ) about the free axis; with wide
     limits and no other torque: θ_{n+1} = θ_n + 2·atan(ω_n h/2), ω_{n+1} = ω_n +

@@ -6,13 +6,14 @@ gravity disabled; (momentum) limbs randomly actuated for 1 s with ≈ 0.5 N·m
 per actuator per step; (energy) actuators disabled, every body part given a
 random 1 m/s kick, energy drift measured after 1 s; averaged over 128 seeds,
 single precision.  Fidelity axis: the substep length h (dt fixed, substeps
-1, 2, 4, 8).
+2, 4, 8, 16; at 1 substep the undamped humanoid's stiff springs are beyond the
+explicit scheme's stability limit, R6).
 
 Quantities (host-side analysis of the GPU's QP, fp64):
   P = Σ m v;  L = Σ (x × m v + I_w ω) about the origin (isotropic inertia, R4);
-  E = Σ ½ m|v|² + ½ ω·I_w ω + Σ_joints ½ k |Δx|² (anchor springs; the angular
-      alignment/limit springs are reported separately as they are not
-      potential-derived for d ≥ 2, R7).
+  E = Σ ½ m|v|² + ½ ω·I_w ω + Σ_joints [½ k |Δx|² + ½ k_a Σ_{i≥d} θ_i²
+      + ½ k_l Σ_{i<d} (θ_i − clamp(θ_i, lo_i, hi_i))²]  (anchor, alignment and limit
+      springs; θ the joint's intrinsic X-Y-Z angles, R7).
     python tools/astronaut.py [--seeds 128] [--json out.json]
 """
 from __future__ import annotations
@@ -51,7 +52,7 @@ def quat_rotate(q, v):
 
 
 def invariants(o_sys, qp):
-    """P, L (about the origin), kinetic energy and anchor-spring energy per env (fp64)."""
+    """P, L (about the origin) and total mechanical energy per env (fp64)."""
     m = np.array([b.mass for b in o_sys.bodies])[None, :, None]
     I = np.array([b.inertia for b in o_sys.bodies])[None]
     x, q, v, w = (qp[k].astype(np.float64) for k in ("pos", "rot", "vel", "ang"))
@@ -66,10 +67,36 @@ def invariants(o_sys, qp):
         ap = x[:, j.parent] + quat_rotate(q[:, j.parent], j.parent_offset)
         ac = x[:, j.child] + quat_rotate(q[:, j.child], j.child_offset)
         pe += 0.5 * j.stiffness * ((ap - ac) ** 2).sum(-1)
+        th = joint_angles(q[:, j.parent], q[:, j.child], j)
+        for i in range(3):
+            if i < j.dof:
+                excess = th[:, i] - np.clip(th[:, i], j.limits[i, 0], j.limits[i, 1])
+                pe += 0.5 * j.limit_stiffness * excess ** 2
+            else:
+                pe += 0.5 * j.angular_stiffness * th[:, i] ** 2
     return P, L, ke + pe
 
 
-def run(seeds=128, substeps_list=(1, 2, 4, 8), horizon_s=1.0):
+def qmul(a, b):
+    aw, ax, ay, az = np.moveaxis(a, -1, 0)
+    bw, bx, by, bz = np.moveaxis(b, -1, 0)
+    return np.stack([aw * bw - ax * bx - ay * by - az * bz, aw * bx + ax * bw + ay * bz - az * by,
+                     aw * by - ax * bz + ay * bw + az * bx, aw * bz + ax * by - ay * bx + az * bw], -1)
+
+
+def joint_angles(qp, qc, j):
+    """Intrinsic X-Y-Z angles of conj(q_p⊗J_p)⊗(q_c⊗J_c) (analysis copy of R7's extraction)."""
+    conj = np.array([1, -1, -1, -1])
+    jc = qmul(j.reference_rotation * conj, j.rotation)
+    qr = qmul(qmul(qp, np.broadcast_to(j.rotation, qp.shape)) * conj, qmul(qc, np.broadcast_to(jc, qc.shape)))
+    qr = np.where(qr[:, :1] < 0, -qr, qr)
+    w, x, y, z = qr.T
+    return np.stack([np.arctan2(-2 * (y * z - w * x), 1 - 2 * (x * x + y * y)),
+                     np.arcsin(np.clip(2 * (x * z + w * y), -1, 1)),
+                     np.arctan2(-2 * (x * y - w * z), 1 - 2 * (y * y + z * z))], -1)
+
+
+def run(seeds=128, substeps_list=(2, 4, 8, 16), horizon_s=1.0):
     import torch
 
     import oracle
