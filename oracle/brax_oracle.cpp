@@ -325,14 +325,24 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
         else tau[i] = tau[i] + T(J.act_strength) * (xclamp(a, T(J.lo[i]), T(J.hi[i])) - th[i]);
       }
     }
-    // torque component i acts about the i-th rotation axis of the intrinsic X-Y-Z
-    // decomposition, in the parent joint frame (R7 as amended in DESIGN.md):
-    //   a0 = x,  a1 = Rx(θ0)·y = (0, cos θ0, sin θ0),
-    //   a2 = Rx(θ0)·Ry(θ1)·z = (sin θ1, −sin θ0 cos θ1, cos θ0 cos θ1)
-    const T c0 = xcos(th[0]), s0 = xsin(th[0]), c1 = xcos(th[1]), s1 = xsin(th[1]);
-    V3<T> a1 = v3(T(0.0), c0, s0);
-    V3<T> a2 = v3(s1, -(s0 * c1), c0 * c1);
-    V3<T> tj = v3(tau[0], T(0.0), T(0.0)) + tau[1] * a1 + tau[2] * a2;
+    // τ_i is the generalised force conjugate to θ_i (R7 as amended in DESIGN.md): the
+    // relative angular velocity is ω = Σ θ̇_i a_i with the rotation axes of R = Rx Ry Rz
+    //   a0 = x,  a1 = Rx(θ0)·y = (0, cos θ0, sin θ0),  a2 = Rx(θ0)·Ry(θ1)·z,
+    // so the torque whose power is Σ τ_i θ̇_i (the gradient of the spring potential) is
+    // Σ τ_i b_i with b the dual basis (b_i·a_j = δ_ij), in the parent joint frame:
+    //   b0 = (1, sin θ0 tan θ1, −cos θ0 tan θ1),  b1 = a1,  b2 = (0, −sin θ0, cos θ0)/cos θ1.
+    // 1/cos θ1 is evaluated as cos θ1 / max(cos² θ1, 0.01) (gimbal-lock guard, R7).
+    // The sines and cosines are read off R = Rx(θ0)Ry(θ1)Rz(θ2): R02 = sin θ1,
+    // R12 = −sin θ0 cos θ1, R22 = cos θ0 cos θ1, so cos θ1 = √(R12² + R22²) ≥ 0.
+    const T c1 = xsqrt(R12 * R12 + R22 * R22);
+    const T s1 = xclamp(R02, T(-1.0), T(1.0));
+    const T c0 = (val(c1) > 0.0) ? R22 / c1 : T(1.0);
+    const T s0 = (val(c1) > 0.0) ? -(R12 / c1) : T(0.0);
+    const T ic = c1 / xmax(c1 * c1, T(0.01));
+    V3<T> b0 = v3(T(1.0), s0 * s1 * ic, -(c0 * s1 * ic));
+    V3<T> b1 = v3(T(0.0), c0, s0);
+    V3<T> b2 = v3(T(0.0), -(s0 * ic), c0 * ic);
+    V3<T> tj = tau[0] * b0 + tau[1] * b1 + tau[2] * b2;
     V3<T> tw = rotate(fp, tj);
     V3<T> td = T(J.c_a) * (P.w - C.w);
     F[J.child] = F[J.child] + f;

@@ -266,13 +266,15 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
       }
     }
   }
-  // torque component i about the i-th rotation axis of R = Rx(θ0)Ry(θ1)Rz(θ2) in the
-  // parent joint frame (R7 as amended): a0 = x; a1 = Rx(θ0)y =
-  // (0, R22, −R12)/cos θ1; a2 = Rx(θ0)Ry(θ1)z = (R02, R12, R22), the third column of R.
+  // τ_i is the generalised force conjugate to θ_i (R7 as amended): the parent-
+  // joint-frame torque is Σ τ_i b_i, b the dual basis of the rotation axes of Rx Ry Rz.
+  // With c1 = cos θ1 = √(R12² + R22²), sin θ0 = −R12/c1, cos θ0 = R22/c1, sin θ1 = R02:
+  //   tj = (τ0, u·R12 + t·R22, u·R22 − t·R12),  u = (τ2 − τ0·R02)/max(c1², 0.01),  t = τ1/c1.
   S c2 = R12 * R12 + R22 * R22;  // cos² θ1
   S ic = sel(gt(c2, bc<S>(0.f)), vrsqrt(c2), bc<S>(0.f));
   S t1 = tau[1] * ic;
-  V3T<S> tj{tau[0] + tau[2] * R02, t1 * R22 + tau[2] * R12, tau[2] * R22 - t1 * R12};
+  S u = (tau[2] - tau[0] * R02) * vmin(ic * ic, bc<S>(100.f));
+  V3T<S> tj{tau[0], u * R12 + t1 * R22, u * R22 - t1 * R12};
   V3T<S> twd = rotate(fp, tj);
   if (!(flags & kJNoCa)) twd = twd + scale(ca_s.x, wp - wc);
   V3T<S> tc = cross_add(rc, f, twd);

@@ -196,6 +196,58 @@ joints { name: "J" parent: "P" child: "C" stiffness: 1000 angular_stiffness: 400
         assert np.allclose(q["ang"][0, 1], w * a1, atol=1e-10)
 
 
+@pytest.mark.parametrize("dof", [1, 2, 3])
+def test_joint_torque_is_the_spring_potential_gradient(dof):
+    """R7 (as amended): the angular-spring torque on the child is −∂V/∂φ, V = ½k_l Σ_{i<dof}
+    (θ_i − clamp θ_i)² + ½k_a Σ_{i≥dof} θ_i², φ a world-frame rotation of the child — the
+    conservative force PAPER.md:264's energy behaviour needs.  V is evaluated here by an
+    independent numpy Euler extraction and differentiated by central differences; the
+    oracle's torque is read from one substep of an iso-inertia child: Δω = h·τ/I."""
+    import sys as _sys
+    _sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    import astronaut
+    lims = " ".join(["angle_limit { min: -10 max: 10 }", "angle_limit { min: -5 max: 5 }",
+                     "angle_limit { min: -8 max: 12 }"][:dof])
+    txt = f"""dt: 0.001
+substeps: 1
+bodies {{ name: "P" frozen {{ all: true }} }}
+bodies {{ name: "C" mass: 1 inertia {{ x: 2 y: 2 z: 2 }} }}
+joints {{ name: "J" parent: "P" child: "C" stiffness: 1000 angular_stiffness: 300
+  limit_stiffness: 500 rotation {{ z: 30 x: 20 }} reference_rotation {{ y: 15 }} {lims} }}"""
+    o = oracle.Oracle(txt)
+    j = o.sys.joints[0]
+    rng = np.random.default_rng(dof)
+    for _ in range(5):
+        ax = rng.normal(size=3)
+        ax /= np.linalg.norm(ax)
+        ang = rng.uniform(0.2, 0.8)
+        qc = np.array([math.cos(ang / 2), *(math.sin(ang / 2) * ax)])
+        qp0 = np.array([1.0, 0, 0, 0])
+
+        def V(q):
+            th = astronaut.joint_angles(qp0[None], q[None], j)[0]
+            v = 0.0
+            for i in range(3):
+                if i < dof:
+                    v += 0.5 * j.limit_stiffness * (th[i] - np.clip(th[i], *j.limits[i])) ** 2
+                else:
+                    v += 0.5 * j.angular_stiffness * th[i] ** 2
+            return v
+        eps = 1e-6
+        grad = np.zeros(3)
+        for k in range(3):
+            d = np.zeros(3)
+            d[k] = eps
+            qplus = oracle.system.qmul(np.array([math.cos(eps / 2), *(math.sin(eps / 2) * d / eps)]), qc)
+            qminus = oracle.system.qmul(np.array([math.cos(eps / 2), *(-math.sin(eps / 2) * d / eps)]), qc)
+            grad[k] = (V(qplus) - V(qminus)) / (2 * eps)
+        q = qp1(o, rot=[qp0, qc])
+        q, _ = o.step(q)
+        tau = q["ang"][0, 1] * 2.0 / 0.001
+        assert np.linalg.norm(grad) > 1.0
+        assert np.allclose(tau, -grad, rtol=1e-6, atol=1e-6 * np.linalg.norm(grad)), (tau, -grad)
+
+
 def test_undamped_energy_drift_shrinks_with_h():
     """Fig. 5 energy protocol in fp64: the undamped, gravity- and
     contact-free humanoid kicked at 1 m/s keeps its energy to O(h), and the drift
