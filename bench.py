@@ -350,7 +350,7 @@ def run_b200(args):
                    "l2": f"inputs larger than L2: {R} rotating batches x {2 * qp_bytes / 1e6:.1f} MB "
                          f"(> 126 MB L2)",
                    "launch": "CUDA graph of brax_step launches" if graph is not None else "eager launches",
-                   "warps_per_block": system.info.warps_per_block},
+                   "kernel_config": system.launch_config(n)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K, "clocks": clocks,
         "blowups": total_blowups,
     }

@@ -126,6 +126,20 @@ brax_status brax_system_slot_table(const brax_system *sys, int32_t *out);
 brax_status brax_system_set_tracing(brax_system *sys, int enable);
 brax_status brax_system_phase_cycles(brax_system *sys, uint64_t out[4]);
 
+/* Launch configuration of the step kernel.  Every configuration
+ * computes bit-identical results (explicit rounding of every operation), so the
+ * choice only affects speed.  With autotuning on (the default), the first launch
+ * of a given n_envs (>= 256) outside CUDA-graph capture times one step of every
+ * configuration on a scratch copy of the caller's state (the caller's buffers are
+ * not written; the call synchronises its stream once) and remembers the fastest
+ * for that n_envs; otherwise a size heuristic chooses.  Environment overrides for
+ * experiments: BRAX_PLAN="G,V", BRAX_MAXREG=R.
+ * brax_system_launch_config writes, for a launch of n_envs envs, out[6] =
+ * {G lane groups per warp, V envs per lane, E envs per block, warps per block,
+ * register budget, 1 if measured by the autotuner else 0}; it does not tune. */
+brax_status brax_system_set_autotune(brax_system *sys, int enable);
+brax_status brax_system_launch_config(const brax_system *sys, int64_t n_envs, int32_t out[6]);
+
 /* Lint warning i (0 <= i < n_lint_warnings) as text; NULL if out of range. */
 const char *brax_system_lint_warning(const brax_system *sys, int32_t i);
 

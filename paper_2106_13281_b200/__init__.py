@@ -75,6 +75,8 @@ _SIGS = {
     "brax_system_lint_warning": ([_P, C.c_int32], C.c_char_p),
     "brax_system_set_tracing": ([_P, C.c_int], C.c_int),
     "brax_system_phase_cycles": ([_P, C.POINTER(C.c_uint64)], C.c_int),
+    "brax_system_set_autotune": ([_P, C.c_int], C.c_int),
+    "brax_system_launch_config": ([_P, C.c_int64, C.POINTER(C.c_int32)], C.c_int),
     "brax_default_qp": ([_P, _P, _P, _P, _P], C.c_int),
     "brax_reset": ([_P, brax_qp, C.c_int64, C.c_uint64, C.c_float, C.c_float, _P], C.c_int),
     "brax_step": ([_P, brax_qp, _P, brax_qp, C.c_int64, _P], C.c_int),
@@ -242,6 +244,15 @@ class System:
 
     def set_tracing(self, enable: bool = True):
         _check(lib.brax_system_set_tracing(self._sys, int(enable)))
+
+    def set_autotune(self, enable: bool = True):
+        _check(lib.brax_system_set_autotune(self._sys, int(enable)))
+
+    def launch_config(self, n_envs: int):
+        """dict(G, V, E, warps, regs, tuned) of the next step launch of n_envs envs (see brax_system_launch_config)."""
+        out = (C.c_int32 * 6)()
+        _check(lib.brax_system_launch_config(self._sys, int(n_envs), out))
+        return dict(zip(("G", "V", "E", "warps", "regs", "tuned"), (int(x) for x in out)))
 
     def phase_cycles(self):
         """(prologue, joints+contacts, integrators, epilogue) SM cycles summed over blocks since the last call."""

@@ -214,6 +214,27 @@ brax_status brax_system_phase_cycles(brax_system* sys, uint64_t out[4]) {
   return BRAX_OK;
 }
 
+brax_status brax_system_set_autotune(brax_system* sys, int enable) {
+  if (!sys) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
+  sys->impl->autotune = enable != 0;
+  return BRAX_OK;
+}
+
+brax_status brax_system_launch_config(const brax_system* sys, int64_t n_envs, int32_t out[6]) {
+  if (!sys || !out) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
+  if (n_envs < 0) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs < 0");
+  const brax::System& s = *sys->impl;
+  const brax::LaunchConfig c = brax::launch_config(s, n_envs);
+  const brax::DPlan& P = s.hd.plan[c.plan];
+  out[0] = P.G;
+  out[1] = P.V;
+  out[2] = P.E;
+  out[3] = P.W;
+  out[4] = c.regs;
+  out[5] = c.tuned ? 1 : 0;
+  return BRAX_OK;
+}
+
 const char* brax_system_lint_warning(const brax_system* sys, int32_t i) {
   if (!sys || i < 0 || size_t(i) >= sys->impl->lint.size()) return nullptr;
   return sys->impl->lint[i].c_str();

@@ -78,10 +78,21 @@ struct alignas(16) DSlot {  // 40 words
 };
 
 // Shared-memory layouts (words): per (item, lane) records, 16-byte aligned,
-// strides chosen so a warp's LDS.128 / STS.128 are bank-conflict free.
+// strides chosen so a warp's LDS.128 / STS.128 are bank-conflict free (an odd
+// number of 16-byte units).  One env per lane (V = 1):
 constexpr int kQS = 20;   // QP record: pos 0-2 | rot 4-7 (w,x,y,z) | vel 8-10 | ang 12-14
 constexpr int kJS = 12;   // joint record: F 0-2 | T_child 4-6 | T_parent 8-10
 constexpr int kCS = 12;   // slot record: P 0-2, active 3 | r_A×P 4-6 | r_B×P 8-10
+// Two envs per lane (V = 2): one record per lane holds both envs interleaved
+// component by component — field f, component c, env half h at word
+// 8f + 4(c >> 1) + 2(c & 1) + h — so an LDS.128 yields two (env0, env1) register
+// pairs, the operands of the packed FP32 instructions (FFMA2 / FMUL2 / FADD2).
+constexpr int kQS2 = 36;  // pos 0-7 | rot 8-15 | vel 16-23 | ang 24-31
+constexpr int kJS2 = 28;  // F 0-7 | T_child 8-15 | T_parent 16-23
+constexpr int kCS2 = 28;  // P 0-5, active 6-7 | r_A×P 8-15 | r_B×P 16-23
+BRAX_HD inline int32_t rec_q(int32_t V) { return V == 2 ? kQS2 : kQS; }
+BRAX_HD inline int32_t rec_j(int32_t V) { return V == 2 ? kJS2 : kJS; }
+BRAX_HD inline int32_t rec_c(int32_t V) { return V == 2 ? kCS2 : kCS; }
 
 // Incidence entries of the body gather (fixed order: joints by index, then slots
 // by index, R29): (item index << 4) | torque-word offset in the record (4 for the
@@ -89,19 +100,22 @@ constexpr int kCS = 12;   // slot record: P 0-2, active 3 | r_A×P 4-6 | r_B×P 
 BRAX_HD inline int32_t inc_pack(int index, bool second_side) { return (index << 4) | (second_side ? 8 : 4); }
 
 // Shared-memory layout of the step kernel (words; every region 16-byte aligned).
-//   [2 mbarriers][tables][QP records B·E·kQS][U][sA A·E][action staging E·A][counts C·E][status E]
-// U holds the joint and slot records during the substeps and the contiguous
-// TMA staging chunks (pos|rot|vel|ang, E·B·13 words) while loading / storing.
+//   [2 mbarriers][tables][QP records B·L·rec_q][U][sA A·E][action staging E·A][counts C·E][status E]
+// with L = E/V lanes (records) per body or item.  U holds the joint and slot
+// records during the substeps and the contiguous TMA staging chunks
+// (pos|rot|vel|ang, E·B·13 words) while loading / storing.
 struct SmemLayout {
   int32_t blob, q, u, a, astg, cnt, stat, total_words;
 };
 BRAX_HD inline int32_t round4(int32_t w) { return (w + 3) & ~3; }
-BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A, int32_t E, int32_t blob_words) {
+BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A, int32_t E, int32_t V,
+                                      int32_t blob_words) {
   SmemLayout L;
+  const int32_t LG = E / V;
   L.blob = 4;
   L.q = L.blob + round4(blob_words);
-  L.u = L.q + B * E * kQS;
-  const int32_t recs = J * E * kJS + C * E * kCS, stg = E * B * 13;
+  L.u = L.q + B * LG * rec_q(V);
+  const int32_t recs = J * LG * rec_j(V) + C * LG * rec_c(V), stg = E * B * 13;
   L.a = L.u + round4(recs > stg ? recs : stg);
   L.astg = L.a + round4(A * E);
   L.cnt = L.astg + round4(A * E);

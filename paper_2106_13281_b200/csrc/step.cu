@@ -53,13 +53,15 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const DHeader& H = ka.hd;
   const DPlan& P = H.plan[ka.plan];
   const StepArgs& a = ka.a;
+  constexpr int V = Lanes<S>::V, QS = Lanes<S>::QS, JS = Lanes<S>::JS, CS = Lanes<S>::CS;
   const int B = H.B, J = H.J, C = H.C, A = H.A, E = P.E, G = P.G;
-  const SmemLayout L = smem_layout(B, J, C, A, E, H.blob_words);
+  const SmemLayout L = smem_layout(B, J, C, A, E, V, H.blob_words);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [0] tables + QP, [1] actions
   uint32_t* sBlob = smem + L.blob;
   float* sQ = reinterpret_cast<float*>(smem + L.q);
   float* sJ = reinterpret_cast<float*>(smem + L.u);
-  float* sC = sJ + J * E * kJS;
+  const int LG = 32 / G;  // lanes per group = records per item (E = LG·V envs)
+  float* sC = sJ + J * LG * JS;
   float* stg = reinterpret_cast<float*>(smem + L.u);  // aliases sJ/sC outside the substeps
   float* sA = reinterpret_cast<float*>(smem + L.a);
   float* sAstg = reinterpret_cast<float*>(smem + L.astg);
@@ -78,9 +80,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       tr_mark = t;
     }
   };
-  const int LG = 32 / G;                                 // lanes per group
-  const int grp = lane / LG, el = lane - grp * LG;       // lane group; first env slot of this lane
-  const int o2q = LG * kQS, o2j = LG * kJS, o2c = LG * kCS;  // second env (S = F2): + LG slots
+  const int grp = lane / LG, el = lane - grp * LG;  // lane group; this lane's record slot (envs el, el + LG)
   const int64_t e0 = int64_t(blockIdx.x) * E;
   const int nvalid = (a.n_envs - e0 < E) ? int(a.n_envs - e0) : E;
   const bool bulk = a.bulk_ok && nvalid == E;          // block-uniform
@@ -112,9 +112,9 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       tma_load(sAstg, a.actions + e0 * A, act_bytes, &bars[1]);
     }
   }
-  if (!bulk) load_block(a, sQ, sStat, B, E, e0, nvalid);  // ragged tail / unaligned: per-row loads
+  if (!bulk) load_block<V>(a, sQ, B, E, e0, nvalid);  // ragged tail / unaligned: per-row loads
   mbar_wait(&bars[0], 0);
-  if (bulk) stg_to_records(stg, sQ, B, E, E);
+  if (bulk) stg_to_records<V>(stg, sQ, B, E);
   for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
   __syncthreads();
   lap(0);
@@ -130,25 +130,25 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const int32_t* jinc = reinterpret_cast<const int32_t*>(sBlob + H.off_jinc);
   const int32_t* cinc_begin = reinterpret_cast<const int32_t*>(sBlob + H.off_cinc_begin);
   const int32_t* cinc = reinterpret_cast<const int32_t*>(sBlob + H.off_cinc);
-  const float* sJe = sJ + el * kJS;  // this env's record of joint 0 (joint j: + j*E*kJS)
-  const float* sCe = sC + el * kCS;
+  const float* sJe = sJ + el * JS;  // this lane's record of joint 0 (joint j: + j·LG·JS)
+  const float* sCe = sC + el * CS;
   const int it0 = item_begin[warp], it1 = item_begin[warp + 1];
   const int bw0 = body_begin[warp], bw1 = body_begin[warp + 1];
 
   // S2 of the first substep; every later S2 is fused into the previous substep's integrate()
   for (int i = bw0; i < bw1; ++i) {
     int b = bodies_of_warp[i * G];
-    if (b >= 0) kinematic<S>(bodies[b], Row<S>{sQ + (b * E + el) * kQS, o2q}, H.h);
+    if (b >= 0) kinematic<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, H.h);
   }
   for (int64_t step = 0; step < a.n_steps; ++step) {
     if (act_bulk) {  // this step's actions arrived in sAstg [E][A]; transpose to sA [A][E]
       mbar_wait(&bars[1], uint32_t(step & 1));
       for (int i = tid; i < E * A; i += blockDim.x) {
         const int env = i / A, k = i - env * A;
-        sA[k * E + env] = sAstg[i];
+        sA[k * E + eslot<V>(env, E)] = sAstg[i];
       }
     } else {
-      load_actions(a, sA, A, E, step, e0, nvalid);
+      load_actions<V>(a, sA, A, E, step, e0, nvalid);
     }  // sA is read in phase 2, after a barrier
     for (int it = it0; it < it1; ++it) {
       int item = items[it * G];
@@ -169,16 +169,16 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         if (item < 0) continue;
         if (item < J) {
           const DJoint& jt = joints[item];
-          joint<S>(jt, Row<S>{sQ + (jt.parent * E + el) * kQS, o2q}, Row<S>{sQ + (jt.child * E + el) * kQS, o2q},
-                   sA + el, E, LG, sJ + (item * E + el) * kJS, o2j);
+          joint<S>(jt, Row<S>{sQ + (jt.parent * LG + el) * QS}, Row<S>{sQ + (jt.child * LG + el) * QS}, sA + el * V,
+                   E, sJ + (item * LG + el) * JS);
         } else {
           int c = item - J;
           const DSlot& sl = slots[c];
-          float* cp = sCnt + c * E + el;
-          S cnt = Lanes<S>::ld(cp, LG);
-          contact<S>(sl, Row<S>{sQ + (sl.a * E + el) * kQS, o2q}, Row<S>{sQ + (sl.b * E + el) * kQS, o2q},
-                     1.f + H.e, H.beta_over_h, H.mu, sC + (c * E + el) * kCS, o2c, cnt);
-          store_count(cp, LG, cnt);
+          float* cp = sCnt + c * E + el * V;
+          S cnt = Lanes<S>::ld(cp);
+          contact<S>(sl, Row<S>{sQ + (sl.a * LG + el) * QS}, Row<S>{sQ + (sl.b * LG + el) * QS}, 1.f + H.e,
+                     H.beta_over_h, H.mu, sC + (c * LG + el) * CS, cnt);
+          Lanes<S>::st(cp, cnt);
         }
       }
       __syncthreads();
@@ -190,24 +190,24 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
 #pragma unroll 4
         for (int k = jinc_begin[b]; k < jinc_begin[b + 1]; ++k) {
           int e = jinc[k];
-          acc.joint(sJe + (e >> 4) * (E * kJS), o2j, e);
+          acc.joint(sJe + (e >> 4) * (LG * JS), e);
         }
 #pragma unroll 4
         for (int k = cinc_begin[b]; k < cinc_begin[b + 1]; ++k) {
           int e = cinc[k];
-          acc.slot(sCe + (e >> 4) * (E * kCS), o2c, e);
+          acc.slot(sCe + (e >> 4) * (LG * CS), e);
         }
         const bool kin = !(step + 1 == a.n_steps && s + 1 == H.S);  // fused S2 of the next substep
-        integrate<S>(bodies[b], Row<S>{sQ + (b * E + el) * kQS, o2q}, acc, H.h, H.g, kin);
+        integrate<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, acc, H.h, H.g, kin);
       }
     }
   }
   lap(2);
   __syncthreads();
   // S9: status bits, contact counts, and the single write-back of the QP (TMA bulk for full blocks)
-  block_extras(a, sQ, sCnt, sStat, B, C, E, e0, nvalid);
+  block_extras<V>(a, sQ, sCnt, sStat, B, C, E, e0, nvalid);
   if (bulk) {
-    records_to_stg(sQ, stg, B, E, E);
+    records_to_stg<V>(sQ, stg, B, E);
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
@@ -222,7 +222,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       tma_store_commit_wait();
     }
   } else {
-    store_block(a, sQ, B, E, e0, nvalid);
+    store_block<V>(a, sQ, B, E, e0, nvalid);
   }
   if (a.status) {
     __syncthreads();
@@ -240,20 +240,22 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
 // alone would leave the SMs with few independent env groups to overlap their
 // per-substep barriers; G = 1 once the grid fills the GPU.
 int choose_plan(const System& sys, int64_t n_envs) {
-  if (const char* e = std::getenv("BRAX_PLAN")) {  // "G,V" override (experiments)
+  auto fits = [&](int i) { return sys.hd.plan[i].smem_bytes <= 227 * 1024; };  // plan 0 always fits
+  if (const char* e = std::getenv("BRAX_PLAN")) {  // "G,V" override (experiments; ignored if it does not fit)
     int g = 0, v = 0;
     if (std::sscanf(e, "%d,%d", &g, &v) == 2)
       for (int i = 0; i < kNumPlans; ++i)
-        if (sys.hd.plan[i].G == g && sys.hd.plan[i].V == v) return i;
+        if (sys.hd.plan[i].G == g && sys.hd.plan[i].V == v && fits(i)) return i;
   }
   int sms = sys.num_sms > 0 ? sys.num_sms : 148;
   int64_t blocks32 = (n_envs + 31) / 32;
   // measured (profiles/): lane groups help only while the smaller blocks still
   // fit one per SM (the batch is too small to fill the GPU with 32-env blocks)
-  if (4 * blocks32 <= sms) return 2;
-  if (2 * blocks32 <= sms) return 1;
-  if (blocks32 >= 4 * sms) return 3;  // large batches: two envs per lane (G = 1, V = 2)
-  return 0;
+  int p = 0;
+  if (4 * blocks32 <= sms) p = 2;
+  else if (2 * blocks32 <= sms) p = 1;
+  else if (blocks32 >= 4 * sms) p = 3;  // large batches: two envs per lane (G = 1, V = 2)
+  return fits(p) ? p : 0;
 }
 
 // Register budget per thread: as many as possible while the SM still holds the
@@ -289,32 +291,137 @@ cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, 
   brax_step_kernel<S, R><<<grid, block, smem, stream>>>(ka);
   return cudaGetLastError();
 }
-}  // namespace
 
-cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream) {
-  if (a.n_envs <= 0 || a.n_steps <= 0) return cudaSuccess;
-  KArgs ka{a, sys.d_blob, sys.hd, choose_plan(sys, a.n_envs)};
+cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream) {
+  KArgs ka{a, sys.d_blob, sys.hd, plan};
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
                  al16(a.rot_out) && al16(a.vel_out) && al16(a.ang_out);
   ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * sys.hd.A) % 4 == 0);
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
   ka.a.phase_cycles = sys.trace ? sys.d_phase_cycles : nullptr;
-  const DPlan& P = sys.hd.plan[ka.plan];
+  const DPlan& P = sys.hd.plan[plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(P.smem_bytes);
-  const int regs = choose_regs(sys, P, int64_t(grid.x));
   if (P.V == 2) {
     if (regs >= 128) return launch_variant<F2, 128>(ka, grid, block, smem, stream);
     if (regs >= 96) return launch_variant<F2, 96>(ka, grid, block, smem, stream);
     return launch_variant<F2, 80>(ka, grid, block, smem, stream);
   }
-  if (regs >= 128) return launch_variant<float, 128>(ka, grid, block, smem, stream);
-  if (regs >= 112) return launch_variant<float, 112>(ka, grid, block, smem, stream);
-  if (regs >= 96) return launch_variant<float, 96>(ka, grid, block, smem, stream);
-  if (regs >= 80) return launch_variant<float, 80>(ka, grid, block, smem, stream);
-  if (regs >= 64) return launch_variant<float, 64>(ka, grid, block, smem, stream);
-  return launch_variant<float, 56>(ka, grid, block, smem, stream);
+  if (regs >= 128) return launch_variant<F1, 128>(ka, grid, block, smem, stream);
+  if (regs >= 112) return launch_variant<F1, 112>(ka, grid, block, smem, stream);
+  if (regs >= 96) return launch_variant<F1, 96>(ka, grid, block, smem, stream);
+  if (regs >= 80) return launch_variant<F1, 80>(ka, grid, block, smem, stream);
+  if (regs >= 64) return launch_variant<F1, 64>(ka, grid, block, smem, stream);
+  return launch_variant<F1, 56>(ka, grid, block, smem, stream);
+}
+
+// the register budget of the instantiated variant launch_with runs for `regs`
+int variant_regs(int V, int regs) {
+  static const int v2[] = {128, 96, 80}, v1[] = {128, 112, 96, 80, 64, 56};
+  const int* t = V == 2 ? v2 : v1;
+  const int n = V == 2 ? 3 : 6;
+  for (int i = 0; i < n; ++i)
+    if (regs >= t[i]) return t[i];
+  return t[n - 1];
+}
+
+bool plan_fits(const System& sys, int p) { return sys.hd.plan[p].smem_bytes <= 227 * 1024; }
+
+int64_t grid_of(const System& sys, int p, int64_t n) { return (n + sys.hd.plan[p].E - 1) / sys.hd.plan[p].E; }
+
+LaunchConfig heuristic_config(const System& sys, int64_t n) {
+  LaunchConfig c;
+  c.plan = choose_plan(sys, n);
+  const char* e = std::getenv("BRAX_MAXREG");
+  c.regs = variant_regs(sys.hd.plan[c.plan].V,
+                        e ? std::atoi(e) : choose_regs(sys, sys.hd.plan[c.plan], grid_of(sys, c.plan, n)));
+  return c;
+}
+
+// Times one step of every plan that fits (at its register budget) on a scratch
+// copy of the caller's state and actions; the caller's buffers are not written.
+LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
+  LaunchConfig best = heuristic_config(sys, a.n_envs);
+  const int64_t n = a.n_envs, B = sys.hd.B;
+  const size_t fbytes[4] = {size_t(n * B * 3 * 4), size_t(n * B * 4 * 4), size_t(n * B * 3 * 4),
+                            size_t(n * B * 3 * 4)};
+  float* buf = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), fbytes[0] + fbytes[1] + fbytes[2] + fbytes[3], stream) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return best;
+  }
+  float* f[4] = {buf, nullptr, nullptr, nullptr};
+  for (int k = 1; k < 4; ++k) f[k] = f[k - 1] + fbytes[k - 1] / 4;
+  const float* src[4] = {a.pos_in, a.rot_in, a.vel_in, a.ang_in};
+  for (int k = 0; k < 4; ++k) cudaMemcpyAsync(f[k], src[k], fbytes[k], cudaMemcpyDeviceToDevice, stream);
+  StepArgs t = a;
+  t.pos_in = t.pos_out = f[0];
+  t.rot_in = t.rot_out = f[1];
+  t.vel_in = t.vel_out = f[2];
+  t.ang_in = t.ang_out = f[3];
+  t.n_steps = 1;
+  t.status = nullptr;
+  t.contact_active = nullptr;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best_ms = 1e30f;
+  for (int p = 0; p < kNumPlans; ++p) {
+    if (!plan_fits(sys, p)) continue;
+    const int regs = variant_regs(sys.hd.plan[p].V, choose_regs(sys, sys.hd.plan[p], grid_of(sys, p, n)));
+    if (launch_with(sys, t, p, regs, stream) != cudaSuccess) {  // warm-up (and feasibility)
+      cudaGetLastError();
+      continue;
+    }
+    cudaEventRecord(e0, stream);
+    for (int r = 0; r < 3; ++r) launch_with(sys, t, p, regs, stream);
+    cudaEventRecord(e1, stream);
+    float ms = 0.f;
+    if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (ms < best_ms) {
+      best_ms = ms;
+      best.plan = p;
+      best.regs = regs;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(buf, stream);
+  cudaStreamSynchronize(stream);
+  best.tuned = true;
+  return best;
+}
+}  // namespace
+
+LaunchConfig launch_config(const System& sys, int64_t n_envs) {
+  if (std::getenv("BRAX_PLAN") || std::getenv("BRAX_MAXREG")) return heuristic_config(sys, n_envs);
+  {
+    std::lock_guard<std::mutex> g(sys.tune_mu);
+    auto it = sys.tuned.find(n_envs);
+    if (it != sys.tuned.end()) return it->second;
+  }
+  return heuristic_config(sys, n_envs);
+}
+
+cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream) {
+  if (a.n_envs <= 0 || a.n_steps <= 0) return cudaSuccess;
+  LaunchConfig c = launch_config(sys, a.n_envs);
+  // first launch of this batch size outside graph capture: measure every plan once
+  if (!c.tuned && sys.autotune && a.n_envs >= 256 && !std::getenv("BRAX_PLAN") && !std::getenv("BRAX_MAXREG")) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+      c = tune(sys, a, stream);
+      std::lock_guard<std::mutex> g(sys.tune_mu);
+      sys.tuned[a.n_envs] = c;
+    }
+    cudaGetLastError();
+  }
+  return launch_with(sys, a, c.plan, c.regs, stream);
 }
 
 }  // namespace brax

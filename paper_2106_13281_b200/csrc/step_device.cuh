@@ -19,48 +19,140 @@ namespace brax {
 namespace dev {
 
 // ---- per-lane scalar types -----------------------------------------------------
+// F1: one env per lane; F2: two envs per lane.  Both spell out every rounding
+// step the same way — products are lazy (M1 / M2) and contract into an FMA
+// exactly where the source writes `a*b + c`, `c - a*b` or `a*b + c*d`, every other
+// add / mul is rounded on its own (__fadd_rn / __fmul_rn / add.rn.f32x2 are never
+// re-fused by the compiler) — so a given env's result is bitwise the same under
+// every launch plan (V = 1 or 2), i.e. independent of the batch size.
+struct F1 { float x; };
 struct F2 { float x, y; };
 struct B2 { bool x, y; };
 
-__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return {a.x + b.x, a.y + b.y}; }
-__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return {a.x - b.x, a.y - b.y}; }
-__device__ __forceinline__ F2 operator*(F2 a, F2 b) { return {a.x * b.x, a.y * b.y}; }
-__device__ __forceinline__ F2 operator-(F2 a) { return {-a.x, -a.y}; }
-__device__ __forceinline__ F2 operator+(F2 a, float b) { return {a.x + b, a.y + b}; }
-__device__ __forceinline__ F2 operator+(float a, F2 b) { return {a + b.x, a + b.y}; }
-__device__ __forceinline__ F2 operator-(F2 a, float b) { return {a.x - b, a.y - b}; }
-__device__ __forceinline__ F2 operator-(float a, F2 b) { return {a - b.x, a - b.y}; }
-__device__ __forceinline__ F2 operator*(float a, F2 b) { return {a * b.x, a * b.y}; }
-__device__ __forceinline__ F2 operator*(F2 a, float b) { return {a.x * b, a.y * b}; }
+struct M1 {  // the product a*b, not yet rounded
+  F1 a, b;
+  __device__ __forceinline__ operator F1() const { return {__fmul_rn(a.x, b.x)}; }
+};
+__device__ __forceinline__ F1 fma1(F1 a, F1 b, F1 c) { return {__fmaf_rn(a.x, b.x, c.x)}; }
+__device__ __forceinline__ F1 neg1(F1 a) { return {-a.x}; }
+__device__ __forceinline__ F1 bc1(float f) { return {f}; }
+__device__ __forceinline__ M1 operator*(F1 a, F1 b) { return {a, b}; }
+__device__ __forceinline__ M1 operator*(float a, F1 b) { return {bc1(a), b}; }
+__device__ __forceinline__ M1 operator*(F1 a, float b) { return {a, bc1(b)}; }
+__device__ __forceinline__ M1 operator*(M1 m, F1 b) { return {F1(m), b}; }
+__device__ __forceinline__ M1 operator*(F1 a, M1 m) { return {a, F1(m)}; }
+__device__ __forceinline__ M1 operator*(M1 m, float b) { return {F1(m), bc1(b)}; }
+__device__ __forceinline__ M1 operator*(float a, M1 m) { return {bc1(a), F1(m)}; }
+__device__ __forceinline__ M1 operator*(M1 m, M1 n) { return {F1(m), F1(n)}; }
+__device__ __forceinline__ M1 operator-(M1 m) { return {neg1(m.a), m.b}; }
+__device__ __forceinline__ F1 operator-(F1 a) { return neg1(a); }
+__device__ __forceinline__ F1 operator+(F1 a, F1 b) { return {__fadd_rn(a.x, b.x)}; }
+__device__ __forceinline__ F1 operator-(F1 a, F1 b) { return {__fadd_rn(a.x, -b.x)}; }
+__device__ __forceinline__ F1 operator+(F1 a, float b) { return {__fadd_rn(a.x, b)}; }
+__device__ __forceinline__ F1 operator+(float a, F1 b) { return {__fadd_rn(a, b.x)}; }
+__device__ __forceinline__ F1 operator-(F1 a, float b) { return {__fadd_rn(a.x, -b)}; }
+__device__ __forceinline__ F1 operator-(float a, F1 b) { return {__fadd_rn(a, -b.x)}; }
+__device__ __forceinline__ F1 operator+(M1 m, F1 c) { return fma1(m.a, m.b, c); }
+__device__ __forceinline__ F1 operator+(F1 c, M1 m) { return fma1(m.a, m.b, c); }
+__device__ __forceinline__ F1 operator-(M1 m, F1 c) { return fma1(m.a, m.b, neg1(c)); }
+__device__ __forceinline__ F1 operator-(F1 c, M1 m) { return fma1(neg1(m.a), m.b, c); }
+__device__ __forceinline__ F1 operator+(M1 m, float c) { return fma1(m.a, m.b, bc1(c)); }
+__device__ __forceinline__ F1 operator+(float c, M1 m) { return fma1(m.a, m.b, bc1(c)); }
+__device__ __forceinline__ F1 operator-(M1 m, float c) { return fma1(m.a, m.b, bc1(-c)); }
+__device__ __forceinline__ F1 operator-(float c, M1 m) { return fma1(neg1(m.a), m.b, bc1(c)); }
+__device__ __forceinline__ F1 operator+(M1 m, M1 n) { return fma1(n.a, n.b, F1(m)); }
+__device__ __forceinline__ F1 operator-(M1 m, M1 n) { return fma1(neg1(n.a), n.b, F1(m)); }
 
-__device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+// F2 arithmetic runs on the packed FP32 pipes of sm_100a (FADD2 / FMUL2 / FFMA2: one
+// instruction for both envs), same contraction rules as F1; ptxas folds operand
+// negation and uniform / immediate scalars into the packed instruction.
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+  F2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// The rounded product as fma(a, b, −0): ptxas fuses a mul.rn.f32x2 into a following
+// add.rn.f32x2 (it does not for the scalar .rn forms), which would round differently
+// from F1.  The −0 addend is a __constant__ (a runtime value to ptxas), so the FFMA2
+// is neither simplified back to a multiply nor fused; fma(a, b, −0) = round(a·b)
+// including the sign of zero.
+__constant__ float kNegZero = -0.0f;
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+  F2 d;
+  const float z = kNegZero;
+  asm("{.reg .b64 ra, rb, rz, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mov.b64 rz, {%6,%6};\n\tfma.rn.f32x2 rd, ra, rb, rz;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(z));
+  return d;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mov.b64 rc, {%6,%7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ F2 neg2(F2 a) { return {-a.x, -a.y}; }
+__device__ __forceinline__ F2 bc2(float f) { return {f, f}; }
+struct M2 {  // the product a*b, not yet rounded
+  F2 a, b;
+  __device__ __forceinline__ operator F2() const { return mul2(a, b); }
+};
+__device__ __forceinline__ M2 operator*(F2 a, F2 b) { return {a, b}; }
+__device__ __forceinline__ M2 operator*(float a, F2 b) { return {bc2(a), b}; }
+__device__ __forceinline__ M2 operator*(F2 a, float b) { return {a, bc2(b)}; }
+__device__ __forceinline__ M2 operator*(M2 m, F2 b) { return {F2(m), b}; }
+__device__ __forceinline__ M2 operator*(F2 a, M2 m) { return {a, F2(m)}; }
+__device__ __forceinline__ M2 operator*(M2 m, float b) { return {F2(m), bc2(b)}; }
+__device__ __forceinline__ M2 operator*(float a, M2 m) { return {bc2(a), F2(m)}; }
+__device__ __forceinline__ M2 operator*(M2 m, M2 n) { return {F2(m), F2(n)}; }
+__device__ __forceinline__ M2 operator-(M2 m) { return {neg2(m.a), m.b}; }
+__device__ __forceinline__ F2 operator-(F2 a) { return neg2(a); }
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return add2(a, b); }
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return add2(a, neg2(b)); }
+__device__ __forceinline__ F2 operator+(F2 a, float b) { return add2(a, bc2(b)); }
+__device__ __forceinline__ F2 operator+(float a, F2 b) { return add2(bc2(a), b); }
+__device__ __forceinline__ F2 operator-(F2 a, float b) { return add2(a, bc2(-b)); }
+__device__ __forceinline__ F2 operator-(float a, F2 b) { return add2(bc2(a), neg2(b)); }
+__device__ __forceinline__ F2 operator+(M2 m, F2 c) { return fma2(m.a, m.b, c); }
+__device__ __forceinline__ F2 operator+(F2 c, M2 m) { return fma2(m.a, m.b, c); }
+__device__ __forceinline__ F2 operator-(M2 m, F2 c) { return fma2(m.a, m.b, neg2(c)); }
+__device__ __forceinline__ F2 operator-(F2 c, M2 m) { return fma2(neg2(m.a), m.b, c); }
+__device__ __forceinline__ F2 operator+(M2 m, float c) { return fma2(m.a, m.b, bc2(c)); }
+__device__ __forceinline__ F2 operator+(float c, M2 m) { return fma2(m.a, m.b, bc2(c)); }
+__device__ __forceinline__ F2 operator-(M2 m, float c) { return fma2(m.a, m.b, bc2(-c)); }
+__device__ __forceinline__ F2 operator-(float c, M2 m) { return fma2(neg2(m.a), m.b, bc2(c)); }
+__device__ __forceinline__ F2 operator+(M2 m, M2 n) { return fma2(n.a, n.b, F2(m)); }
+__device__ __forceinline__ F2 operator-(M2 m, M2 n) { return fma2(neg2(n.a), n.b, F2(m)); }
+
+__device__ __forceinline__ F1 vmin(F1 a, F1 b) { return {fminf(a.x, b.x)}; }
 __device__ __forceinline__ F2 vmin(F2 a, F2 b) { return {fminf(a.x, b.x), fminf(a.y, b.y)}; }
-__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ F1 vmax(F1 a, F1 b) { return {fmaxf(a.x, b.x)}; }
 __device__ __forceinline__ F2 vmax(F2 a, F2 b) { return {fmaxf(a.x, b.x), fmaxf(a.y, b.y)}; }
-__device__ __forceinline__ float vabs(float a) { return fabsf(a); }
+__device__ __forceinline__ F1 vabs(F1 a) { return {fabsf(a.x)}; }
 __device__ __forceinline__ F2 vabs(F2 a) { return {fabsf(a.x), fabsf(a.y)}; }
-__device__ __forceinline__ float vsqrt(float a) { return sqrtf(a); }
-__device__ __forceinline__ F2 vsqrt(F2 a) { return {sqrtf(a.x), sqrtf(a.y)}; }
-__device__ __forceinline__ float vrsqrt(float a) { return rsqrtf(a); }
+__device__ __forceinline__ F1 vrsqrt(F1 a) { return {rsqrtf(a.x)}; }
 __device__ __forceinline__ F2 vrsqrt(F2 a) { return {rsqrtf(a.x), rsqrtf(a.y)}; }
-__device__ __forceinline__ float vdiv(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ F1 vdiv(F1 a, F1 b) { return {__fdividef(a.x, b.x)}; }
 __device__ __forceinline__ F2 vdiv(F2 a, F2 b) { return {__fdividef(a.x, b.x), __fdividef(a.y, b.y)}; }
-__device__ __forceinline__ float vcopysign(float a, float b) { return copysignf(a, b); }
+__device__ __forceinline__ F1 vcopysign(F1 a, F1 b) { return {copysignf(a.x, b.x)}; }
 __device__ __forceinline__ F2 vcopysign(F2 a, F2 b) { return {copysignf(a.x, b.x), copysignf(a.y, b.y)}; }
-__device__ __forceinline__ bool lt(float a, float b) { return a < b; }
+__device__ __forceinline__ bool lt(F1 a, F1 b) { return a.x < b.x; }
 __device__ __forceinline__ B2 lt(F2 a, F2 b) { return {a.x < b.x, a.y < b.y}; }
-__device__ __forceinline__ bool gt(float a, float b) { return a > b; }
+__device__ __forceinline__ bool gt(F1 a, F1 b) { return a.x > b.x; }
 __device__ __forceinline__ B2 gt(F2 a, F2 b) { return {a.x > b.x, a.y > b.y}; }
-__device__ __forceinline__ float sel(bool m, float a, float b) { return m ? a : b; }
+__device__ __forceinline__ F1 sel(bool m, F1 a, F1 b) { return m ? a : b; }
 __device__ __forceinline__ F2 sel(B2 m, F2 a, F2 b) { return {m.x ? a.x : b.x, m.y ? a.y : b.y}; }
 __device__ __forceinline__ bool both(bool m, bool n) { return m && n; }
 __device__ __forceinline__ B2 both(B2 m, B2 n) { return {m.x && n.x, m.y && n.y}; }
 __device__ __forceinline__ bool any(bool m) { return m; }
 __device__ __forceinline__ bool any(B2 m) { return m.x || m.y; }
-__device__ __forceinline__ float as_count(bool m) { return m ? 1.f : 0.f; }
+__device__ __forceinline__ F1 as_count(bool m) { return {m ? 1.f : 0.f}; }
 __device__ __forceinline__ F2 as_count(B2 m) { return {m.x ? 1.f : 0.f, m.y ? 1.f : 0.f}; }
 template <class S> __device__ __forceinline__ S bc(float f);
-template <> __device__ __forceinline__ float bc<float>(float f) { return f; }
+template <> __device__ __forceinline__ F1 bc<F1>(float f) { return {f}; }
 template <> __device__ __forceinline__ F2 bc<F2>(float f) { return {f, f}; }
 template <class S> __device__ __forceinline__ S clampv(S x, float lo, float hi) {
   return vmin(vmax(x, bc<S>(lo)), bc<S>(hi));
@@ -72,6 +164,13 @@ template <class S> __device__ __forceinline__ V3T<S> operator+(V3T<S> a, V3T<S> 
 template <class S> __device__ __forceinline__ V3T<S> operator-(V3T<S> a, V3T<S> b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
 template <class S> __device__ __forceinline__ V3T<S> operator*(S s, V3T<S> a) { return {s * a.x, s * a.y, s * a.z}; }
 template <class S> __device__ __forceinline__ V3T<S> scale(float s, V3T<S> a) { return {s * a.x, s * a.y, s * a.z}; }
+// c + s·a with the products fused (one FMA per component)
+template <class S> __device__ __forceinline__ V3T<S> axpy(float s, V3T<S> a, V3T<S> c) {
+  return {s * a.x + c.x, s * a.y + c.y, s * a.z + c.z};
+}
+template <class S> __device__ __forceinline__ V3T<S> axpy(S s, V3T<S> a, V3T<S> c) {
+  return {s * a.x + c.x, s * a.y + c.y, s * a.z + c.z};
+}
 template <class S> __device__ __forceinline__ V3T<S> had(const float* m, V3T<S> a) { return {m[0] * a.x, m[1] * a.y, m[2] * a.z}; }
 template <class S> __device__ __forceinline__ S dot(V3T<S> a, V3T<S> b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 template <class S> __device__ __forceinline__ V3T<S> cross(V3T<S> a, V3T<S> b) {
@@ -141,70 +240,81 @@ template <class S> __device__ __forceinline__ S asin_f(S x) {
 }
 
 // ---- shared-memory access for V = 1 or 2 envs per lane ---------------------------
-// A lane of a group of L lanes handles env slot `el` and (S = F2) `el + L`; the
-// second env's record sits `o2` words after the first's.
-__device__ __forceinline__ float ld1(const float* p, int) { return *p; }
-__device__ __forceinline__ F2 ld2(const float* p, int o2) { return {p[0], p[o2]}; }
+// Records (device_tables.h): V = 1 — field f at words 4f..4f+3 of the env's record;
+// V = 2 — one record per lane, both envs interleaved: field f at words 8f..8f+7 as
+// (c0 env0, c0 env1, c1 env0, c1 env1 | c2 env0, c2 env1, c3 env0, c3 env1).
 template <class S> struct Lanes;
-template <> struct Lanes<float> {
-  static __device__ __forceinline__ float4 ld4(const float* p, int) { return *reinterpret_cast<const float4*>(p); }
-  static __device__ __forceinline__ V3T<float> ld3(const float* p, int o2) {
-    float4 a = ld4(p, o2);
-    return {a.x, a.y, a.z};
+template <> struct Lanes<F1> {
+  static constexpr int V = 1, M = 4;  // envs per lane, words per record field
+  static constexpr int QS = kQS, JS = kJS, CS = kCS;
+  static __device__ __forceinline__ V3T<F1> ld3(const float* p) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    return {{a.x}, {a.y}, {a.z}};
   }
-  static __device__ __forceinline__ Q4T<float> ldq(const float* p, int o2) {
-    float4 a = ld4(p, o2);
-    return {a.x, a.y, a.z, a.w};
+  static __device__ __forceinline__ Q4T<F1> ldq(const float* p) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    return {{a.x}, {a.y}, {a.z}, {a.w}};
   }
-  static __device__ __forceinline__ void st3(float* p, int, V3T<float> v, float w = 0.f) {
-    *reinterpret_cast<float4*>(p) = make_float4(v.x, v.y, v.z, w);
+  static __device__ __forceinline__ void st3(float* p, V3T<F1> v, F1 w = {0.f}) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.x.x, v.y.x, v.z.x, w.x);
   }
-  static __device__ __forceinline__ void stq(float* p, int, Q4T<float> q) {
-    *reinterpret_cast<float4*>(p) = make_float4(q.w, q.x, q.y, q.z);
+  static __device__ __forceinline__ void stq(float* p, Q4T<F1> q) {
+    *reinterpret_cast<float4*>(p) = make_float4(q.w.x, q.x.x, q.y.x, q.z.x);
   }
-  static __device__ __forceinline__ float ld(const float* p, int) { return *p; }
-  static __device__ __forceinline__ float w4(const float* p, int) { return p[3]; }
+  static __device__ __forceinline__ F1 ld(const float* p) { return {*p}; }  // per-env scalar arrays
+  static __device__ __forceinline__ void st(float* p, F1 v) { *p = v.x; }
+  static __device__ __forceinline__ F1 w4(const float* p) { return {p[3]}; }  // 4th word of field 0
 };
 template <> struct Lanes<F2> {
-  static __device__ __forceinline__ V3T<F2> ld3(const float* p, int o2) {
-    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + o2);
-    return {{a.x, b.x}, {a.y, b.y}, {a.z, b.z}};
+  static constexpr int V = 2, M = 8;
+  static constexpr int QS = kQS2, JS = kJS2, CS = kCS2;
+  static __device__ __forceinline__ V3T<F2> ld3(const float* p) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    return {{a.x, a.y}, {a.z, a.w}, {b.x, b.y}};
   }
-  static __device__ __forceinline__ Q4T<F2> ldq(const float* p, int o2) {
-    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + o2);
-    return {{a.x, b.x}, {a.y, b.y}, {a.z, b.z}, {a.w, b.w}};
+  static __device__ __forceinline__ Q4T<F2> ldq(const float* p) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    return {{a.x, a.y}, {a.z, a.w}, {b.x, b.y}, {b.z, b.w}};
   }
-  static __device__ __forceinline__ void st3(float* p, int o2, V3T<F2> v, F2 w = {0.f, 0.f}) {
-    *reinterpret_cast<float4*>(p) = make_float4(v.x.x, v.y.x, v.z.x, w.x);
-    *reinterpret_cast<float4*>(p + o2) = make_float4(v.x.y, v.y.y, v.z.y, w.y);
+  static __device__ __forceinline__ void st3(float* p, V3T<F2> v, F2 w = {0.f, 0.f}) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.x.x, v.x.y, v.y.x, v.y.y);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v.z.x, v.z.y, w.x, w.y);
   }
-  static __device__ __forceinline__ void stq(float* p, int o2, Q4T<F2> q) {
-    *reinterpret_cast<float4*>(p) = make_float4(q.w.x, q.x.x, q.y.x, q.z.x);
-    *reinterpret_cast<float4*>(p + o2) = make_float4(q.w.y, q.x.y, q.y.y, q.z.y);
+  static __device__ __forceinline__ void stq(float* p, Q4T<F2> q) {
+    *reinterpret_cast<float4*>(p) = make_float4(q.w.x, q.w.y, q.x.x, q.x.y);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(q.y.x, q.y.y, q.z.x, q.z.y);
   }
-  static __device__ __forceinline__ F2 ld(const float* p, int o2) { return {p[0], p[o2]}; }
-  static __device__ __forceinline__ F2 w4(const float* p, int o2) { return {p[3], p[o2 + 3]}; }
+  // per-env scalar arrays hold a lane's two envs in adjacent words
+  static __device__ __forceinline__ F2 ld(const float* p) {
+    float2 a = *reinterpret_cast<const float2*>(p);
+    return {a.x, a.y};
+  }
+  static __device__ __forceinline__ void st(float* p, F2 v) { *reinterpret_cast<float2*>(p) = make_float2(v.x, v.y); }
+  static __device__ __forceinline__ F2 w4(const float* p) {
+    float2 a = *reinterpret_cast<const float2*>(p + 6);
+    return {a.x, a.y};
+  }
 };
 
-// QP record of one (body, env) in shared memory: pos | rot | vel | ang, float4 each
+// QP record of one (body, lane) in shared memory: pos | rot | vel | ang
 template <class S> struct Row {
-  float* p;  // = sQ + (b*E + env) * kQS
-  int o2;    // second env's record (S = F2): + L·kQS words
-  __device__ __forceinline__ V3T<S> pos() const { return Lanes<S>::ld3(p, o2); }
-  __device__ __forceinline__ Q4T<S> rot() const { return Lanes<S>::ldq(p + 4, o2); }
-  __device__ __forceinline__ V3T<S> vel() const { return Lanes<S>::ld3(p + 8, o2); }
-  __device__ __forceinline__ V3T<S> ang() const { return Lanes<S>::ld3(p + 12, o2); }
-  __device__ __forceinline__ void set_pos(V3T<S> v) const { Lanes<S>::st3(p, o2, v); }
-  __device__ __forceinline__ void set_rot(Q4T<S> q) const { Lanes<S>::stq(p + 4, o2, q); }
-  __device__ __forceinline__ void set_vel(V3T<S> v) const { Lanes<S>::st3(p + 8, o2, v); }
-  __device__ __forceinline__ void set_ang(V3T<S> v) const { Lanes<S>::st3(p + 12, o2, v); }
+  float* p;  // = sQ + (b·L + lane slot) · Lanes<S>::QS
+  static constexpr int M = Lanes<S>::M;
+  __device__ __forceinline__ V3T<S> pos() const { return Lanes<S>::ld3(p); }
+  __device__ __forceinline__ Q4T<S> rot() const { return Lanes<S>::ldq(p + M); }
+  __device__ __forceinline__ V3T<S> vel() const { return Lanes<S>::ld3(p + 2 * M); }
+  __device__ __forceinline__ V3T<S> ang() const { return Lanes<S>::ld3(p + 3 * M); }
+  __device__ __forceinline__ void set_pos(V3T<S> v) const { Lanes<S>::st3(p, v); }
+  __device__ __forceinline__ void set_rot(Q4T<S> q) const { Lanes<S>::stq(p + M, q); }
+  __device__ __forceinline__ void set_vel(V3T<S> v) const { Lanes<S>::st3(p + 2 * M, v); }
+  __device__ __forceinline__ void set_ang(V3T<S> v) const { Lanes<S>::st3(p + 3 * M, v); }
 };
 
 // ---- S2: kinematic integrator (R3, R21) -------------------------
 template <class S> __device__ __forceinline__ void kinematic(const DBody& bd, Row<S> r, float h) {
   V3T<S> v = r.vel();
   if (!(bd.flags & kFlagFreePos)) v = had(bd.mpos, v);
-  r.set_pos(r.pos() + scale(h, v));
+  r.set_pos(axpy(h, v, r.pos()));
   if (!bd.rot_frozen) {
     V3T<S> w = r.ang();
     if (!(bd.flags & kFlagFreeRot)) w = had(bd.mrot, w);
@@ -220,11 +330,10 @@ template <class S> __device__ __forceinline__ void kinematic(const DBody& bd, Ro
 }
 
 // ---- S3 + S4: joint spring/limits with its actuator (R5, R7-R12)
-// act: this env's column of the block's actions sA[k][env] (row stride E, second env + L).
-// out: this (joint, env) record: F on child | T child | T parent.
+// act: this lane's column of the block's actions sA[k][slot] (row stride E).
+// out: this (joint, lane) record: F on child | T child | T parent.
 template <class S>
-__device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, const float* act, int E, int L,
-                                      float* out, int o2) {
+__device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, const float* act, int E, float* out) {
   // the parameter record, read with LDS.128 (struct fields at fixed float4 slots)
   const float4* J4 = reinterpret_cast<const float4*>(&Jm);
   const int4 h0 = *reinterpret_cast<const int4*>(&Jm), h1 = reinterpret_cast<const int4*>(&Jm)[1];
@@ -238,7 +347,7 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
   V3T<S> wp = P.ang(), wc = C.ang();
   V3T<S> f = scale(op_k.w, dx);
   if (!(flags & kJNoCl))
-    f = f + scale(oc_cl.w, cross_add(wp, rp, P.vel()) - cross_add(wc, rc, C.vel()));
+    f = axpy(oc_cl.w, cross_add(wp, rp, P.vel()) - cross_add(wc, rc, C.vel()), f);
   Q4T<S> fp = qmul(qp, Q4T<S>{bc<S>(jp.x), bc<S>(jp.y), bc<S>(jp.z), bc<S>(jp.w)});
   Q4T<S> fc = qmul(qc, Q4T<S>{bc<S>(jc.x), bc<S>(jc.y), bc<S>(jc.z), bc<S>(jc.w)});
   Q4T<S> qr = qmul(qconj(fp), fc);
@@ -260,7 +369,7 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       if (i < dof) {
-        S a = Lanes<S>::ld(act + (act_offset + i) * E, L);
+        S a = Lanes<S>::ld(act + (act_offset + i) * E);
         tau[i] = tau[i] + ((act_kind == 0) ? ca_s.y * clampv(a, -1.f, 1.f)
                                            : ca_s.y * (clampv(a, lo[i], hi[i]) - th[i]));
       }
@@ -276,12 +385,13 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
   S u = (tau[2] - tau[0] * R02) * vmin(ic * ic, bc<S>(100.f));
   V3T<S> tj{tau[0], u * R12 + t1 * R22, u * R22 - t1 * R12};
   V3T<S> twd = rotate(fp, tj);
-  if (!(flags & kJNoCa)) twd = twd + scale(ca_s.x, wp - wc);
+  if (!(flags & kJNoCa)) twd = axpy(ca_s.x, wp - wc, twd);
   V3T<S> tc = cross_add(rc, f, twd);
   V3T<S> tp = cross_add(rp, f, twd);
-  Lanes<S>::st3(out, o2, f);
-  Lanes<S>::st3(out + 4, o2, tc);
-  Lanes<S>::st3(out + 8, o2, V3T<S>{-tp.x, -tp.y, -tp.z});
+  constexpr int M = Lanes<S>::M;
+  Lanes<S>::st3(out, f);
+  Lanes<S>::st3(out + M, tc);
+  Lanes<S>::st3(out + 2 * M, V3T<S>{-tp.x, -tp.y, -tp.z});
 }
 
 // Closest points between segments (Ericson, Real-Time Collision Detection §5.1.9),
@@ -312,15 +422,15 @@ __device__ __forceinline__ void seg_seg(V3T<S> p1, V3T<S> q1, V3T<S> p2, V3T<S> 
       t = sel(tl, zero, sel(th, bc<S>(1.f), t));
     }
   }
-  c1 = p1 + s * d1;
-  c2 = p2 + t * d2;
+  c1 = axpy(s, d1, p1);
+  c2 = axpy(t, d2, p2);
 }
 
 // ---- S5: contact slot, velocity-level impulse + Baumgarte (R13-R19)
-// out: this (slot, env) record: P, active | r_A×P | r_B×P; cnt: substeps active.
+// out: this (slot, lane) record: P, active | r_A×P | r_B×P; cnt: substeps active.
 template <class S>
 __device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, float opl_e, float beta_over_h,
-                                        float mu, float* out, int o2, S& cnt) {
+                                        float mu, float* out, S& cnt) {
   // the parameter record, read with LDS.128 at its fixed float4 slots
   const float4* S4 = reinterpret_cast<const float4*>(&SLm);
   const int4 h0 = *reinterpret_cast<const int4*>(&SLm), h1 = reinterpret_cast<const int4*>(&SLm)[1];
@@ -351,21 +461,21 @@ __device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, fl
       d = -dot(c - cB, n);
       pt = c;
     } else {
-      V3T<S> c = (type == 1) ? cA + scale(ells.x, rotate_z(qA)) : cA;
+      V3T<S> c = (type == 1) ? axpy(ells.x, rotate_z(qA), cA) : cA;
       d = ra - dot(c - cB, n);
-      pt = c - scale(ra, n);
+      pt = axpy(-ra, n, c);
     }
   } else {
     V3T<S> pa = cA, pb = cB;
     if (type == 4) {  // sphere (A) – capsule (B)
       V3T<S> axb = rotate_z(qB);
-      V3T<S> e0 = cB + scale(ells.y, axb), e1 = cB - scale(ells.y, axb);
+      V3T<S> e0 = axpy(ells.y, axb, cB), e1 = axpy(-ells.y, axb, cB);
       V3T<S> seg = e0 - e1;
       if (ells.y > 0.f) pb = e1 + clampv(vdiv(dot(cA - e1, seg), dot(seg, seg)), 0.f, 1.f) * seg;
       else pb = e1;
     } else if (type == 5) {  // capsule – capsule
       V3T<S> axa = rotate_z(qA), axb = rotate_z(qB);
-      seg_seg(cA + scale(ells.x, axa), cA - scale(ells.x, axa), cB + scale(ells.y, axb), cB - scale(ells.y, axb),
+      seg_seg(axpy(ells.x, axa, cA), axpy(-ells.x, axa, cA), axpy(ells.y, axb, cB), axpy(-ells.y, axb, cB),
               !(ells.x > 0.f), !(ells.y > 0.f), pa, pb);
     }
     V3T<S> delta = pa - pb;
@@ -376,7 +486,7 @@ __device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, fl
     V3T<S> zhat{zero, zero, bc<S>(1.f)};
     n = sel3<S>(nz, idist * delta, zhat);  // R16: ẑ when the centres coincide
     d = (ra + rb) - dist;
-    pt = scale(0.5f, (pa - scale(ra, n)) + (pb + scale(rb, n)));
+    pt = scale(0.5f, axpy(-ra, n, pa) + axpy(rb, n, pb));
   }
   auto pen = gt(d, zero);  // R16: strict d > 0
   V3T<S> P{zero, zero, zero}, ta{zero, zero, zero}, tb{zero, zero, zero};
@@ -418,39 +528,36 @@ __device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, fl
       active = as_count(act);
     }
   }
-  Lanes<S>::st3(out, o2, P, active);
-  Lanes<S>::st3(out + 4, o2, ta);
-  Lanes<S>::st3(out + 8, o2, tb);
+  constexpr int M = Lanes<S>::M;
+  Lanes<S>::st3(out, P, active);
+  Lanes<S>::st3(out + M, ta);
+  Lanes<S>::st3(out + 2 * M, tb);
   cnt = cnt + active;
 }
 
-__device__ __forceinline__ void store_count(float* p, int, float c) { *p = c; }
-__device__ __forceinline__ void store_count(float* p, int o2, F2 c) {
-  p[0] = c.x;
-  p[o2] = c.y;
-}
 
 // ---- S6: per-body accumulation over the static incidence lists (fixed order) --
 // e = (item << 4) | t with t = 4 (child / A side: sign +1) or 8 (parent / B side:
-// sign −1); rec: this env's record of the item; the torque vector sits at word t.
+// sign −1); rec: this lane's record of the item; the torque vector is field t/4.
 template <class S> struct Acc {
   V3T<S> F, T, dV, dW;
   S cnt;
+  static constexpr int M = Lanes<S>::M;
   __device__ __forceinline__ Acc() {
     const S z = bc<S>(0.f);
     F = T = dV = dW = V3T<S>{z, z, z};
     cnt = z;
   }
-  __device__ __forceinline__ void joint(const float* rec, int o2, int e) {
+  __device__ __forceinline__ void joint(const float* rec, int e) {
     const float sg = (e & 8) ? -1.f : 1.f;
-    F = F + scale(sg, Lanes<S>::ld3(rec, o2));
-    T = T + Lanes<S>::ld3(rec + (e & 15), o2);
+    F = axpy(sg, Lanes<S>::ld3(rec), F);
+    T = T + Lanes<S>::ld3(rec + (e & 15) * (M / 4));
   }
-  __device__ __forceinline__ void slot(const float* rec, int o2, int e) {
+  __device__ __forceinline__ void slot(const float* rec, int e) {
     const float sg = (e & 8) ? -1.f : 1.f;
-    dV = dV + scale(sg, Lanes<S>::ld3(rec, o2));
-    dW = dW + scale(sg, Lanes<S>::ld3(rec + (e & 15), o2));
-    cnt = cnt + Lanes<S>::w4(rec, o2);
+    dV = axpy(sg, Lanes<S>::ld3(rec), dV);
+    dW = axpy(sg, Lanes<S>::ld3(rec + (e & 15) * (M / 4)), dW);
+    cnt = cnt + Lanes<S>::w4(rec);
   }
 };
 
@@ -461,22 +568,23 @@ template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Ro
                                                              const float* g, bool kin) {
   const bool iso = bd.flags & kFlagIso, fp = bd.flags & kFlagFreePos, fr = bd.flags & kFlagFreeRot;
   Q4T<S> q = r.rot();
-  V3T<S> v = r.vel() + scale(h, scale(bd.inv_mass, acc.F) + bc3<S>(g));
-  V3T<S> w = r.ang() + scale(h, iw(q, bd.inv_inertia, iso, acc.T));
+  V3T<S> v = axpy(h, axpy(bd.inv_mass, acc.F, bc3<S>(g)), r.vel());
+  V3T<S> w = axpy(h, iw(q, bd.inv_inertia, iso, acc.T), r.ang());
   if (!fp) v = had(bd.mpos, v);
   if (!fr) w = had(bd.mrot, w);
   auto hit = gt(acc.cnt, bc<S>(0.f));
   if (any(hit)) {
     S ic = sel(hit, vdiv(bc<S>(1.f), acc.cnt), bc<S>(0.f));  // R14: mean over the body's active contacts
-    v = v + (bd.inv_mass * ic) * acc.dV;
-    w = w + ic * iw(q, bd.inv_inertia, iso, acc.dW);
+    const S mic = bd.inv_mass * ic;
+    v = axpy(mic, acc.dV, v);
+    w = axpy(ic, iw(q, bd.inv_inertia, iso, acc.dW), w);
     if (!fp) v = had(bd.mpos, v);
     if (!fr) w = had(bd.mrot, w);
   }
   r.set_vel(v);
   r.set_ang(w);
   if (kin) {  // next substep's kinematic integrator (v, ω already masked)
-    r.set_pos(r.pos() + scale(h, v));
+    r.set_pos(axpy(h, v, r.pos()));
     if (!bd.rot_frozen) {
       Q4T<S> dq = qmul(Q4T<S>{bc<S>(0.f), w.x, w.y, w.z}, q);
       const float hh = 0.5f * h;
@@ -489,19 +597,33 @@ template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Ro
   }
 }
 
-// ---- S1 / S9: staging of one QP field [n][B][K] <-> sQ record words foff..foff+K-1.
+// Word of (body b, env slot env, field f, component c) in the QP records (V envs per lane).
+template <int V> __device__ __forceinline__ int qword(int b, int env, int f, int c, int E) {
+  if (V == 1) return (b * E + env) * kQS + 4 * f + c;
+  const int LG = E >> 1, h = env >= LG ? 1 : 0, el = env - h * LG;
+  return (b * LG + el) * kQS2 + 8 * f + 4 * (c >> 1) + 2 * (c & 1) + h;
+}
+// Position of env slot `env` in a per-env row of E words (actions, contact counts):
+// V = 2 keeps a lane's two envs (el, el + E/2) adjacent.
+template <int V> __device__ __forceinline__ int eslot(int env, int E) {
+  if (V == 1) return env;
+  const int LG = E >> 1, h = env >= LG ? 1 : 0;
+  return 2 * (env - h * LG) + h;
+}
+
+// ---- S1 / S9: staging of one QP field [n][B][K] <-> record field f.
 // One env row (B·K contiguous floats) per warp iteration, lanes along the row:
 // coalesced, and no integer division (K is a compile-time constant).
-template <int K, bool kLoad>
-__device__ __forceinline__ void stage(const float* gin, float* gout, float* sQ, int foff, int64_t e0, int nvalid,
-                                      int B, int E) {
+template <int K, bool kLoad, int V>
+__device__ __forceinline__ void stage(const float* gin, float* gout, float* sQ, int f, int64_t e0, int nvalid, int B,
+                                      int E) {
   const int row_len = B * K;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int env = warp; env < nvalid; env += nw) {
     const int64_t g0 = (e0 + env) * row_len;
     for (int k = lane; k < row_len; k += 32) {
       const int b = k / K, c = k - (k / K) * K;
-      float* s = sQ + (b * E + env) * kQS + foff + c;
+      float* s = sQ + qword<V>(b, env, f, c, E);
       if (kLoad) *s = __ldg(gin + g0 + k);
       else gout[g0 + k] = *s;
     }
@@ -547,96 +669,157 @@ __device__ __forceinline__ void tma_store_commit_wait() {
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Staging area layout (words): the block's contiguous global chunks
-// pos [E][B][3] | rot [E][B][4] | vel [E][B][3] | ang [E][B][3].
-__device__ __forceinline__ void stg_to_records(const float* stg, float* sQ, int B, int E, int nvalid) {
+// pos [E][B][3] | rot [E][B][4] | vel [E][B][3] | ang [E][B][3].  Full blocks only.
+template <int V> __device__ __forceinline__ void stg_to_records(const float* stg, float* sQ, int B, int E) {
   const float* sp = stg;
   const float* sr = stg + E * B * 3;
   const float* sv = sr + E * B * 4;
   const float* sw = sv + E * B * 3;
-  for (int i = threadIdx.x; i < nvalid * B; i += blockDim.x) {
-    const int env = i / B, b = i - env * B;
-    float4* r = reinterpret_cast<float4*>(sQ + (b * E + env) * kQS);
-    r[0] = make_float4(sp[3 * i], sp[3 * i + 1], sp[3 * i + 2], 0.f);
-    r[1] = make_float4(sr[4 * i], sr[4 * i + 1], sr[4 * i + 2], sr[4 * i + 3]);
-    r[2] = make_float4(sv[3 * i], sv[3 * i + 1], sv[3 * i + 2], 0.f);
-    r[3] = make_float4(sw[3 * i], sw[3 * i + 1], sw[3 * i + 2], 0.f);
+  if (V == 1) {
+    for (int i = threadIdx.x; i < E * B; i += blockDim.x) {
+      const int env = i / B, b = i - env * B;
+      float4* r = reinterpret_cast<float4*>(sQ + (b * E + env) * kQS);
+      r[0] = make_float4(sp[3 * i], sp[3 * i + 1], sp[3 * i + 2], 0.f);
+      r[1] = make_float4(sr[4 * i], sr[4 * i + 1], sr[4 * i + 2], sr[4 * i + 3]);
+      r[2] = make_float4(sv[3 * i], sv[3 * i + 1], sv[3 * i + 2], 0.f);
+      r[3] = make_float4(sw[3 * i], sw[3 * i + 1], sw[3 * i + 2], 0.f);
+    }
+  } else {
+    const int LG = E >> 1;
+    for (int i = threadIdx.x; i < LG * B; i += blockDim.x) {
+      const int el = i / B, b = i - el * B;
+      const int i0 = i, i1 = i + LG * B;  // staging rows of envs el and el + LG
+      float4* r = reinterpret_cast<float4*>(sQ + (b * LG + el) * kQS2);
+      r[0] = make_float4(sp[3 * i0], sp[3 * i1], sp[3 * i0 + 1], sp[3 * i1 + 1]);
+      r[1] = make_float4(sp[3 * i0 + 2], sp[3 * i1 + 2], 0.f, 0.f);
+      r[2] = make_float4(sr[4 * i0], sr[4 * i1], sr[4 * i0 + 1], sr[4 * i1 + 1]);
+      r[3] = make_float4(sr[4 * i0 + 2], sr[4 * i1 + 2], sr[4 * i0 + 3], sr[4 * i1 + 3]);
+      r[4] = make_float4(sv[3 * i0], sv[3 * i1], sv[3 * i0 + 1], sv[3 * i1 + 1]);
+      r[5] = make_float4(sv[3 * i0 + 2], sv[3 * i1 + 2], 0.f, 0.f);
+      r[6] = make_float4(sw[3 * i0], sw[3 * i1], sw[3 * i0 + 1], sw[3 * i1 + 1]);
+      r[7] = make_float4(sw[3 * i0 + 2], sw[3 * i1 + 2], 0.f, 0.f);
+    }
   }
 }
-__device__ __forceinline__ void records_to_stg(const float* sQ, float* stg, int B, int E, int nvalid) {
+template <int V> __device__ __forceinline__ void records_to_stg(const float* sQ, float* stg, int B, int E) {
   float* sp = stg;
   float* sr = stg + E * B * 3;
   float* sv = sr + E * B * 4;
   float* sw = sv + E * B * 3;
-  for (int i = threadIdx.x; i < nvalid * B; i += blockDim.x) {
-    const int env = i / B, b = i - env * B;
-    const float4* r = reinterpret_cast<const float4*>(sQ + (b * E + env) * kQS);
-    float4 p = r[0], q = r[1], v = r[2], w = r[3];
-    sp[3 * i] = p.x; sp[3 * i + 1] = p.y; sp[3 * i + 2] = p.z;
-    sr[4 * i] = q.x; sr[4 * i + 1] = q.y; sr[4 * i + 2] = q.z; sr[4 * i + 3] = q.w;
-    sv[3 * i] = v.x; sv[3 * i + 1] = v.y; sv[3 * i + 2] = v.z;
-    sw[3 * i] = w.x; sw[3 * i + 1] = w.y; sw[3 * i + 2] = w.z;
+  if (V == 1) {
+    for (int i = threadIdx.x; i < E * B; i += blockDim.x) {
+      const int env = i / B, b = i - env * B;
+      const float4* r = reinterpret_cast<const float4*>(sQ + (b * E + env) * kQS);
+      float4 p = r[0], q = r[1], v = r[2], w = r[3];
+      sp[3 * i] = p.x; sp[3 * i + 1] = p.y; sp[3 * i + 2] = p.z;
+      sr[4 * i] = q.x; sr[4 * i + 1] = q.y; sr[4 * i + 2] = q.z; sr[4 * i + 3] = q.w;
+      sv[3 * i] = v.x; sv[3 * i + 1] = v.y; sv[3 * i + 2] = v.z;
+      sw[3 * i] = w.x; sw[3 * i + 1] = w.y; sw[3 * i + 2] = w.z;
+    }
+  } else {
+    const int LG = E >> 1;
+    for (int i = threadIdx.x; i < LG * B; i += blockDim.x) {
+      const int el = i / B, b = i - el * B;
+      const int i0 = i, i1 = i + LG * B;
+      const float4* r = reinterpret_cast<const float4*>(sQ + (b * LG + el) * kQS2);
+      float4 p0 = r[0], p1 = r[1], q0 = r[2], q1 = r[3], v0 = r[4], v1 = r[5], w0 = r[6], w1 = r[7];
+      sp[3 * i0] = p0.x; sp[3 * i0 + 1] = p0.z; sp[3 * i0 + 2] = p1.x;
+      sp[3 * i1] = p0.y; sp[3 * i1 + 1] = p0.w; sp[3 * i1 + 2] = p1.y;
+      sr[4 * i0] = q0.x; sr[4 * i0 + 1] = q0.z; sr[4 * i0 + 2] = q1.x; sr[4 * i0 + 3] = q1.z;
+      sr[4 * i1] = q0.y; sr[4 * i1 + 1] = q0.w; sr[4 * i1 + 2] = q1.y; sr[4 * i1 + 3] = q1.w;
+      sv[3 * i0] = v0.x; sv[3 * i0 + 1] = v0.z; sv[3 * i0 + 2] = v1.x;
+      sv[3 * i1] = v0.y; sv[3 * i1 + 1] = v0.w; sv[3 * i1 + 2] = v1.y;
+      sw[3 * i0] = w0.x; sw[3 * i0 + 1] = w0.z; sw[3 * i0 + 2] = w1.x;
+      sw[3 * i1] = w0.y; sw[3 * i1 + 1] = w0.w; sw[3 * i1 + 2] = w1.y;
+    }
   }
 }
 
 // S1: the block's E envs' QP -> shared memory (env slots past the batch end get identity state)
-__device__ __forceinline__ void load_block(const StepArgs& a, float* sQ, uint32_t* sStat, int B, int E, int64_t e0,
-                                           int nvalid) {
+template <int V>
+__device__ __forceinline__ void load_block(const StepArgs& a, float* sQ, int B, int E, int64_t e0, int nvalid) {
   if (nvalid < E) {
-    for (int i = threadIdx.x; i < B * E; i += blockDim.x) {
-      float4* p = reinterpret_cast<float4*>(sQ + i * kQS);
-      p[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-      p[1] = make_float4(1.f, 0.f, 0.f, 0.f);
-      p[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-      p[3] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nrec = B * (E / V), RS = V == 2 ? kQS2 : kQS;
+    for (int i = threadIdx.x; i < nrec; i += blockDim.x) {
+      float4* p = reinterpret_cast<float4*>(sQ + i * RS);
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (V == 1) {
+        p[0] = z; p[1] = make_float4(1.f, 0.f, 0.f, 0.f); p[2] = z; p[3] = z;
+      } else {
+        p[0] = z; p[1] = z; p[2] = make_float4(1.f, 1.f, 0.f, 0.f); p[3] = z;
+        p[4] = z; p[5] = z; p[6] = z; p[7] = z;
+      }
     }
     __syncthreads();
   }
-  stage<3, true>(a.pos_in, nullptr, sQ, 0, e0, nvalid, B, E);
-  stage<4, true>(a.rot_in, nullptr, sQ, 4, e0, nvalid, B, E);
-  stage<3, true>(a.vel_in, nullptr, sQ, 8, e0, nvalid, B, E);
-  stage<3, true>(a.ang_in, nullptr, sQ, 12, e0, nvalid, B, E);
+  stage<3, true, V>(a.pos_in, nullptr, sQ, 0, e0, nvalid, B, E);
+  stage<4, true, V>(a.rot_in, nullptr, sQ, 1, e0, nvalid, B, E);
+  stage<3, true, V>(a.vel_in, nullptr, sQ, 2, e0, nvalid, B, E);
+  stage<3, true, V>(a.ang_in, nullptr, sQ, 3, e0, nvalid, B, E);
 }
 
-// S1 (per step): this step's action [n][A] -> sA[k][env] (one env row per warp iteration)
+// S1 (per step): this step's action [n][A] -> sA[k][eslot(env)] (one env row per warp iteration)
+template <int V>
 __device__ __forceinline__ void load_actions(const StepArgs& a, float* sA, int A, int E, int64_t step, int64_t e0,
                                              int nvalid) {
   if (A <= 0) return;
   const float* act = a.actions + (step * a.n_envs + e0) * A;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int env = warp; env < nvalid; env += nw)
-    for (int k = lane; k < A; k += 32) sA[k * E + env] = __ldg(act + env * A + k);
+  for (int env = warp; env < nvalid; env += nw) {
+    const int slot = eslot<V>(env, E);
+    for (int k = lane; k < A; k += 32) sA[k * E + slot] = __ldg(act + env * A + k);
+  }
 }
 
 // S9: status bits and contact counts (after a barrier)
+template <int V>
 __device__ __forceinline__ void block_extras(const StepArgs& a, const float* sQ, const float* sCnt, uint32_t* sStat,
                                              int B, int C, int E, int64_t e0, int nvalid) {
+  auto word_bits = [](float v) -> uint32_t { return isfinite(v) ? (fabsf(v) > 1e6f ? 2u : 0u) : 1u; };
   if (a.status) {
-    for (int i = threadIdx.x; i < B * E; i += blockDim.x) {
-      const float* p = sQ + i * kQS;
-      uint32_t bits = 0;
+    if (V == 1) {
+      for (int i = threadIdx.x; i < B * E; i += blockDim.x) {
+        const float* p = sQ + i * kQS;
+        uint32_t bits = 0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (k == 3 || k == 11 || k == 15) continue;  // padding words
-        float v = p[k];
-        bits |= isfinite(v) ? (fabsf(v) > 1e6f ? 2u : 0u) : 1u;
+        for (int k = 0; k < 16; ++k) {
+          if (k == 3 || k == 11 || k == 15) continue;  // padding words
+          bits |= word_bits(p[k]);
+        }
+        if (bits) atomicOr(&sStat[i % E], bits);
       }
-      if (bits) atomicOr(&sStat[i % E], bits);
+    } else {
+      const int LG = E >> 1;
+      for (int i = threadIdx.x; i < B * LG; i += blockDim.x) {
+        const float* p = sQ + i * kQS2;
+        uint32_t bits0 = 0, bits1 = 0;
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          if (k == 6 || k == 22 || k == 30) continue;  // padding words (pos, vel, ang 4th component)
+          bits0 |= word_bits(p[k]);
+          bits1 |= word_bits(p[k + 1]);
+        }
+        const int el = i % LG;
+        if (bits0) atomicOr(&sStat[el], bits0);
+        if (bits1) atomicOr(&sStat[el + LG], bits1);
+      }
     }
   }
   if (a.contact_active) {
     for (int i = threadIdx.x; i < nvalid * C; i += blockDim.x) {
       int env = i / C, c = i - env * C;
-      a.contact_active[(e0 + env) * C + c] = uint8_t(sCnt[c * E + env]);
+      a.contact_active[(e0 + env) * C + c] = uint8_t(sCnt[c * E + eslot<V>(env, E)]);
     }
   }
 }
 
 // S9 fallback (ragged tail / unaligned): per-row stores of the QP
-__device__ __forceinline__ void store_block(const StepArgs& a, float* sQ, int B, int E, int64_t e0, int nvalid) {
-  stage<3, false>(nullptr, a.pos_out, sQ, 0, e0, nvalid, B, E);
-  stage<4, false>(nullptr, a.rot_out, sQ, 4, e0, nvalid, B, E);
-  stage<3, false>(nullptr, a.vel_out, sQ, 8, e0, nvalid, B, E);
-  stage<3, false>(nullptr, a.ang_out, sQ, 12, e0, nvalid, B, E);
+template <int V> __device__ __forceinline__ void store_block(const StepArgs& a, float* sQ, int B, int E, int64_t e0,
+                                                             int nvalid) {
+  stage<3, false, V>(nullptr, a.pos_out, sQ, 0, e0, nvalid, B, E);
+  stage<4, false, V>(nullptr, a.rot_out, sQ, 1, e0, nvalid, B, E);
+  stage<3, false, V>(nullptr, a.vel_out, sQ, 2, e0, nvalid, B, E);
+  stage<3, false, V>(nullptr, a.ang_out, sQ, 3, e0, nvalid, B, E);
 }
 
 }  // namespace dev

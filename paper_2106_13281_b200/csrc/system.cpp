@@ -373,7 +373,7 @@ System* build_host(const Config& cfg) {
 
   for (int pi = 0; pi < kNumPlans; ++pi) {
     DPlan& P = hd.plan[pi];
-    P.smem_bytes = smem_layout(B, J, C, hd.A, P.E, hd.blob_words).total_words * 4;
+    P.smem_bytes = smem_layout(B, J, C, hd.A, P.E, P.V, hd.blob_words).total_words * 4;
   }
   s->smem_bytes = size_t(hd.plan[0].smem_bytes);
   if (size_t(hd.plan[0].smem_bytes) > 227 * 1024)

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -10,6 +12,12 @@
 #include "device_tables.h"
 
 namespace brax {
+
+struct LaunchConfig {
+  int plan = 0;     // index into DHeader::plan
+  int regs = 0;     // register budget variant
+  bool tuned = false;
+};
 
 struct System {
   Config cfg;
@@ -27,6 +35,11 @@ struct System {
   bool trace = false;                  // per-phase cycle tracing (brax_system_set_tracing)
   unsigned long long* d_phase_cycles = nullptr;  // device [4]
   size_t smem_bytes = 0;
+  // launch configuration per batch size, measured on the first uncaptured launch
+  // (every plan gives the same bits, so the choice only affects speed)
+  bool autotune = true;
+  mutable std::mutex tune_mu;
+  mutable std::map<int64_t, LaunchConfig> tuned;
   ~System();
 };
 
@@ -39,8 +52,10 @@ System* build_system(const Config& cfg, int device);
 void default_qp(const Config& cfg, std::vector<double>& pos, std::vector<double>& rot);
 
 
-// Lane-group plan index chosen for a launch of n_envs envs (step.cu).
+// Lane-group plan index chosen by the size heuristic for n_envs envs (step.cu).
 int choose_plan(const System& sys, int64_t n_envs);
+// The configuration the next launch of n_envs envs uses (tuned, overridden or heuristic).
+LaunchConfig launch_config(const System& sys, int64_t n_envs);
 
 // Kernel launchers (step.cu, reset.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream);

@@ -261,7 +261,8 @@ def test_slot_table_and_default_qp_on_device_system():
 @pytest.mark.parametrize("name", ["ant", "humanoid", "grasp", "coverage"])
 def test_every_launch_plan_matches_oracle(name):
     """The launch heuristics pick the lane-group count G, envs per lane V and the
-    register budget per call; every combination must give the oracle's answer."""
+    register budget per call; every combination must give the oracle's answer, and
+    the same bits (an env's result does not depend on the batch size)."""
     import os
     o, s = scene(name)
     n = 333
@@ -275,6 +276,10 @@ def test_every_launch_plan_matches_oracle(name):
                 os.environ["BRAX_PLAN"] = plan
                 os.environ["BRAX_MAXREG"] = regs
                 got, status, ca = gpu_step(s, qp, act)
+                if plan == "1,1" and regs == "56":
+                    first = got
+                for k in FIELDS:
+                    assert np.array_equal(got[k], first[k]), (plan, regs, k)
                 err, errs = max_err(got, ref, keep)
                 assert err <= TOL_STEP, (plan, regs, errs)
                 assert np.array_equal(ca[keep], ex["contact_active"][keep]), (plan, regs)
@@ -282,3 +287,30 @@ def test_every_launch_plan_matches_oracle(name):
     finally:
         os.environ.pop("BRAX_PLAN", None)
         os.environ.pop("BRAX_MAXREG", None)
+
+
+def test_autotune_picks_a_plan_without_touching_inputs():
+    """The first launch of a batch size times every plan on a scratch copy (the
+    caller's input is not written), remembers the fastest, and the result equals
+    the heuristic plan's bit for bit."""
+    o, s0 = scene("ant")
+    s = bx.System(oracle.load_scene("ant"))
+    n = 1000
+    qp = trajectory_states(o, n, seed=51, T0=2)
+    act = synth.actions(52, 1, n, o.act_dim)[0]
+    assert s.launch_config(n)["tuned"] == 0
+    qd = dev(qp)
+    before = host(qd)
+    out = s.alloc_qp(n)
+    s.step(qd, torch.from_numpy(act).cuda(), out)
+    torch.cuda.synchronize()
+    for k in FIELDS:
+        assert np.array_equal(host(qd)[k], before[k])
+    cfg = s.launch_config(n)
+    assert cfg["tuned"] == 1 and cfg["E"] == 32 * cfg["V"] // cfg["G"], cfg
+    s0.set_autotune(False)
+    ref, _, _ = gpu_step(s0, qp, act)
+    s0.set_autotune(True)
+    got = host(out)
+    for k in FIELDS:
+        assert np.array_equal(got[k], ref[k]), k

@@ -71,6 +71,6 @@ for scene in a.scenes.split(","):
             ms = e0.elapsed_time(e1)
             rate = n * T / (ms / 1e3)
             tf = rate * counts[scene]["flops_per_env_step"] / 1e12
-            print(json.dumps({"scene": scene, "substeps": s.substeps, "envs": n, "G": G, "warps": s.info.warps_per_block, "rollout": a.rollout,
+            print(json.dumps({"scene": scene, "substeps": s.substeps, "envs": n, "G": G, "cfg": s.launch_config(n), "rollout": a.rollout,
                               "us_per_step": 1e3 * ms / T, "env_steps_per_s": rate, "tflops": tf,
                               "frac_fp32_1965": tf / 74.45}), flush=True)
