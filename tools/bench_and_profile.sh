@@ -9,6 +9,10 @@ timeout 600 python bench.py --impl reference --steps 200 --warmup 3 > gpurun_out
 CMD="python bench.py --steps 50 --warmup 3 --no-cpu-baseline --e2e-steps 2"
 $CMD > gpurun_out/bench_small_${TAG}.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch_${TAG}.log 2>&1
+# full capture of the launch configuration the bench's autotuner chose
+PLAN=$(python -c "import json; c=json.load(open('gpurun_out/bench_${TAG}.json'))['config']['kernel_config']; print(f\"{c['G']},{c['V']}\")" 2>/dev/null || echo "1,1")
+export BRAX_PLAN=$PLAN
 python tools/profile_step.py > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:brax_step -s 3 -c 1 -o gpurun_out/prof_${TAG}_ant python tools/profile_step.py > gpurun_out/ncu_full_${TAG}.log 2>&1
-echo done
+unset BRAX_PLAN
+echo "done (full capture plan $PLAN)"
