@@ -90,7 +90,7 @@ def _load():
             lib = C.CDLL(build())
             dp = C.POINTER(C.c_double)
             lib.oracle_step.argtypes = [C.POINTER(_OSys), C.POINTER(_OOpts), C.c_int64, C.c_int64, dp, dp, dp, dp,
-                                        dp, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint8)]
+                                        dp, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), dp]
             lib.oracle_step.restype = C.c_int
             lib.oracle_step_f32.argtypes = lib.oracle_step.argtypes
             lib.oracle_step_f32.restype = C.c_int
@@ -188,12 +188,14 @@ class Oracle:
         d = self.default_qp()
         return {k: np.broadcast_to(v, (n,) + v.shape).copy() for k, v in d.items()}
 
-    def step(self, qp, action=None, *, threads: int = 1, fp32: bool = False):
+    def step(self, qp, action=None, *, threads: int = 1, fp32: bool = False, contact_dv: bool = False):
         """One Brax step (substeps × Alg. 1) on a batch; returns (qp_out, extras).
 
         qp: dict of arrays pos [n,B,3], rot [n,B,4], vel [n,B,3], ang [n,B,3]
         (any float dtype; promoted to fp64).  action: [n, act_dim] or None.
-        extras: contact_active [n,C] u8, status [n] u32, ambiguous [n] bool.
+        extras: contact_active [n,C] u8, status [n] u32, ambiguous [n] bool, and with
+        contact_dv=True "contact_dv" [n,B,6]: the last substep's collision-integrator
+        velocity change (Δv, Δω) per body.
         fp32=True runs the same code in fp32 arithmetic: a diagnostic of the fp32
         rounding floor of the method, never a parity reference."""
         lib = _load()
@@ -211,6 +213,7 @@ class Oracle:
         amb = np.zeros(n, dtype=np.uint8)
         dp = C.POINTER(C.c_double)
         ca_ptr = ca.ctypes.data_as(C.POINTER(C.c_uint8)) if self.n_slots else None
+        cdv = np.zeros((n, B, 6)) if contact_dv else None
 
         def run(e0, e1):
             fn = lib.oracle_step_f32 if fp32 else lib.oracle_step
@@ -219,7 +222,8 @@ class Oracle:
                                  out["vel"].ctypes.data_as(dp), out["ang"].ctypes.data_as(dp),
                                  act.ctypes.data_as(dp), ca_ptr,
                                  status.ctypes.data_as(C.POINTER(C.c_uint32)),
-                                 amb.ctypes.data_as(C.POINTER(C.c_uint8)))
+                                 amb.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                 cdv.ctypes.data_as(dp) if cdv is not None else None)
             assert rc == 0
 
         if threads <= 1 or n < 2 * threads:
@@ -232,7 +236,10 @@ class Oracle:
                 th.start()
             for th in ths:
                 th.join()
-        return out, {"contact_active": ca, "status": status, "ambiguous": amb.astype(bool)}
+        ex = {"contact_active": ca, "status": status, "ambiguous": amb.astype(bool)}
+        if cdv is not None:
+            ex["contact_dv"] = cdv
+        return out, ex
 
     def rollout(self, qp, actions, *, threads: int = 1):
         """Apply step T times; actions [T, n, A] (or None).  Returns the final qp and

@@ -258,7 +258,11 @@ void narrowphase(const OSys& S, const OSlot& sl, const BodyState<T>* st, double 
 }
 
 template <class T>
-struct EnvOut { uint8_t* active; bool ambiguous; };
+struct EnvOut {
+  uint8_t* active;
+  bool ambiguous;
+  double* contact_dv;  // [B][6] or NULL: the collision integrator's Δv, Δω of this substep (NEXT-1 obs)
+};
 
 // One substep of Alg. 1 on one env.  `st` holds all B bodies.
 template <class T>
@@ -419,19 +423,28 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
   }
   // ---- 6. collision integrator (R14 mean over active contacts) -
   for (int b = 0; b < B; ++b) {
+    if (out->contact_dv)
+      for (int k = 0; k < 6; ++k) out->contact_dv[6 * b + k] = 0.0;
     const OBody& bd = S.bodies[b];
     if (bd.is_static || cnt[b] == 0) continue;
     BodyState<T>& s = st[b];
+    const V3<T> v0 = s.v, w0 = s.w;
     T scale = opt.combine_sum ? T(1.0) : T(1.0) / T(double(cnt[b]));
     s.v = hadamard(V<T>(bd.mpos), s.v + scale * dV[b]);
     s.w = hadamard(V<T>(bd.mrot), s.w + scale * dW[b]);
+    if (out->contact_dv) {  // velocity change of the collision integrator: after − before
+      const V3<T> dv = s.v - v0, dw = s.w - w0;
+      double* o = out->contact_dv + 6 * b;
+      o[0] = val(dv.x); o[1] = val(dv.y); o[2] = val(dv.z);
+      o[3] = val(dw.x); o[4] = val(dw.y); o[5] = val(dw.z);
+    }
   }
 }
 
 template <class T>
 void step_range(const OSys& S, const OOpts& opt, int64_t e0, int64_t e1, double* pos, double* rot,
                 double* vel, double* ang, const double* action, uint8_t* contact_active,
-                uint32_t* status, uint8_t* ambiguous) {
+                uint32_t* status, uint8_t* ambiguous, double* contact_dv) {
   const int B = S.nb;
   std::vector<BodyState<T>> st(B);
   for (int64_t e = e0; e < e1; ++e) {
@@ -445,7 +458,8 @@ void step_range(const OSys& S, const OOpts& opt, int64_t e0, int64_t e1, double*
       st[b].v = V<T>(v + 3 * b);
       st[b].w = V<T>(w + 3 * b);
     }
-    EnvOut<T> out{contact_active ? contact_active + e * S.ns : nullptr, false};
+    EnvOut<T> out{contact_active ? contact_active + e * S.ns : nullptr, false,
+                  contact_dv ? contact_dv + e * B * 6 : nullptr};
     if (out.active) std::memset(out.active, 0, S.ns);
     const double* a = action ? action + e * S.act_dim : nullptr;
     for (int s = 0; s < S.substeps; ++s) substep<T>(S, opt, st.data(), a, &out);
@@ -476,20 +490,23 @@ extern "C" {
 // pos/rot/vel/ang: [n][B][3|4|3|3] fp64; action: [n][act_dim] fp64 (may be NULL iff act_dim == 0).
 // contact_active: [n][ns] u8 number of substeps each slot was active (or NULL).
 // status: [n] bit0 non-finite, bit1 |x| > 1e6 (or NULL).  ambiguous: [n] R23 flag (or NULL).
+// contact_dv: [n][B][6] the last substep's collision-integrator Δv, Δω per body (or NULL).
 int oracle_step(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, double* pos, double* rot,
                 double* vel, double* ang, const double* action, uint8_t* contact_active,
-                uint32_t* status, uint8_t* ambiguous) {
+                uint32_t* status, uint8_t* ambiguous, double* contact_dv) {
   if (!S || !opt || e1 < e0) return 1;
-  step_range<double>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous);
+  step_range<double>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous,
+                     contact_dv);
   return 0;
 }
 
 // Diagnostic: the same step in fp32 arithmetic (inputs/outputs fp64 arrays).
 int oracle_step_f32(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, double* pos, double* rot,
                     double* vel, double* ang, const double* action, uint8_t* contact_active,
-                    uint32_t* status, uint8_t* ambiguous) {
+                    uint32_t* status, uint8_t* ambiguous, double* contact_dv) {
   if (!S || !opt || e1 < e0) return 1;
-  step_range<float>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous);
+  step_range<float>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous,
+                    contact_dv);
   return 0;
 }
 
@@ -501,7 +518,7 @@ int oracle_count_ops(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, do
   if (!S || !opt || e1 < e0) return 1;
   g_flops = 0;
   g_mufu = 0;
-  step_range<Cnt>(*S, *opt, e0, e1, pos, rot, vel, ang, action, nullptr, nullptr, nullptr);
+  step_range<Cnt>(*S, *opt, e0, e1, pos, rot, vel, ang, action, nullptr, nullptr, nullptr, nullptr);
   *flops = g_flops;
   *mufu = g_mufu;
   return 0;

@@ -11,6 +11,8 @@ reset (SURVEY §8(c).1 brax_reset; SPEC.md:352-360 reset noise):
   v += M_pos ⊙ σ_v·u(env, b, 0) and ω += M_rot ⊙ σ_ω·u(env, b, 1), where
   u(e, b, f)_k = (x_k >> 8)·2⁻²⁴·2 − 1 for the first three 32-bit outputs x_k of
   Philox4x32-10 with key = (seed mod 2³², seed >> 32), counter = (e, b, f, 0).
+Env auto-reset (NEXT-1): the k-th reset of env e draws from counter
+(e, b, f, k), so k = 0 is brax_reset itself; e is the env's global index.
 """
 from __future__ import annotations
 
@@ -45,17 +47,21 @@ def uniform_pm1(x: int) -> float:
     return ((x >> 8) * 2.0 ** -24) * 2.0 - 1.0
 
 
-def reset_qp(sys, dqp, n: int, seed: int, vel_noise: float, ang_noise: float):
+def reset_qp(sys, dqp, n: int, seed: int, vel_noise: float, ang_noise: float, *, env_ids=None, episode=None):
+    """default_qp + noise for n envs; env_ids [n] global env indices (default 0..n-1),
+    episode [n] reset counts (default 0)."""
     seed = int(seed) & 0xFFFFFFFFFFFFFFFF
     key = (seed & MASK, seed >> 32)
     B = len(sys.bodies)
+    env_ids = np.arange(n) if env_ids is None else np.asarray(env_ids)
+    episode = np.zeros(n, dtype=np.int64) if episode is None else np.asarray(episode)
     out = {k: np.broadcast_to(v, (n,) + v.shape).copy() for k, v in dqp.items()}
     for e in range(n):
         for b, body in enumerate(sys.bodies):
             if body.is_static:
                 continue
-            xv = philox4x32_10((e, b, 0, 0), key)
-            xw = philox4x32_10((e, b, 1, 0), key)
+            xv = philox4x32_10((int(env_ids[e]), b, 0, int(episode[e])), key)
+            xw = philox4x32_10((int(env_ids[e]), b, 1, int(episode[e])), key)
             for k in range(3):
                 out["vel"][e, b, k] += (1.0 - body.frozen_pos[k]) * vel_noise * uniform_pm1(xv[k])
                 out["ang"][e, b, k] += (1.0 - body.frozen_rot[k]) * ang_noise * uniform_pm1(xw[k])

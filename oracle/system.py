@@ -146,6 +146,20 @@ class Actuator:
 
 
 @dataclass
+class Task:
+    """Locomotion env epilogue (NEXT-1; R30-R35)."""
+    torso: int
+    forward: np.ndarray             # reward direction (world)
+    survive_reward: float
+    ctrl_cost: float
+    healthy_z: tuple | None         # (min, max) torso height; outside -> done
+    episode_length: int
+    contact_obs: bool               # append clipped per-body contact Δv, Δω
+    reset_vel_noise: float
+    reset_ang_noise: float
+
+
+@dataclass
 class System:
     dt: float
     substeps: int
@@ -159,6 +173,7 @@ class System:
     colliders: list                 # flat, global collider index order
     pairs: list                     # (colA, colB, type) after orientation
     slots: list                     # (pair, type, bodyA, bodyB, colA, colB, point)
+    task: Task | None = None
 
     @property
     def act_dim(self) -> int:
@@ -167,6 +182,17 @@ class System:
     @property
     def n_bodies(self) -> int:
         return len(self.bodies)
+
+    @property
+    def n_joint_dofs(self) -> int:
+        return sum(j.dof for j in self.joints)
+
+    @property
+    def obs_dim(self) -> int:
+        """torso z, quat (5) | joint angles (Σdof) | torso v, ω (6) | joint rates (Σdof) | contacts (6B)."""
+        if self.task is None:
+            return 0
+        return 11 + 2 * self.n_joint_dofs + (6 * len(self.bodies) if self.task.contact_obs else 0)
 
     def slot_table(self) -> np.ndarray:
         """Integer contact-slot table [C, 7] (pair, type, bodyA, bodyB, colA, colB, point)."""
@@ -218,7 +244,7 @@ def parse_system(text: str) -> System:
     root = parse_text(text)
     top = _fields(root, "config", {
         "dt", "substeps", "gravity", "friction", "elasticity", "baumgarte_erp",
-        "bodies", "joints", "actuators", "collide_include", "defaults"})
+        "bodies", "joints", "actuators", "collide_include", "defaults", "task"})
     dt = _one(top, "dt", "config", "num", 0.01)
     substeps = _one(top, "substeps", "config", "num", 1.0)
     if not dt > 0:
@@ -431,9 +457,57 @@ def parse_system(text: str) -> System:
     if len(slots) > 255:
         raise ValidationError("config", "more than 255 contact slots")
 
+    task = _parse_task(_one(top, "task", "config", "msg", None), bodies, names)
     return System(dt=dt, substeps=int(substeps), gravity=gravity, friction=friction,
                   elasticity=elasticity, baumgarte=beta, bodies=bodies, joints=joints,
-                  actuators=actuators, colliders=colliders, pairs=pairs, slots=slots)
+                  actuators=actuators, colliders=colliders, pairs=pairs, slots=slots, task=task)
+
+
+def _parse_task(node, bodies, names):
+    """task { torso forward survive_reward ctrl_cost healthy_z episode_length contact_obs reset_noise }."""
+    if node is None:
+        return None
+    path = "config.task"
+    tf = _fields(node, path, {"torso", "forward", "survive_reward", "ctrl_cost", "healthy_z", "episode_length",
+                              "contact_obs", "reset_noise"})
+    tn = _one(tf, "torso", path, "str")
+    if tn is None:
+        raise ValidationError(f"{path}.torso", "required")
+    if tn not in names:
+        raise ValidationError(f"{path}.torso", f"unknown body '{tn}'")
+    torso = names[tn]
+    if bodies[torso].is_static:
+        raise ValidationError(f"{path}.torso", "must not be a static body")
+    fwd = _vec3(_one(tf, "forward", path, "msg", [("x", 1.0, 0, 0)]), f"{path}.forward")
+    if not np.any(fwd != 0):
+        raise ValidationError(f"{path}.forward", "must be nonzero")
+    ctrl = _one(tf, "ctrl_cost", path, "num", 0.5)
+    if ctrl < 0:
+        raise ValidationError(f"{path}.ctrl_cost", "must be >= 0")
+    hz = _one(tf, "healthy_z", path, "msg", None)
+    healthy = None
+    if hz is not None:
+        hf = _fields(hz, f"{path}.healthy_z", {"min", "max"})
+        lo = _one(hf, "min", f"{path}.healthy_z", "num", None)
+        hi = _one(hf, "max", f"{path}.healthy_z", "num", None)
+        if lo is None or hi is None or not lo < hi:
+            raise ValidationError(f"{path}.healthy_z", "needs min < max")
+        healthy = (lo, hi)
+    L = _one(tf, "episode_length", path, "num", 1000.0)
+    if L != int(L) or L < 1:
+        raise ValidationError(f"{path}.episode_length", "must be a positive integer")
+    co = _one(tf, "contact_obs", path, None, False)
+    if co not in (True, False):
+        raise ValidationError(f"{path}.contact_obs", "expected true or false")
+    rn = _one(tf, "reset_noise", path, "msg", [])
+    rf = _fields(rn, f"{path}.reset_noise", {"vel", "ang"})
+    sv = _one(rf, "vel", f"{path}.reset_noise", "num", 0.1)
+    sw = _one(rf, "ang", f"{path}.reset_noise", "num", 0.1)
+    if sv < 0 or sw < 0:
+        raise ValidationError(f"{path}.reset_noise", "must be >= 0")
+    return Task(torso=torso, forward=fwd, survive_reward=_one(tf, "survive_reward", path, "num", 1.0),
+                ctrl_cost=ctrl, healthy_z=healthy, episode_length=int(L), contact_obs=bool(co),
+                reset_vel_noise=sv, reset_ang_noise=sw)
 
 
 def _orient(colliders, i, j):

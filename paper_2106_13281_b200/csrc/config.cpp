@@ -244,7 +244,7 @@ Config parse_config(const std::string& text) {
   Parser p{tokenize(text)};
   std::vector<Node> root = p.block(true);
   Fields top(root, "config", {"dt", "substeps", "gravity", "friction", "elasticity", "baumgarte_erp", "bodies",
-                              "joints", "actuators", "collide_include", "defaults"});
+                              "joints", "actuators", "collide_include", "defaults", "task"});
   Config c;
   c.dt = top.num("dt", 0.01);
   double sub = top.num("substeps", 1.0);
@@ -503,6 +503,49 @@ Config parse_config(const std::string& text) {
       c.slots.push_back({int(pi), pr.type, A.body, c.colliders[pr.col_b].body, pr.col_a, pr.col_b, first + k});
   }
   if (c.slots.size() > 255) invalid("config", "more than 255 contact slots");
+  if (const std::vector<Node>* tn = top.msg("task")) {
+    const std::string path = "config.task";
+    Fields tf(*tn, path, {"torso", "forward", "survive_reward", "ctrl_cost", "healthy_z", "episode_length",
+                          "contact_obs", "reset_noise"});
+    Task& t = c.task;
+    t.present = true;
+    bool has = false;
+    const std::string torso = tf.str("torso", &has);
+    if (!has) invalid(path + ".torso", "required");
+    if (!body_ix.count(torso)) invalid(path + ".torso", "unknown body '" + torso + "'");
+    t.torso = body_ix[torso];
+    if (c.bodies[t.torso].is_static()) invalid(path + ".torso", "must not be a static body");
+    if (const std::vector<Node>* f = tf.msg("forward")) {
+      t.forward[0] = t.forward[1] = t.forward[2] = 0;
+      vec3(f, path + ".forward", t.forward);
+    }
+    if (t.forward[0] == 0 && t.forward[1] == 0 && t.forward[2] == 0) invalid(path + ".forward", "must be nonzero");
+    t.survive_reward = tf.num("survive_reward", 1.0);
+    t.ctrl_cost = tf.num("ctrl_cost", 0.5);
+    if (t.ctrl_cost < 0) invalid(path + ".ctrl_cost", "must be >= 0");
+    if (const std::vector<Node>* hz = tf.msg("healthy_z")) {
+      Fields hf(*hz, path + ".healthy_z", {"min", "max"});
+      if (!hf.has("min") || !hf.has("max")) invalid(path + ".healthy_z", "needs min < max");
+      t.z_lo = hf.num("min", 0);
+      t.z_hi = hf.num("max", 0);
+      if (!(t.z_lo < t.z_hi)) invalid(path + ".healthy_z", "needs min < max");
+      t.has_healthy = true;
+    }
+    const double L = tf.num("episode_length", 1000.0);
+    if (L != std::floor(L) || L < 1 || L > 2147483647.0) invalid(path + ".episode_length", "must be a positive integer");
+    t.episode_length = int(L);
+    if (const Node* co = tf.one("contact_obs")) {
+      if (co->kind != Node::kIdent || (co->str != "true" && co->str != "false"))
+        invalid(path + ".contact_obs", "expected true or false");
+      t.contact_obs = co->str == "true";
+    }
+    if (const std::vector<Node>* rn = tf.msg("reset_noise")) {
+      Fields rf(*rn, path + ".reset_noise", {"vel", "ang"});
+      t.noise_vel = rf.num("vel", 0.1);
+      t.noise_ang = rf.num("ang", 0.1);
+    }
+    if (t.noise_vel < 0 || t.noise_ang < 0) invalid(path + ".reset_noise", "must be >= 0");
+  }
   return c;
 }
 

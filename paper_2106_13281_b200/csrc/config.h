@@ -71,6 +71,20 @@ struct Actuator {
 struct Pair { int col_a, col_b, type; };
 struct Slot { int pair, type, a, b, col_a, col_b, point; };
 
+// Locomotion env epilogue (NEXT-1; R30-R35): reward, done, auto-reset
+// and observations computed by the step kernel while the bodies are resident.
+struct Task {
+  bool present = false;
+  int torso = 0;
+  double forward[3] = {1, 0, 0};
+  double survive_reward = 1.0, ctrl_cost = 0.5;
+  bool has_healthy = false;
+  double z_lo = 0, z_hi = 0;
+  int episode_length = 1000;
+  bool contact_obs = false;
+  double noise_vel = 0.1, noise_ang = 0.1;
+};
+
 struct Config {
   double dt = 0.01;
   int substeps = 1;
@@ -83,6 +97,17 @@ struct Config {
   std::vector<Pair> pairs;
   std::vector<Slot> slots;
   int act_dim = 0;
+  Task task;
+  int n_joint_dofs() const {
+    int n = 0;
+    for (const Joint& j : joints) n += j.dof;
+    return n;
+  }
+  // z, quat | joint angles | v, ω | joint rates | per-body contact Δv, Δω (R32)
+  int obs_dim() const {
+    if (!task.present) return 0;
+    return 11 + 2 * n_joint_dofs() + (task.contact_obs ? 6 * int(bodies.size()) : 0);
+  }
 };
 
 // Parse + validate; throws brax::Error.
