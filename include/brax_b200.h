@@ -183,6 +183,40 @@ brax_status brax_step_ex(const brax_system *sys, brax_qp in, const float *action
 brax_status brax_rollout(const brax_system *sys, brax_qp in, const float *actions, int64_t n_steps, brax_qp out,
                          int64_t n_envs, const brax_step_extras *extras, void *stream);
 
+/* ---- NEXT-1: Gym-like env epilogue fused into the step (Table 1;
+ * :505-509 rewards; R30-R35).  Needs a `task { ... }` block in the system
+ * text.  Per step and env, after the last substep and while the bodies are still
+ * in shared memory:
+ *   reward = ((x'_torso − x_torso)·forward)/dt + survive_reward − ctrl_cost·Σ a²
+ *   done   = torso z' outside healthy_z, or steps + 1 >= episode_length
+ *   done envs auto-reset: default_qp + the task's reset noise with Philox counter
+ *   (env_offset + env, body, field, episode + 1); steps = 0, episode += 1
+ *   obs    = [z, quat | joint angles | v, ω | joint rates | clip(contact Δv, Δω, ±1)
+ *            per body if contact_obs] of the returned (possibly reset) state.
+ * All arrays are device arrays; steps and episode are updated in place. */
+typedef struct brax_env_io {
+  float *obs;          /* [n_steps][n][obs_dim] (brax_env_reset: [n][obs_dim]) or NULL */
+  float *reward;       /* [n_steps][n] or NULL */
+  uint8_t *done;       /* [n_steps][n] or NULL */
+  int32_t *steps;      /* [n] in/out: steps since the env's last reset (required) */
+  uint32_t *episode;   /* [n] in/out: resets so far = reset-noise counter (required) */
+  uint64_t seed;       /* reset-noise key (as brax_reset's seed) */
+  int64_t env_offset;  /* global index of env 0 of this batch (multi-GPU shards) */
+} brax_env_io;
+/* out = {has_task, obs_dim, episode_length, torso body index (or -1)}. */
+brax_status brax_system_task_info(const brax_system *sys, int32_t out[4]);
+/* n_steps steps with the epilogue after each (in may equal out; actions [n_steps][n][A]).
+ * BRAX_E_INVALID_ARGUMENT if the system has no task or steps / episode are NULL. */
+brax_status brax_env_step(const brax_system *sys, brax_qp in, const float *actions, int64_t n_steps, brax_qp out,
+                          int64_t n_envs, const brax_env_io *io, void *stream);
+/* Episode-0 reset (the task's reset noise, Philox counter (env_offset + env, b, f, 0)),
+ * steps = episode = 0, and io->obs (if not NULL). */
+brax_status brax_env_reset(const brax_system *sys, brax_qp out, int64_t n_envs, const brax_env_io *io,
+                           void *stream);
+/* Observation rows [n][obs_dim] of a QP (contact terms zero); the QP is not modified. */
+brax_status brax_env_observe(const brax_system *sys, brax_qp qp, int64_t n_envs, float *obs, void *stream);
+
+
 const char *brax_status_string(brax_status s);
 const char *brax_last_error_detail(void);
 int brax_abi_version(void);

@@ -24,6 +24,7 @@ __all__ = [
     "brax_config_slot_table", "brax_config_default_qp", "brax_system_create", "brax_system_destroy",
     "brax_system_get_info", "brax_system_slot_table", "brax_default_qp", "brax_reset", "brax_step",
     "brax_step_ex", "brax_rollout", "brax_qp", "brax_step_extras", "brax_system_info", "LIB_PATH", "lib",
+    "brax_env_io", "brax_system_task_info", "brax_env_step", "brax_env_reset", "brax_env_observe",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbrax_b200.so")
@@ -51,6 +52,11 @@ class brax_qp(C.Structure):
 
 class brax_step_extras(C.Structure):
     _fields_ = [("status", C.c_void_p), ("contact_active", C.c_void_p)]
+
+
+class brax_env_io(C.Structure):
+    _fields_ = [("obs", C.c_void_p), ("reward", C.c_void_p), ("done", C.c_void_p), ("steps", C.c_void_p),
+                ("episode", C.c_void_p), ("seed", C.c_uint64), ("env_offset", C.c_int64)]
 
 
 class brax_system_info(C.Structure):
@@ -82,6 +88,10 @@ _SIGS = {
     "brax_step": ([_P, brax_qp, _P, brax_qp, C.c_int64, _P], C.c_int),
     "brax_step_ex": ([_P, brax_qp, _P, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_rollout": ([_P, brax_qp, _P, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
+    "brax_system_task_info": ([_P, _i32p], C.c_int),
+    "brax_env_step": ([_P, brax_qp, _P, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_env_io), _P], C.c_int),
+    "brax_env_reset": ([_P, brax_qp, C.c_int64, C.POINTER(brax_env_io), _P], C.c_int),
+    "brax_env_observe": ([_P, brax_qp, C.c_int64, _P, _P], C.c_int),
     "brax_status_string": ([C.c_int], C.c_char_p),
     "brax_last_error_detail": ([], C.c_char_p),
     "brax_abi_version": ([], C.c_int),
@@ -208,6 +218,38 @@ def brax_rollout(sys: int, qp_in, actions, n_steps: int, qp_out, n_envs: int, st
                             _qp(qp_out), n_envs, None if x is None else C.byref(x), _stream(stream)))
 
 
+def _ptr(t):
+    return None if t is None else int(t.data_ptr())
+
+
+def _env_io(obs, reward, done, steps, episode, seed, env_offset):
+    return brax_env_io(_ptr(obs), _ptr(reward), _ptr(done), _ptr(steps), _ptr(episode),
+                       int(seed) & 0xFFFFFFFFFFFFFFFF, int(env_offset))
+
+
+def brax_system_task_info(sys: int):
+    out = (C.c_int32 * 4)()
+    _check(lib.brax_system_task_info(sys, out))
+    return dict(zip(("has_task", "obs_dim", "episode_length", "torso"), (int(x) for x in out)))
+
+
+def brax_env_step(sys: int, qp_in, actions, n_steps: int, qp_out, n_envs: int, obs, reward, done, steps, episode,
+                  seed: int = 0, env_offset: int = 0, stream=None) -> None:
+    io = _env_io(obs, reward, done, steps, episode, seed, env_offset)
+    _check(lib.brax_env_step(sys, _qp(qp_in), _ptr(actions), n_steps, _qp(qp_out), n_envs, C.byref(io),
+                             _stream(stream)))
+
+
+def brax_env_reset(sys: int, qp_out, n_envs: int, obs, steps, episode, seed: int = 0, env_offset: int = 0,
+                   stream=None) -> None:
+    io = _env_io(obs, None, None, steps, episode, seed, env_offset)
+    _check(lib.brax_env_reset(sys, _qp(qp_out), n_envs, C.byref(io), _stream(stream)))
+
+
+def brax_env_observe(sys: int, qp, n_envs: int, obs, stream=None) -> None:
+    _check(lib.brax_env_observe(sys, _qp(qp), n_envs, _ptr(obs), _stream(stream)))
+
+
 # ---------------------------------------------------------------- convenience object
 class System:
     """A config parsed and turned into a device-resident system (owns both handles)."""
@@ -285,6 +327,47 @@ class System:
         else:
             brax_step_ex(self._sys, qp_in, action, qp_out, n, status, contact_active, stream)
         return qp_out
+
+    # ---- NEXT-1 env epilogue (needs a `task` block) ----
+    def task_info(self):
+        return brax_system_task_info(self._sys)
+
+    def env_state(self, n: int):
+        """Device buffers for an env batch: qp, steps [n] int32, episode [n] int32 (uint32 bits)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        return {"qp": self.alloc_qp(n), "steps": torch.zeros(n, dtype=torch.int32, device=dev),
+                "episode": torch.zeros(n, dtype=torch.int32, device=dev)}
+
+    def env_reset(self, state, seed: int = 0, env_offset: int = 0, stream=None):
+        """Episode-0 reset of state (env_state dict) in place; returns obs [n, obs_dim]."""
+        import torch
+        n = state["steps"].shape[0]
+        obs = torch.empty((n, self.task_info()["obs_dim"]), device=state["steps"].device)
+        brax_env_reset(self._sys, state["qp"], n, obs, state["steps"], state["episode"], seed, env_offset, stream)
+        return obs
+
+    def env_step(self, state, actions, seed: int = 0, env_offset: int = 0, stream=None):
+        """actions [n, A] (one step) or [T, n, A]; advances state in place and returns
+        dict(obs [T, n, obs_dim], reward [T, n], done [T, n] uint8) (T = 1 for one step)."""
+        import torch
+        n = state["steps"].shape[0]
+        if actions is not None and actions.dim() == 2:
+            actions = actions.unsqueeze(0)
+        T = 1 if actions is None else actions.shape[0]
+        dev = state["steps"].device
+        out = {"obs": torch.empty((T, n, self.task_info()["obs_dim"]), device=dev),
+               "reward": torch.empty((T, n), device=dev), "done": torch.empty((T, n), dtype=torch.uint8, device=dev)}
+        brax_env_step(self._sys, state["qp"], actions, T, state["qp"], n, out["obs"], out["reward"], out["done"],
+                      state["steps"], state["episode"], seed, env_offset, stream)
+        return out
+
+    def env_observe(self, qp, stream=None):
+        import torch
+        n = qp["pos"].shape[0]
+        obs = torch.empty((n, self.task_info()["obs_dim"]), device=qp["pos"].device)
+        brax_env_observe(self._sys, qp, n, obs, stream)
+        return obs
 
     def rollout(self, qp_in, actions, qp_out=None, *, n_steps=None, status=None, contact_active=None,
                 stream=None):

@@ -48,16 +48,20 @@ brax_status cuda_status(cudaError_t e, const char* what) {
 }
 
 brax_status step_common(const brax_system* sys, brax_qp in, const float* actions, int64_t n_steps, brax_qp out,
-                        int64_t n_envs, const brax_step_extras* x, void* stream) {
+                        int64_t n_envs, const brax_step_extras* x, void* stream, const brax_env_io* io = nullptr,
+                        float* observe_only = nullptr) {
   if (!sys || !sys->impl) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
   if (n_envs < 0 || n_steps < 0) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs and n_steps must be >= 0");
-  if (n_envs == 0 || n_steps == 0) return BRAX_OK;
+  const bool env = io != nullptr || observe_only != nullptr;
+  if (env && !sys->impl->cfg.task.present) return fail(BRAX_E_INVALID_ARGUMENT, "system has no task block");
+  if (io && (!io->steps || !io->episode)) return fail(BRAX_E_INVALID_ARGUMENT, "env io: steps and episode are required");
+  if (n_envs == 0 || (n_steps == 0 && !observe_only)) return BRAX_OK;
   if (n_envs > (int64_t(1) << 40)) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs too large");
   brax_status st = check_qp(in, "in");
   if (st != BRAX_OK) return st;
   if ((st = check_qp(out, "out")) != BRAX_OK) return st;
   const brax::System& s = *sys->impl;
-  if (s.hd.A > 0 && !actions) return fail(BRAX_E_INVALID_ARGUMENT, "action is NULL but act_dim > 0");
+  if (s.hd.A > 0 && !actions && !observe_only) return fail(BRAX_E_INVALID_ARGUMENT, "action is NULL but act_dim > 0");
   if (actions && !aligned16(actions)) return fail(BRAX_E_MISALIGNED, "action must be 16-byte aligned");
   // aliasing: identical (in == out for all four arrays) is fine, any other overlap is not
   const float* ins[4] = {in.pos, in.rot, in.vel, in.ang};
@@ -83,6 +87,24 @@ brax_status step_common(const brax_system* sys, brax_qp in, const float* actions
   brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, out.pos, out.rot, out.vel, out.ang, actions,
                    x ? x->status : nullptr, x ? x->contact_active : nullptr, n_envs, n_steps, 0, 0, nullptr};
   if (a.contact_active && s.hd.C == 0) a.contact_active = nullptr;
+  if (env) {
+    a.env = 1;
+    a.dqp = s.d_default_qp;
+    a.masks = s.d_masks;
+    if (observe_only) {
+      a.n_steps = 0;
+      a.actions = nullptr;
+      a.obs = observe_only;
+    } else {
+      a.obs = io->obs;
+      a.reward = io->reward;
+      a.done = io->done;
+      a.steps = io->steps;
+      a.episode = io->episode;
+      a.seed = io->seed;
+      a.env_offset = io->env_offset;
+    }
+  }
   int cur = -1;
   cudaGetDevice(&cur);
   if (cur != s.device) {
@@ -276,6 +298,48 @@ brax_status brax_step_ex(const brax_system* sys, brax_qp in, const float* action
 brax_status brax_rollout(const brax_system* sys, brax_qp in, const float* actions, int64_t n_steps, brax_qp out,
                          int64_t n_envs, const brax_step_extras* extras, void* stream) {
   return step_common(sys, in, actions, n_steps, out, n_envs, extras, stream);
+}
+
+brax_status brax_system_task_info(const brax_system* sys, int32_t out[4]) {
+  if (!sys || !out) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
+  const brax::Config& c = sys->impl->cfg;
+  out[0] = c.task.present ? 1 : 0;
+  out[1] = c.obs_dim();
+  out[2] = c.task.present ? c.task.episode_length : 0;
+  out[3] = c.task.present ? c.task.torso : -1;
+  return BRAX_OK;
+}
+
+brax_status brax_env_step(const brax_system* sys, brax_qp in, const float* actions, int64_t n_steps, brax_qp out,
+                          int64_t n_envs, const brax_env_io* io, void* stream) {
+  if (!io) return fail(BRAX_E_INVALID_ARGUMENT, "io is NULL");
+  return step_common(sys, in, actions, n_steps, out, n_envs, nullptr, stream, io);
+}
+
+brax_status brax_env_observe(const brax_system* sys, brax_qp qp, int64_t n_envs, float* obs, void* stream) {
+  if (!obs) return fail(BRAX_E_INVALID_ARGUMENT, "obs is NULL");
+  return step_common(sys, qp, nullptr, 0, qp, n_envs, nullptr, stream, nullptr, obs);
+}
+
+brax_status brax_env_reset(const brax_system* sys, brax_qp out, int64_t n_envs, const brax_env_io* io,
+                           void* stream) {
+  if (!sys || !io) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
+  const brax::System& s = *sys->impl;
+  if (!s.cfg.task.present) return fail(BRAX_E_INVALID_ARGUMENT, "system has no task block");
+  if (!io->steps || !io->episode) return fail(BRAX_E_INVALID_ARGUMENT, "env io: steps and episode are required");
+  if (n_envs < 0) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs must be >= 0");
+  if (n_envs == 0) return BRAX_OK;
+  brax_status st = check_qp(out, "out");
+  if (st != BRAX_OK) return st;
+  cudaSetDevice(s.device);
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaError_t e = brax::launch_reset(s, out.pos, out.rot, out.vel, out.ang, n_envs, io->seed,
+                                     float(s.cfg.task.noise_vel), float(s.cfg.task.noise_ang), cs, io->env_offset);
+  if (e == cudaSuccess) e = cudaMemsetAsync(io->steps, 0, size_t(n_envs) * 4, cs);
+  if (e == cudaSuccess) e = cudaMemsetAsync(io->episode, 0, size_t(n_envs) * 4, cs);
+  if (e != cudaSuccess) return cuda_status(e, "brax_env_reset");
+  if (!io->obs) return BRAX_OK;
+  return step_common(sys, out, nullptr, 0, out, n_envs, nullptr, stream, nullptr, io->obs);
 }
 
 }  // extern "C"

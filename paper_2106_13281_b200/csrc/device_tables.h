@@ -55,7 +55,7 @@ struct alignas(16) DBody {  // 16 words
 };
 struct alignas(16) DJoint {  // 36 words
   int32_t parent, child, dof, act_kind;
-  int32_t act_offset, flags, pad0, pad1;
+  int32_t act_offset, flags, obs_off, pad1;  // obs_off: Σ dof of the joints before this one (R32)
   float o_p[3], k;          // parent anchor offset; stiffness
   float o_c[3], c_l;        // child anchor offset; linear (spring) damping
   float jp[4];              // J_p = rotation
@@ -101,28 +101,47 @@ BRAX_HD inline int32_t inc_pack(int index, bool second_side) { return (index << 
 
 // Shared-memory layout of the step kernel (words; every region 16-byte aligned).
 //   [2 mbarriers][tables][QP records B·L·rec_q][U][sA A·E][action staging E·A][counts C·E][status E]
+//   [env epilogue, systems with a task: x0 3E | steps E | episode E | reset flag E | contact Δv 6·B·E]
 // with L = E/V lanes (records) per body or item.  U holds the joint and slot
-// records during the substeps and the contiguous TMA staging chunks
-// (pos|rot|vel|ang, E·B·13 words) while loading / storing.
+// records during the substeps, the contiguous TMA staging chunks (pos|rot|vel|ang,
+// E·B·13 words) while loading / storing, and the observation rows (E·obs_dim) in
+// the env epilogue.
 struct SmemLayout {
-  int32_t blob, q, u, a, astg, cnt, stat, total_words;
+  int32_t blob, q, u, a, astg, cnt, stat, x0, steps, ep, rst, co, total_words;
 };
 BRAX_HD inline int32_t round4(int32_t w) { return (w + 3) & ~3; }
 BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A, int32_t E, int32_t V,
-                                      int32_t blob_words) {
+                                      int32_t blob_words, int32_t obs_dim, int32_t contact_obs) {
   SmemLayout L;
   const int32_t LG = E / V;
   L.blob = 4;
   L.q = L.blob + round4(blob_words);
   L.u = L.q + B * LG * rec_q(V);
-  const int32_t recs = J * LG * rec_j(V) + C * LG * rec_c(V), stg = E * B * 13;
-  L.a = L.u + round4(recs > stg ? recs : stg);
+  int32_t u = J * LG * rec_j(V) + C * LG * rec_c(V);
+  if (u < E * B * 13) u = E * B * 13;
+  if (u < E * obs_dim) u = E * obs_dim;
+  L.a = L.u + round4(u);
   L.astg = L.a + round4(A * E);
   L.cnt = L.astg + round4(A * E);
   L.stat = L.cnt + round4(C * E);
-  L.total_words = L.stat + round4(E);
+  L.x0 = L.stat + round4(E);
+  const int32_t env = obs_dim > 0 ? 1 : 0;
+  L.steps = L.x0 + env * round4(3 * E);
+  L.ep = L.steps + env * round4(E);
+  L.rst = L.ep + env * round4(E);
+  L.co = L.rst + env * round4(E);
+  L.total_words = L.co + env * (contact_obs ? round4(6 * B * E) : 0);
   return L;
 }
+
+// Env epilogue parameters (NEXT-1, R30-R35); present == 0: no task.
+struct DTask {
+  int32_t present, torso, episode_length, contact_obs;
+  int32_t nq, obs_dim, has_healthy, pad0;
+  float fwd[3], dt;
+  float survive, ctrl_cost, z_lo, z_hi;
+  float noise_vel, noise_ang, pad1, pad2;
+};
 
 // Arguments of one step launch (device pointers; see include/brax_b200.h).
 struct StepArgs {
@@ -136,6 +155,19 @@ struct StepArgs {
   int32_t bulk_ok;             // all QP pointers 16-byte aligned: TMA bulk staging for full blocks
   int32_t act_bulk_ok;         // actions 16-byte aligned and n·A % 4 == 0: TMA bulk action staging
   unsigned long long* phase_cycles;  // [4] per-phase SM cycles summed over blocks (tracing), or NULL
+  // env epilogue (NEXT-1): env == 0 -> physics only.  With env == 1 every step also
+  // writes reward [t][n], done [t][n], obs [t][n][obs_dim] and auto-resets done envs;
+  // n_steps == 0 with env == 1 only observes (obs [n][obs_dim], QP not written).
+  int32_t env;
+  float* obs;
+  float* reward;
+  uint8_t* done;
+  int32_t* steps;              // [n] in/out
+  uint32_t* episode;           // [n] in/out
+  uint64_t seed;               // reset-noise key
+  int64_t env_offset;          // global index of env 0 (Philox counter)
+  const float* dqp;            // default_qp: pos [B][3] | rot [B][4]
+  const float* masks;          // per body: mpos[3] mrot[3] static
 };
 
 // A work plan for one lane-group count G (E = 32/G envs per block): each warp's
@@ -159,6 +191,7 @@ struct DHeader {            // passed by value as a kernel argument
   int32_t off_jinc_begin, off_jinc;    // per body: joint incidence entries
   int32_t off_cinc_begin, off_cinc;    // per body: contact-slot incidence entries
   uint32_t row_magic[4];    // ⌈2³²/(B·K)⌉ for K = 3, 4 (index 0: K=3, 1: K=4), A (index 2)
+  DTask task;
   DPlan plan[kNumPlans];
 };
 

@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "device_rng.cuh"
 #include "step_device.cuh"
 #include "system.h"
 
@@ -55,7 +56,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const StepArgs& a = ka.a;
   constexpr int V = Lanes<S>::V, QS = Lanes<S>::QS, JS = Lanes<S>::JS, CS = Lanes<S>::CS;
   const int B = H.B, J = H.J, C = H.C, A = H.A, E = P.E, G = P.G;
-  const SmemLayout L = smem_layout(B, J, C, A, E, V, H.blob_words);
+  const DTask& T = H.task;
+  const SmemLayout L = smem_layout(B, J, C, A, E, V, H.blob_words, T.obs_dim, T.contact_obs);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [0] tables + QP, [1] actions
   uint32_t* sBlob = smem + L.blob;
   float* sQ = reinterpret_cast<float*>(smem + L.q);
@@ -67,6 +69,16 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   float* sAstg = reinterpret_cast<float*>(smem + L.astg);
   float* sCnt = reinterpret_cast<float*>(smem + L.cnt);
   uint32_t* sStat = smem + L.stat;
+  // env epilogue (NEXT-1): torso position at the step start, steps / episode / reset flag
+  // per env, contact Δv [B][6][E] of the last substep, observation rows (alias U)
+  float* sX0 = reinterpret_cast<float*>(smem + L.x0);
+  int32_t* sSteps = reinterpret_cast<int32_t*>(smem + L.steps);
+  uint32_t* sEp = smem + L.ep;
+  int32_t* sRst = reinterpret_cast<int32_t*>(smem + L.rst);
+  float* sCo = reinterpret_cast<float*>(smem + L.co);
+  float* sObs = reinterpret_cast<float*>(smem + L.u);
+  const bool envm = a.env != 0;
+  const bool save_co = envm && T.contact_obs;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // tracing (brax_system_phase_cycles): thread 0 times prologue / joints+contacts /
@@ -116,6 +128,14 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   mbar_wait(&bars[0], 0);
   if (bulk) stg_to_records<V>(stg, sQ, B, E);
   for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
+  if (envm) {
+    for (int i = tid; i < E; i += blockDim.x) {
+      sSteps[i] = i < nvalid && a.steps ? a.steps[e0 + i] : 0;
+      sEp[i] = i < nvalid && a.episode ? a.episode[e0 + i] : 0u;
+    }
+    if (save_co)
+      for (int i = tid; i < 6 * B * E; i += blockDim.x) sCo[i] = 0.f;
+  }
   __syncthreads();
   lap(0);
 
@@ -135,12 +155,66 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const int it0 = item_begin[warp], it1 = item_begin[warp + 1];
   const int bw0 = body_begin[warp], bw1 = body_begin[warp + 1];
 
+  const int od = T.obs_dim;
+  // ---- NEXT-1 env epilogue pieces (R30-R35; per-env scalar code spells out its rounding) ----
+  auto save_x0 = [&]() {  // torso position at the step boundary (before S2)
+    for (int i = tid; i < E; i += blockDim.x)
+      for (int k = 0; k < 3; ++k) sX0[3 * i + k] = sQ[qword<V>(T.torso, i, 0, k, E)];
+  };
+  auto observe = [&](float* obs_out) {  // obs rows of the block's envs -> obs_out [nvalid][od]
+    // joints: angles and rates, by the warps that own them
+    for (int it = it0; it < it1; ++it) {
+      int item = items[it * G];
+      if (item < 0 || item >= J) continue;
+      const DJoint& jt = joints[item];
+      joint_obs<S>(jt, Row<S>{sQ + (jt.parent * LG + el) * QS}, Row<S>{sQ + (jt.child * LG + el) * QS},
+                   sObs + el * od, LG * od, 5 + jt.obs_off, 11 + T.nq + jt.obs_off);
+    }
+    // torso and contact parts, one thread per (env, word)
+    const int nco = T.contact_obs ? 6 * B : 0;
+    for (int i = tid; i < E * (11 + nco); i += blockDim.x) {
+      const int env = i / (11 + nco), k = i - env * (11 + nco);
+      float v;
+      int at;
+      if (k < 11) {
+        const int f = k == 0 ? 0 : k < 5 ? 1 : k < 8 ? 2 : 3;
+        const int c = k == 0 ? 2 : k < 5 ? k - 1 : k < 8 ? k - 5 : k - 8;
+        v = sQ[qword<V>(T.torso, env, f, c, E)];
+        at = k < 5 ? k : 5 + T.nq + (k - 5);
+      } else {
+        const int b = (k - 11) / 6, kk = (k - 11) - 6 * b;
+        v = fminf(fmaxf(sCo[(b * 6 + kk) * E + eslot<V>(env, E)], -1.f), 1.f);
+        at = 11 + 2 * T.nq + (k - 11);
+      }
+      sObs[env * od + at] = v;
+    }
+    __syncthreads();
+    for (int i = tid; i < nvalid * od; i += blockDim.x) obs_out[i] = sObs[i];
+    __syncthreads();
+  };
+
+  if (envm && a.n_steps == 0) {  // observe only (brax_env_observe / brax_env_reset): QP not written
+    observe(a.obs + e0 * od);
+    return;
+  }
   // S2 of the first substep; every later S2 is fused into the previous substep's integrate()
+  if (envm) {
+    save_x0();
+    __syncthreads();
+  }
   for (int i = bw0; i < bw1; ++i) {
     int b = bodies_of_warp[i * G];
     if (b >= 0) kinematic<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, H.h);
   }
   for (int64_t step = 0; step < a.n_steps; ++step) {
+    if (envm && step > 0) {  // env mode ends every step at the boundary: its S2 runs here
+      save_x0();
+      __syncthreads();
+      for (int i = bw0; i < bw1; ++i) {
+        int b = bodies_of_warp[i * G];
+        if (b >= 0) kinematic<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, H.h);
+      }
+    }
     if (act_bulk) {  // this step's actions arrived in sAstg [E][A]; transpose to sA [A][E]
       mbar_wait(&bars[1], uint32_t(step & 1));
       for (int i = tid; i < E * A; i += blockDim.x) {
@@ -197,9 +271,64 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
           int e = cinc[k];
           acc.slot(sCe + (e >> 4) * (LG * CS), e);
         }
-        const bool kin = !(step + 1 == a.n_steps && s + 1 == H.S);  // fused S2 of the next substep
-        integrate<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, acc, H.h, H.g, kin);
+        const bool last = s + 1 == H.S;
+        const bool kin = !(last && (envm || step + 1 == a.n_steps));  // fused S2 of the next substep
+        integrate<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, acc, H.h, H.g, kin,
+                     save_co && last ? sCo + b * 6 * E + el * V : nullptr, E);
       }
+    }
+    if (envm) {
+      __syncthreads();
+      // reward, done, step / episode counters (one thread per env)
+      for (int i = tid; i < E; i += blockDim.x) {
+        float x1[3];
+        for (int k = 0; k < 3; ++k) x1[k] = sQ[qword<V>(T.torso, i, 0, k, E)];
+        float fwd = __fmul_rn(__fadd_rn(x1[0], -sX0[3 * i]), T.fwd[0]);
+        fwd = __fmaf_rn(__fadd_rn(x1[1], -sX0[3 * i + 1]), T.fwd[1], fwd);
+        fwd = __fmaf_rn(__fadd_rn(x1[2], -sX0[3 * i + 2]), T.fwd[2], fwd);
+        float ctrl = 0.f;
+        for (int k = 0; k < A; ++k) {
+          const float u = sA[k * E + eslot<V>(i, E)];
+          ctrl = __fmaf_rn(u, u, ctrl);
+        }
+        const float reward = __fadd_rn(__fadd_rn(__fdiv_rn(fwd, T.dt), T.survive), -__fmul_rn(T.ctrl_cost, ctrl));
+        const int32_t st1 = sSteps[i] + 1;
+        bool done = st1 >= T.episode_length;
+        if (T.has_healthy) done = done || x1[2] < T.z_lo || x1[2] > T.z_hi;
+        sRst[i] = done ? 1 : 0;
+        sSteps[i] = done ? 0 : st1;
+        if (done) sEp[i] += 1u;
+        if (i < nvalid) {
+          if (a.reward) a.reward[step * a.n_envs + e0 + i] = reward;
+          if (a.done) a.done[step * a.n_envs + e0 + i] = done ? 1 : 0;
+        }
+      }
+      __syncthreads();
+      // auto-reset of done envs (R34): default_qp + noise, Philox counter (env, b, f, episode)
+      const uint2 key = make_uint2(uint32_t(a.seed & 0xffffffffu), uint32_t(a.seed >> 32));
+      for (int i = tid; i < E * B; i += blockDim.x) {
+        const int env = i / B, b = i - env * B;
+        if (!sRst[env]) continue;
+        float x[3], q[4], v[3], w[3];
+        reset_body(a.dqp, a.masks, B, b, uint32_t(a.env_offset + e0 + env), sEp[env], key, T.noise_vel,
+                   T.noise_ang, x, q, v, w);
+        for (int k = 0; k < 3; ++k) {
+          sQ[qword<V>(b, env, 0, k, E)] = x[k];
+          sQ[qword<V>(b, env, 2, k, E)] = v[k];
+          sQ[qword<V>(b, env, 3, k, E)] = w[k];
+        }
+        for (int k = 0; k < 4; ++k) sQ[qword<V>(b, env, 1, k, E)] = q[k];
+        if (save_co)
+          for (int k = 0; k < 6; ++k) sCo[(b * 6 + k) * E + eslot<V>(env, E)] = 0.f;
+      }
+      __syncthreads();
+      if (a.obs) observe(a.obs + (step * a.n_envs + e0) * od);
+    }
+  }
+  if (envm) {
+    for (int i = tid; i < nvalid; i += blockDim.x) {
+      if (a.steps) a.steps[e0 + i] = sSteps[i];
+      if (a.episode) a.episode[e0 + i] = sEp[i];
     }
   }
   lap(2);
@@ -364,6 +493,7 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   t.n_steps = 1;
   t.status = nullptr;
   t.contact_active = nullptr;
+  t.env = 0;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -409,10 +539,11 @@ LaunchConfig launch_config(const System& sys, int64_t n_envs) {
 }
 
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream) {
-  if (a.n_envs <= 0 || a.n_steps <= 0) return cudaSuccess;
+  if (a.n_envs <= 0 || (a.n_steps <= 0 && !a.env)) return cudaSuccess;
   LaunchConfig c = launch_config(sys, a.n_envs);
   // first launch of this batch size outside graph capture: measure every plan once
-  if (!c.tuned && sys.autotune && a.n_envs >= 256 && !std::getenv("BRAX_PLAN") && !std::getenv("BRAX_MAXREG")) {
+  if (!c.tuned && sys.autotune && a.n_envs >= 256 && a.n_steps > 0 && !std::getenv("BRAX_PLAN") &&
+      !std::getenv("BRAX_MAXREG")) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
       c = tune(sys, a, stream);

@@ -394,6 +394,52 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
   Lanes<S>::st3(out + 2 * M, V3T<S>{-tp.x, -tp.y, -tp.z});
 }
 
+// ---- NEXT-1 observation of one joint (R32): its free axes' angles θ_i (R7) and
+// rates θ̇_i = b_i·ω_r, ω_r = R(q_p⊗J_p)ᵀ(ω_c − ω_p), b the dual basis of the rotation
+// axes (as in joint()).  rows: obs row of this lane's first env; the second env's
+// (S = F2) is `second` words further; angle i at word ang0 + i, rate i at rate0 + i.
+template <class S> __device__ __forceinline__ void st_rows(float* p, int second, S v);
+template <> __device__ __forceinline__ void st_rows<F1>(float* p, int, F1 v) { *p = v.x; }
+template <> __device__ __forceinline__ void st_rows<F2>(float* p, int second, F2 v) {
+  p[0] = v.x;
+  p[second] = v.y;
+}
+template <class S>
+__device__ __forceinline__ void joint_obs(const DJoint& Jm, Row<S> P, Row<S> C, float* rows, int second, int ang0,
+                                          int rate0) {
+  const float4* J4 = reinterpret_cast<const float4*>(&Jm);
+  const int dof = reinterpret_cast<const int4*>(&Jm)->z;
+  const float4 jp = J4[4], jc = J4[5];
+  Q4T<S> fp = qmul(P.rot(), Q4T<S>{bc<S>(jp.x), bc<S>(jp.y), bc<S>(jp.z), bc<S>(jp.w)});
+  Q4T<S> fc = qmul(C.rot(), Q4T<S>{bc<S>(jc.x), bc<S>(jc.y), bc<S>(jc.z), bc<S>(jc.w)});
+  Q4T<S> qr = qmul(qconj(fp), fc);
+  S sg = sel(lt(qr.w, bc<S>(0.f)), bc<S>(-1.f), bc<S>(1.f));
+  qr = Q4T<S>{sg * qr.w, sg * qr.x, sg * qr.y, sg * qr.z};
+  S R02 = 2.f * (qr.x * qr.z + qr.w * qr.y);
+  S R12 = 2.f * (qr.y * qr.z - qr.w * qr.x);
+  S R22 = 1.f - 2.f * (qr.x * qr.x + qr.y * qr.y);
+  S R01 = 2.f * (qr.x * qr.y - qr.w * qr.z);
+  S R00 = 1.f - 2.f * (qr.y * qr.y + qr.z * qr.z);
+  S s1 = clampv(R02, -1.f, 1.f);
+  S th[3] = {atan2_f(-R12, R22), asin_f(s1), atan2_f(-R01, R00)};
+  S c2 = R12 * R12 + R22 * R22;
+  S ic = sel(gt(c2, bc<S>(0.f)), vrsqrt(c2), bc<S>(0.f));   // 1 / cos θ1
+  S c0 = sel(gt(c2, bc<S>(0.f)), R22 * ic, bc<S>(1.f));      // cos θ0
+  S s0 = sel(gt(c2, bc<S>(0.f)), -(R12 * ic), bc<S>(0.f));   // sin θ0
+  S c1 = c2 * ic;                                             // cos θ1
+  S icg = c1 * vdiv(bc<S>(1.f), vmax(c2, bc<S>(0.01f)));      // cos θ1 / max(cos² θ1, 0.01)
+  V3T<S> wr = rotate(qconj(fp), C.ang() - P.ang());
+  S t = s1 * icg;
+  S rate[3] = {wr.x + (s0 * t) * wr.y - (c0 * t) * wr.z, c0 * wr.y + s0 * wr.z, c0 * icg * wr.z - s0 * icg * wr.y};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    if (i < dof) {
+      st_rows<S>(rows + ang0 + i, second, th[i]);
+      st_rows<S>(rows + rate0 + i, second, rate[i]);
+    }
+  }
+}
+
 // Closest points between segments (Ericson, Real-Time Collision Detection §5.1.9),
 // with the per-env branches written as selects.  Degenerate (zero-length)
 // segments are a parameter property (uniform): a = |d1|², e = |d2|² > 0 unless ℓ = 0.
@@ -564,14 +610,17 @@ template <class S> struct Acc {
 // ---- S7 + S8: potential integrator then collision integrator (R14, R21),
 // fused (kin = true) with the next substep's S2 kinematic integrator of the same
 // body: same arithmetic as kinematic(), with v and ω still in registers.
+// co (env epilogue with contact observations, last substep of a step): this body's
+// and lane's [6][E] slot for the collision integrator's velocity change; else NULL.
 template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Row<S> r, const Acc<S>& acc, float h,
-                                                             const float* g, bool kin) {
+                                                             const float* g, bool kin, float* co, int E) {
   const bool iso = bd.flags & kFlagIso, fp = bd.flags & kFlagFreePos, fr = bd.flags & kFlagFreeRot;
   Q4T<S> q = r.rot();
   V3T<S> v = axpy(h, axpy(bd.inv_mass, acc.F, bc3<S>(g)), r.vel());
   V3T<S> w = axpy(h, iw(q, bd.inv_inertia, iso, acc.T), r.ang());
   if (!fp) v = had(bd.mpos, v);
   if (!fr) w = had(bd.mrot, w);
+  const V3T<S> v_pre = v, w_pre = w;
   auto hit = gt(acc.cnt, bc<S>(0.f));
   if (any(hit)) {
     S ic = sel(hit, vdiv(bc<S>(1.f), acc.cnt), bc<S>(0.f));  // R14: mean over the body's active contacts
@@ -583,6 +632,15 @@ template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Ro
   }
   r.set_vel(v);
   r.set_ang(w);
+  if (co) {  // collision integrator's velocity change: after − before (R32)
+    const V3T<S> dv = v - v_pre, dw = w - w_pre;
+    Lanes<S>::st(co, dv.x);
+    Lanes<S>::st(co + E, dv.y);
+    Lanes<S>::st(co + 2 * E, dv.z);
+    Lanes<S>::st(co + 3 * E, dw.x);
+    Lanes<S>::st(co + 4 * E, dw.y);
+    Lanes<S>::st(co + 5 * E, dw.z);
+  }
   if (kin) {  // next substep's kinematic integrator (v, ω already masked)
     r.set_pos(axpy(h, v, r.pos()));
     if (!bd.rot_frozen) {

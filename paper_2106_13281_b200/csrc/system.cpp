@@ -152,6 +152,25 @@ System* build_host(const Config& cfg) {
   hd.mu = float(cfg.friction);
   hd.e = float(cfg.elasticity);
   for (int k = 0; k < 3; ++k) hd.g[k] = float(cfg.gravity[k]);
+  {
+    DTask& t = hd.task;
+    const Task& src = cfg.task;
+    t.present = src.present ? 1 : 0;
+    t.torso = src.torso;
+    t.episode_length = src.episode_length;
+    t.contact_obs = src.contact_obs ? 1 : 0;
+    t.nq = cfg.n_joint_dofs();
+    t.obs_dim = cfg.obs_dim();
+    t.has_healthy = src.has_healthy ? 1 : 0;
+    for (int k = 0; k < 3; ++k) t.fwd[k] = float(src.forward[k]);
+    t.dt = float(cfg.dt);
+    t.survive = float(src.survive_reward);
+    t.ctrl_cost = float(src.ctrl_cost);
+    t.z_lo = float(src.z_lo);
+    t.z_hi = float(src.z_hi);
+    t.noise_vel = float(src.noise_vel);
+    t.noise_ang = float(src.noise_ang);
+  }
 
   std::vector<DBody> bodies(B);
   std::vector<int> dyn;
@@ -182,8 +201,11 @@ System* build_host(const Config& cfg) {
   auto zero3 = [](const float* p) { return p[0] == 0.f && p[1] == 0.f && p[2] == 0.f; };
   auto ident = [](const float* q) { return q[0] == 1.f && q[1] == 0.f && q[2] == 0.f && q[3] == 0.f; };
   hd.off_joints = int32_t(blob.size());
+  int obs_off = 0;
   for (const Joint& j : cfg.joints) {
     DJoint d{};
+    d.obs_off = obs_off;
+    obs_off += j.dof;
     d.parent = j.parent;
     d.child = j.child;
     d.dof = j.dof;
@@ -373,7 +395,8 @@ System* build_host(const Config& cfg) {
 
   for (int pi = 0; pi < kNumPlans; ++pi) {
     DPlan& P = hd.plan[pi];
-    P.smem_bytes = smem_layout(B, J, C, hd.A, P.E, P.V, hd.blob_words).total_words * 4;
+    P.smem_bytes =
+        smem_layout(B, J, C, hd.A, P.E, P.V, hd.blob_words, hd.task.obs_dim, hd.task.contact_obs).total_words * 4;
   }
   s->smem_bytes = size_t(hd.plan[0].smem_bytes);
   if (size_t(hd.plan[0].smem_bytes) > 227 * 1024)
