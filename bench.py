@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--scene", default="ant")
     p.add_argument("--envs", type=int, default=None, help="envs per GPU")
     p.add_argument("--no-graph", action="store_true", help="launch each step from Python instead of a CUDA graph")
+    p.add_argument("--no-env", action="store_true", help="skip the brax_env_step (NEXT-1) measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=200)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -293,6 +294,54 @@ def run_b200(args):
                "h2d_bytes_per_step": int(qp_bytes + n * A * 4), "d2h_bytes_per_step": int(qp_bytes),
                "steps": Ke, "path": "pinned host -> cudaMemcpyAsync -> brax_step -> host, per step"}
 
+    # NEXT-1: the same workload through brax_env_step (reward, done, auto-reset and
+    # observations fused into the step), when the scene has a task block
+    env_line = None
+    tinfo = system.task_info()
+    if tinfo["has_task"] and not args.no_env:
+        od = tinfo["obs_dim"]
+        with torch.cuda.stream(stream):
+            est = []
+            for r in range(R):
+                st = {"steps": torch.zeros(n, dtype=torch.int32, device=dev),
+                      "episode": torch.zeros(n, dtype=torch.int32, device=dev),
+                      "obs": torch.empty((n, od), device=dev), "reward": torch.empty(n, device=dev),
+                      "done": torch.empty(n, dtype=torch.uint8, device=dev)}
+                est.append(st)
+
+            def env_round():
+                for r in range(R):
+                    st = est[r]
+                    bx.brax_env_step(system.handle, sets[r], acts[r] if A else None, 1, sets[r], n, st["obs"],
+                                     st["reward"], st["done"], st["steps"], st["episode"], seed=rank + 1,
+                                     env_offset=rank * n, stream=stream)
+            for _ in range(3):
+                env_round()
+        stream.synchronize()
+        egraph = None
+        if not args.no_graph:
+            egraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(egraph, stream=stream):
+                env_round()
+            stream.synchronize()
+        Kr = max(1, full)
+        with torch.cuda.stream(stream):
+            (egraph.replay() if egraph is not None else env_round())
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(Kr):
+                egraph.replay() if egraph is not None else env_round()
+            e1.record(stream)
+            e1.synchronize()
+        env_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(env_ms, op=dist.ReduceOp.MAX)
+        steps_env = Kr * R
+        env_line = {"value": n * world * steps_env / (float(env_ms[0]) / 1e3), "unit": "env-steps/s",
+                    "ms_per_step": float(env_ms[0]) / steps_env, "steps": steps_env, "obs_dim": od,
+                    "api": "brax_env_step: physics + reward/done/auto-reset/observation epilogue, one launch"}
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -352,6 +401,7 @@ def run_b200(args):
                    "launch": "CUDA graph of brax_step launches" if graph is not None else "eager launches",
                    "kernel_config": system.launch_config(n)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K, "clocks": clocks,
+        "env_epilogue": env_line,
         "blowups": total_blowups,
     }
     print(json.dumps(line), flush=True)

@@ -48,7 +48,7 @@ struct KArgs {
 // S = float: one env per lane; F2: two envs per lane.  R: register budget per
 // thread (instantiated for several budgets; launch_step picks the largest that
 // keeps two blocks resident per SM).
-template <class S, int R>
+template <class S, int R, bool kEnv>
 __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka) {
   extern __shared__ __align__(16) uint32_t smem[];
   const DHeader& H = ka.hd;
@@ -77,7 +77,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   int32_t* sRst = reinterpret_cast<int32_t*>(smem + L.rst);
   float* sCo = reinterpret_cast<float*>(smem + L.co);
   float* sObs = reinterpret_cast<float*>(smem + L.u);
-  const bool envm = a.env != 0;
+  constexpr bool envm = kEnv;  // env epilogue compiled in (a.env != 0) or out
   const bool save_co = envm && T.contact_obs;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -406,18 +406,18 @@ int choose_regs(const System& sys, const DPlan& P, int64_t grid) {
 }
 
 namespace {
-template <class S, int R>
+template <class S, int R, bool kEnv = false>
 cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(brax_step_kernel<S, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(brax_step_kernel<S, R, kEnv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
-  brax_step_kernel<S, R><<<grid, block, smem, stream>>>(ka);
+  brax_step_kernel<S, R, kEnv><<<grid, block, smem, stream>>>(ka);
   return cudaGetLastError();
 }
 
@@ -432,6 +432,15 @@ cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs
   const DPlan& P = sys.hd.plan[plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(P.smem_bytes);
+  if (a.env) {  // env-epilogue instantiations (fewer register variants)
+    if (P.V == 2) {
+      if (regs >= 128) return launch_variant<F2, 128, true>(ka, grid, block, smem, stream);
+      return launch_variant<F2, 96, true>(ka, grid, block, smem, stream);
+    }
+    if (regs >= 128) return launch_variant<F1, 128, true>(ka, grid, block, smem, stream);
+    if (regs >= 96) return launch_variant<F1, 96, true>(ka, grid, block, smem, stream);
+    return launch_variant<F1, 64, true>(ka, grid, block, smem, stream);
+  }
   if (P.V == 2) {
     if (regs >= 128) return launch_variant<F2, 128>(ka, grid, block, smem, stream);
     if (regs >= 96) return launch_variant<F2, 96>(ka, grid, block, smem, stream);

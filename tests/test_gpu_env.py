@@ -106,7 +106,7 @@ def test_env_step_matches_oracle(name):
         got = st["qp"][k].cpu().numpy()
         assert np.max(np.abs(got[keep] - ref["qp"][k][keep])) < TOL, k
     obs = out["obs"][0].cpu().numpy()
-    assert np.max(np.abs(obs[keep] - ref["obs"][keep])) < 10 * TOL
+    assert np.max(np.abs(obs[keep] - ref["obs"][keep])) < TOL
 
 
 def test_env_rollout_equals_single_steps_and_plans_agree():
