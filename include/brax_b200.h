@@ -183,6 +183,20 @@ brax_status brax_step_ex(const brax_system *sys, brax_qp in, const float *action
 brax_status brax_rollout(const brax_system *sys, brax_qp in, const float *actions, int64_t n_steps, brax_qp out,
                          int64_t n_envs, const brax_step_extras *extras, void *stream);
 
+/* ---- NEXT-2: on-device random actions (no action buffer in HBM).  Step t of the
+ * launch (global step step0 + t) of env i uses, for action component k,
+ *   a_k = (x_(k mod 4) >> 8)·2⁻²³ − 1 ∈ [−1, 1),  x = Philox4x32-10(key = seed,
+ *   counter = (env_offset + i, step0 + t, ⌊k/4⌋, 0x41435431)),
+ * the same generator as the reset noise (separate counter space). */
+typedef struct {
+  uint64_t seed;
+  int64_t env_offset;  /* global index of env 0 of this batch */
+  int64_t step0;       /* global step index of the launch's first step */
+} brax_random_actions;
+/* brax_rollout with on-device random actions. */
+brax_status brax_rollout_random(const brax_system *sys, brax_qp in, int64_t n_steps, brax_qp out, int64_t n_envs,
+                                const brax_random_actions *ra, const brax_step_extras *extras, void *stream);
+
 /* ---- NEXT-1: Gym-like env epilogue fused into the step (Table 1;
  * :505-509 rewards; R30-R35).  Needs a `task { ... }` block in the system
  * text.  Per step and env, after the last substep and while the bodies are still
@@ -209,6 +223,9 @@ brax_status brax_system_task_info(const brax_system *sys, int32_t out[4]);
  * BRAX_E_INVALID_ARGUMENT if the system has no task or steps / episode are NULL. */
 brax_status brax_env_step(const brax_system *sys, brax_qp in, const float *actions, int64_t n_steps, brax_qp out,
                           int64_t n_envs, const brax_env_io *io, void *stream);
+/* brax_env_step with on-device random actions (NEXT-2; ctrl cost uses them). */
+brax_status brax_env_step_random(const brax_system *sys, brax_qp in, int64_t n_steps, brax_qp out, int64_t n_envs,
+                                 const brax_random_actions *ra, const brax_env_io *io, void *stream);
 /* Episode-0 reset (the task's reset noise, Philox counter (env_offset + env, b, f, 0)),
  * steps = episode = 0, and io->obs (if not NULL). */
 brax_status brax_env_reset(const brax_system *sys, brax_qp out, int64_t n_envs, const brax_env_io *io,

@@ -67,3 +67,24 @@ def reset_qp(sys, dqp, n: int, seed: int, vel_noise: float, ang_noise: float, *,
                 out["ang"][e, b, k] += (1.0 - body.frozen_rot[k]) * ang_noise * uniform_pm1(xw[k])
     assert out["pos"].shape == (n, B, 3)
     return out
+
+
+ACT_TAG = 0x41435431  # "ACT1"
+
+
+def random_actions(n: int, act_dim: int, n_steps: int, seed: int, env_offset: int = 0, step0: int = 0):
+    """NEXT-2 on-device random actions (include/brax_b200.h brax_random_actions):
+    a[t, i, k] = u(x_(k mod 4)), x = Philox4x32-10(key = seed, counter =
+    (env_offset + i, step0 + t, k // 4, ACT_TAG)); returns [n_steps, n, act_dim] fp64
+    (every value is exactly representable in fp32)."""
+    seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    key = (seed & MASK, seed >> 32)
+    out = np.zeros((n_steps, n, act_dim))
+    for t in range(n_steps):
+        for i in range(n):
+            for g in range((act_dim + 3) // 4):
+                x = philox4x32_10(((env_offset + i) & MASK, (step0 + t) & MASK, g, ACT_TAG), key)
+                for j in range(4):
+                    if 4 * g + j < act_dim:
+                        out[t, i, 4 * g + j] = uniform_pm1(x[j])
+    return out

@@ -25,6 +25,7 @@ __all__ = [
     "brax_system_get_info", "brax_system_slot_table", "brax_default_qp", "brax_reset", "brax_step",
     "brax_step_ex", "brax_rollout", "brax_qp", "brax_step_extras", "brax_system_info", "LIB_PATH", "lib",
     "brax_env_io", "brax_system_task_info", "brax_env_step", "brax_env_reset", "brax_env_observe",
+    "brax_random_actions", "brax_rollout_random", "brax_env_step_random",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbrax_b200.so")
@@ -59,6 +60,10 @@ class brax_env_io(C.Structure):
                 ("episode", C.c_void_p), ("seed", C.c_uint64), ("env_offset", C.c_int64)]
 
 
+class brax_random_actions(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("env_offset", C.c_int64), ("step0", C.c_int64)]
+
+
 class brax_system_info(C.Structure):
     _fields_ = [("n_bodies", C.c_int32), ("n_dynamic", C.c_int32), ("n_joints", C.c_int32),
                 ("act_dim", C.c_int32), ("n_contact_slots", C.c_int32), ("substeps", C.c_int32),
@@ -89,6 +94,10 @@ _SIGS = {
     "brax_step_ex": ([_P, brax_qp, _P, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_rollout": ([_P, brax_qp, _P, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_system_task_info": ([_P, _i32p], C.c_int),
+    "brax_rollout_random": ([_P, brax_qp, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_random_actions),
+                             C.POINTER(brax_step_extras), _P], C.c_int),
+    "brax_env_step_random": ([_P, brax_qp, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_random_actions),
+                              C.POINTER(brax_env_io), _P], C.c_int),
     "brax_env_step": ([_P, brax_qp, _P, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_env_io), _P], C.c_int),
     "brax_env_reset": ([_P, brax_qp, C.c_int64, C.POINTER(brax_env_io), _P], C.c_int),
     "brax_env_observe": ([_P, brax_qp, C.c_int64, _P, _P], C.c_int),
@@ -227,6 +236,23 @@ def _env_io(obs, reward, done, steps, episode, seed, env_offset):
                        int(seed) & 0xFFFFFFFFFFFFFFFF, int(env_offset))
 
 
+def brax_rollout_random(sys: int, qp_in, n_steps: int, qp_out, n_envs: int, seed: int, env_offset: int = 0,
+                        step0: int = 0, status=None, contact_active=None, stream=None) -> None:
+    ra = brax_random_actions(int(seed) & 0xFFFFFFFFFFFFFFFF, int(env_offset), int(step0))
+    x = _extras(status, contact_active)
+    _check(lib.brax_rollout_random(sys, _qp(qp_in), n_steps, _qp(qp_out), n_envs, C.byref(ra),
+                                   None if x is None else C.byref(x), _stream(stream)))
+
+
+def brax_env_step_random(sys: int, qp_in, n_steps: int, qp_out, n_envs: int, obs, reward, done, steps, episode,
+                         seed: int = 0, env_offset: int = 0, act_seed: int = 0, step0: int = 0,
+                         stream=None) -> None:
+    io = _env_io(obs, reward, done, steps, episode, seed, env_offset)
+    ra = brax_random_actions(int(act_seed) & 0xFFFFFFFFFFFFFFFF, int(env_offset), int(step0))
+    _check(lib.brax_env_step_random(sys, _qp(qp_in), n_steps, _qp(qp_out), n_envs, C.byref(ra), C.byref(io),
+                                    _stream(stream)))
+
+
 def brax_system_task_info(sys: int):
     out = (C.c_int32 * 4)()
     _check(lib.brax_system_task_info(sys, out))
@@ -361,6 +387,14 @@ class System:
         brax_env_step(self._sys, state["qp"], actions, T, state["qp"], n, out["obs"], out["reward"], out["done"],
                       state["steps"], state["episode"], seed, env_offset, stream)
         return out
+
+    def rollout_random(self, qp_in, n_steps: int, qp_out=None, *, seed: int = 0, env_offset: int = 0,
+                       step0: int = 0, status=None, contact_active=None, stream=None):
+        """n_steps steps in one launch with on-device random actions (NEXT-2)."""
+        qp_out = qp_in if qp_out is None else qp_out
+        brax_rollout_random(self._sys, qp_in, n_steps, qp_out, qp_in["pos"].shape[0], seed, env_offset, step0,
+                            status, contact_active, stream)
+        return qp_out
 
     def env_observe(self, qp, stream=None):
         import torch

@@ -49,7 +49,7 @@ brax_status cuda_status(cudaError_t e, const char* what) {
 
 brax_status step_common(const brax_system* sys, brax_qp in, const float* actions, int64_t n_steps, brax_qp out,
                         int64_t n_envs, const brax_step_extras* x, void* stream, const brax_env_io* io = nullptr,
-                        float* observe_only = nullptr) {
+                        float* observe_only = nullptr, const brax_random_actions* ra = nullptr) {
   if (!sys || !sys->impl) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
   if (n_envs < 0 || n_steps < 0) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs and n_steps must be >= 0");
   const bool env = io != nullptr || observe_only != nullptr;
@@ -61,7 +61,9 @@ brax_status step_common(const brax_system* sys, brax_qp in, const float* actions
   if (st != BRAX_OK) return st;
   if ((st = check_qp(out, "out")) != BRAX_OK) return st;
   const brax::System& s = *sys->impl;
-  if (s.hd.A > 0 && !actions && !observe_only) return fail(BRAX_E_INVALID_ARGUMENT, "action is NULL but act_dim > 0");
+  if (s.hd.A > 0 && !actions && !observe_only && !ra)
+    return fail(BRAX_E_INVALID_ARGUMENT, "action is NULL but act_dim > 0");
+  if (ra && actions) return fail(BRAX_E_INVALID_ARGUMENT, "give either actions or random actions");
   if (actions && !aligned16(actions)) return fail(BRAX_E_MISALIGNED, "action must be 16-byte aligned");
   // aliasing: identical (in == out for all four arrays) is fine, any other overlap is not
   const float* ins[4] = {in.pos, in.rot, in.vel, in.ang};
@@ -87,6 +89,12 @@ brax_status step_common(const brax_system* sys, brax_qp in, const float* actions
   brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, out.pos, out.rot, out.vel, out.ang, actions,
                    x ? x->status : nullptr, x ? x->contact_active : nullptr, n_envs, n_steps, 0, 0, nullptr};
   if (a.contact_active && s.hd.C == 0) a.contact_active = nullptr;
+  if (ra && s.hd.A > 0) {
+    a.act_random = 1;
+    a.act_seed = ra->seed;
+    a.act_env_offset = ra->env_offset;
+    a.act_step0 = ra->step0;
+  }
   if (env) {
     a.env = 1;
     a.dqp = s.d_default_qp;
@@ -298,6 +306,18 @@ brax_status brax_step_ex(const brax_system* sys, brax_qp in, const float* action
 brax_status brax_rollout(const brax_system* sys, brax_qp in, const float* actions, int64_t n_steps, brax_qp out,
                          int64_t n_envs, const brax_step_extras* extras, void* stream) {
   return step_common(sys, in, actions, n_steps, out, n_envs, extras, stream);
+}
+
+brax_status brax_rollout_random(const brax_system* sys, brax_qp in, int64_t n_steps, brax_qp out, int64_t n_envs,
+                                const brax_random_actions* ra, const brax_step_extras* extras, void* stream) {
+  if (!ra) return fail(BRAX_E_INVALID_ARGUMENT, "ra is NULL");
+  return step_common(sys, in, nullptr, n_steps, out, n_envs, extras, stream, nullptr, nullptr, ra);
+}
+
+brax_status brax_env_step_random(const brax_system* sys, brax_qp in, int64_t n_steps, brax_qp out, int64_t n_envs,
+                                 const brax_random_actions* ra, const brax_env_io* io, void* stream) {
+  if (!ra || !io) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
+  return step_common(sys, in, nullptr, n_steps, out, n_envs, nullptr, stream, io, nullptr, ra);
 }
 
 brax_status brax_system_task_info(const brax_system* sys, int32_t out[4]) {

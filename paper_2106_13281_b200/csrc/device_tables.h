@@ -168,7 +168,13 @@ struct StepArgs {
   int64_t env_offset;          // global index of env 0 (Philox counter)
   const float* dqp;            // default_qp: pos [B][3] | rot [B][4]
   const float* masks;          // per body: mpos[3] mrot[3] static
+  // NEXT-2 on-device random actions (actions == NULL): a_k = u(Philox(key = act_seed,
+  // counter = (act_env_offset + env, act_step0 + step, k/4, kActTag)))_(k mod 4) ∈ [−1, 1)
+  int32_t act_random;
+  uint64_t act_seed;
+  int64_t act_env_offset, act_step0;
 };
+constexpr uint32_t kActTag = 0x41435431u;  // "ACT1": separates the action stream from the reset stream
 
 // A work plan for one lane-group count G (E = 32/G envs per block): each warp's
 // lanes form G groups of E lanes; group g runs item items[step*G + g] on the

@@ -221,6 +221,16 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         const int env = i / A, k = i - env * A;
         sA[k * E + eslot<V>(env, E)] = sAstg[i];
       }
+    } else if (a.act_random) {  // NEXT-2: this step's actions from the counter-based generator
+      const uint2 key = make_uint2(uint32_t(a.act_seed & 0xffffffffu), uint32_t(a.act_seed >> 32));
+      const int A4 = (A + 3) >> 2;
+      const uint32_t t = uint32_t(a.act_step0 + step);
+      for (int i = tid; i < E * A4; i += blockDim.x) {
+        const int env = i / A4, g = i - env * A4;
+        const uint4 x = philox4x32_10(make_uint4(uint32_t(a.act_env_offset + e0 + env), t, uint32_t(g), kActTag), key);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        for (int j = 0; j < 4 && 4 * g + j < A; ++j) sA[(4 * g + j) * E + eslot<V>(env, E)] = u_pm1(xs[j]);
+      }
     } else {
       load_actions<V>(a, sA, A, E, step, e0, nvalid);
     }  // sA is read in phase 2, after a barrier

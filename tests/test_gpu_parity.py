@@ -314,3 +314,32 @@ def test_autotune_picks_a_plan_without_touching_inputs():
     got = host(out)
     for k in FIELDS:
         assert np.array_equal(got[k], ref[k]), k
+
+
+def test_rollout_random_actions_match_the_oracle_generator():
+    """NEXT-2: on-device Philox actions are bit-identical to oracle.philox's
+    stream (so the rollout equals one fed those actions from HBM), and the env
+    epilogue variant too."""
+    from oracle.philox import random_actions
+    o, s = scene("ant")
+    n, T = 333, 4
+    qp = trajectory_states(o, n, seed=61, T0=0)
+    acts = random_actions(n, o.act_dim, T, seed=99, env_offset=5, step0=7).astype(np.float32)
+    a = dev(qp)
+    s.rollout_random(a, T, seed=99, env_offset=5, step0=7)
+    b = dev(qp)
+    s.rollout(b, torch.from_numpy(acts).cuda())
+    for k in FIELDS:
+        assert torch.equal(a[k], b[k]), k
+    st1 = s.env_state(n)
+    s.env_reset(st1, seed=1)
+    st2 = {"qp": {k: v.clone() for k, v in st1["qp"].items()}, "steps": st1["steps"].clone(),
+           "episode": st1["episode"].clone()}
+    od = s.task_info()["obs_dim"]
+    out = {"obs": torch.empty((T, n, od), device="cuda"), "reward": torch.empty((T, n), device="cuda"),
+           "done": torch.empty((T, n), dtype=torch.uint8, device="cuda")}
+    bx.brax_env_step_random(s.handle, st1["qp"], T, st1["qp"], n, out["obs"], out["reward"], out["done"],
+                            st1["steps"], st1["episode"], seed=1, env_offset=5, act_seed=99, step0=7)
+    ref = s.env_step(st2, torch.from_numpy(acts).cuda(), seed=1, env_offset=5)
+    for key in ("obs", "reward", "done"):
+        assert torch.equal(out[key], ref[key]), key

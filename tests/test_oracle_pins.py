@@ -641,3 +641,19 @@ def test_op_counts_ant():
     per = fl / 4
     assert 30e3 < per < 90e3
     assert mu > 0
+
+
+def test_random_action_stream():
+    """NEXT-2 action generator: values in [−1, 1) on the 2⁻²³ grid, the counter
+    layout (env, step, k // 4, tag) of the header, distinct per env and step,
+    and a disjoint counter space from the reset noise (tag word)."""
+    from oracle.philox import ACT_TAG, random_actions, uniform_pm1
+    a = random_actions(5, 6, 3, seed=2 ** 40 + 7, env_offset=10, step0=100)
+    assert a.shape == (3, 5, 6) and np.all(a >= -1) and np.all(a < 1)
+    assert np.array_equal(a * 2 ** 23, np.round(a * 2 ** 23))
+    key = ((2 ** 40 + 7) & 0xFFFFFFFF, (2 ** 40 + 7) >> 32)
+    x = philox4x32_10((12, 101, 1, ACT_TAG), key)
+    assert a[1, 2, 4] == uniform_pm1(x[0]) and a[1, 2, 5] == uniform_pm1(x[1])
+    assert len(np.unique(a.reshape(-1))) == a.size
+    b = random_actions(5, 6, 3, seed=2 ** 40 + 7, env_offset=11, step0=100)
+    assert np.array_equal(a[:, 1:], b[:, :-1])  # env ids are global
