@@ -110,10 +110,13 @@ struct SmemLayout {
   int32_t blob, q, u, a, astg, cnt, stat, x0, steps, ep, rst, co, total_words;
 };
 BRAX_HD inline int32_t round4(int32_t w) { return (w + 3) & ~3; }
-BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A, int32_t E, int32_t V,
-                                      int32_t blob_words, int32_t obs_dim, int32_t contact_obs) {
+// E envs per block in LG lane slots; paired: two values per slot (V = 2 envs, or
+// value + tangent of the JVP step); RW: words per row of a per-env array (actions,
+// contact counts, contact Δv): LG·(paired ? 2 : 1).
+BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A, int32_t E, int32_t LG,
+                                      int32_t paired, int32_t blob_words, int32_t obs_dim, int32_t contact_obs) {
   SmemLayout L;
-  const int32_t LG = E / V;
+  const int32_t V = paired ? 2 : 1, RW = LG * V;
   L.blob = 4;
   L.q = L.blob + round4(blob_words);
   L.u = L.q + B * LG * rec_q(V);
@@ -121,16 +124,16 @@ BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A
   if (u < E * B * 13) u = E * B * 13;
   if (u < E * obs_dim) u = E * obs_dim;
   L.a = L.u + round4(u);
-  L.astg = L.a + round4(A * E);
+  L.astg = L.a + round4(A * RW);
   L.cnt = L.astg + round4(A * E);
-  L.stat = L.cnt + round4(C * E);
+  L.stat = L.cnt + round4(C * RW);
   L.x0 = L.stat + round4(E);
   const int32_t env = obs_dim > 0 ? 1 : 0;
   L.steps = L.x0 + env * round4(3 * E);
   L.ep = L.steps + env * round4(E);
   L.rst = L.ep + env * round4(E);
   L.co = L.rst + env * round4(E);
-  L.total_words = L.co + env * (contact_obs ? round4(6 * B * E) : 0);
+  L.total_words = L.co + env * (contact_obs ? round4(6 * B * RW) : 0);
   return L;
 }
 
@@ -185,7 +188,7 @@ struct DPlan {
   int32_t G, V, E, W;  // lane groups per warp, envs per lane, envs per block E = 32·V/G, warps
   int32_t off_item_begin, off_items;          // per warp: item steps [begin, end); items[step*G + g]
   int32_t off_body_begin, off_bodies_of_warp;  // per warp: body steps; bodies[step*G + g]
-  int32_t smem_bytes, pad0, pad1, pad2;
+  int32_t smem_bytes, smem_bytes_jvp, pad1, pad2;  // jvp: value + tangent records (V = 1 plans)
 };
 
 struct DHeader {            // passed by value as a kernel argument

@@ -54,15 +54,18 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const DHeader& H = ka.hd;
   const DPlan& P = H.plan[ka.plan];
   const StepArgs& a = ka.a;
-  constexpr int V = Lanes<S>::V, QS = Lanes<S>::QS, JS = Lanes<S>::JS, CS = Lanes<S>::CS;
+  // V: layout id of the lane type (1: F1, 2: F2 env pairs, 3: D1 value/tangent pairs);
+  // SL: words per lane slot in per-env arrays; RW = LG·SL: their row width
+  constexpr int V = Lanes<S>::V, SL = Lanes<S>::SL, QS = Lanes<S>::QS, JS = Lanes<S>::JS, CS = Lanes<S>::CS;
   const int B = H.B, J = H.J, C = H.C, A = H.A, E = P.E, G = P.G;
   const DTask& T = H.task;
-  const SmemLayout L = smem_layout(B, J, C, A, E, V, H.blob_words, T.obs_dim, T.contact_obs);
+  const int LG = 32 / G;  // lanes per group = records per item
+  const int RW = LG * SL;
+  const SmemLayout L = smem_layout(B, J, C, A, E, LG, SL == 2, H.blob_words, kEnv ? T.obs_dim : 0, T.contact_obs);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [0] tables + QP, [1] actions
   uint32_t* sBlob = smem + L.blob;
   float* sQ = reinterpret_cast<float*>(smem + L.q);
   float* sJ = reinterpret_cast<float*>(smem + L.u);
-  const int LG = 32 / G;  // lanes per group = records per item (E = LG·V envs)
   float* sC = sJ + J * LG * JS;
   float* stg = reinterpret_cast<float*>(smem + L.u);  // aliases sJ/sC outside the substeps
   float* sA = reinterpret_cast<float*>(smem + L.a);
@@ -134,7 +137,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       sEp[i] = i < nvalid && a.episode ? a.episode[e0 + i] : 0u;
     }
     if (save_co)
-      for (int i = tid; i < 6 * B * E; i += blockDim.x) sCo[i] = 0.f;
+      for (int i = tid; i < 6 * B * RW; i += blockDim.x) sCo[i] = 0.f;
   }
   __syncthreads();
   lap(0);
@@ -159,7 +162,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   // ---- NEXT-1 env epilogue pieces (R30-R35; per-env scalar code spells out its rounding) ----
   auto save_x0 = [&]() {  // torso position at the step boundary (before S2)
     for (int i = tid; i < E; i += blockDim.x)
-      for (int k = 0; k < 3; ++k) sX0[3 * i + k] = sQ[qword<V>(T.torso, i, 0, k, E)];
+      for (int k = 0; k < 3; ++k) sX0[3 * i + k] = sQ[qword<V>(T.torso, i, 0, k, LG)];
   };
   auto observe = [&](float* obs_out) {  // obs rows of the block's envs -> obs_out [nvalid][od]
     // joints: angles and rates, by the warps that own them
@@ -179,11 +182,11 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       if (k < 11) {
         const int f = k == 0 ? 0 : k < 5 ? 1 : k < 8 ? 2 : 3;
         const int c = k == 0 ? 2 : k < 5 ? k - 1 : k < 8 ? k - 5 : k - 8;
-        v = sQ[qword<V>(T.torso, env, f, c, E)];
+        v = sQ[qword<V>(T.torso, env, f, c, LG)];
         at = k < 5 ? k : 5 + T.nq + (k - 5);
       } else {
         const int b = (k - 11) / 6, kk = (k - 11) - 6 * b;
-        v = fminf(fmaxf(sCo[(b * 6 + kk) * E + eslot<V>(env, E)], -1.f), 1.f);
+        v = fminf(fmaxf(sCo[(b * 6 + kk) * RW + eslot<V>(env, LG)], -1.f), 1.f);
         at = 11 + 2 * T.nq + (k - 11);
       }
       sObs[env * od + at] = v;
@@ -219,7 +222,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       mbar_wait(&bars[1], uint32_t(step & 1));
       for (int i = tid; i < E * A; i += blockDim.x) {
         const int env = i / A, k = i - env * A;
-        sA[k * E + eslot<V>(env, E)] = sAstg[i];
+        sA[k * RW + eslot<V>(env, LG)] = sAstg[i];
       }
     } else if (a.act_random) {  // NEXT-2: this step's actions from the counter-based generator
       const uint2 key = make_uint2(uint32_t(a.act_seed & 0xffffffffu), uint32_t(a.act_seed >> 32));
@@ -229,16 +232,15 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         const int env = i / A4, g = i - env * A4;
         const uint4 x = philox4x32_10(make_uint4(uint32_t(a.act_env_offset + e0 + env), t, uint32_t(g), kActTag), key);
         const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-        for (int j = 0; j < 4 && 4 * g + j < A; ++j) sA[(4 * g + j) * E + eslot<V>(env, E)] = u_pm1(xs[j]);
+        for (int j = 0; j < 4 && 4 * g + j < A; ++j) sA[(4 * g + j) * RW + eslot<V>(env, LG)] = u_pm1(xs[j]);
       }
     } else {
-      load_actions<V>(a, sA, A, E, step, e0, nvalid);
+      load_actions<V>(a, sA, A, E, LG, step, e0, nvalid);
     }  // sA is read in phase 2, after a barrier
     for (int it = it0; it < it1; ++it) {
       int item = items[it * G];
       if (item >= J) {
-        sCnt[(item - J) * E + el] = 0.f;
-        if (LG != E) sCnt[(item - J) * E + el + LG] = 0.f;
+        for (int k = 0; k < SL; ++k) sCnt[(item - J) * RW + el * SL + k] = 0.f;
       }
     }
     for (int s = 0; s < H.S; ++s) {
@@ -253,12 +255,12 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         if (item < 0) continue;
         if (item < J) {
           const DJoint& jt = joints[item];
-          joint<S>(jt, Row<S>{sQ + (jt.parent * LG + el) * QS}, Row<S>{sQ + (jt.child * LG + el) * QS}, sA + el * V,
-                   E, sJ + (item * LG + el) * JS);
+          joint<S>(jt, Row<S>{sQ + (jt.parent * LG + el) * QS}, Row<S>{sQ + (jt.child * LG + el) * QS}, sA + el * SL,
+                   RW, sJ + (item * LG + el) * JS);
         } else {
           int c = item - J;
           const DSlot& sl = slots[c];
-          float* cp = sCnt + c * E + el * V;
+          float* cp = sCnt + c * RW + el * SL;
           S cnt = Lanes<S>::ld(cp);
           contact<S>(sl, Row<S>{sQ + (sl.a * LG + el) * QS}, Row<S>{sQ + (sl.b * LG + el) * QS}, 1.f + H.e,
                      H.beta_over_h, H.mu, sC + (c * LG + el) * CS, cnt);
@@ -284,7 +286,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         const bool last = s + 1 == H.S;
         const bool kin = !(last && (envm || step + 1 == a.n_steps));  // fused S2 of the next substep
         integrate<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, acc, H.h, H.g, kin,
-                     save_co && last ? sCo + b * 6 * E + el * V : nullptr, E);
+                     save_co && last ? sCo + b * 6 * RW + el * SL : nullptr, RW);
       }
     }
     if (envm) {
@@ -292,13 +294,13 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       // reward, done, step / episode counters (one thread per env)
       for (int i = tid; i < E; i += blockDim.x) {
         float x1[3];
-        for (int k = 0; k < 3; ++k) x1[k] = sQ[qword<V>(T.torso, i, 0, k, E)];
+        for (int k = 0; k < 3; ++k) x1[k] = sQ[qword<V>(T.torso, i, 0, k, LG)];
         float fwd = __fmul_rn(__fadd_rn(x1[0], -sX0[3 * i]), T.fwd[0]);
         fwd = __fmaf_rn(__fadd_rn(x1[1], -sX0[3 * i + 1]), T.fwd[1], fwd);
         fwd = __fmaf_rn(__fadd_rn(x1[2], -sX0[3 * i + 2]), T.fwd[2], fwd);
         float ctrl = 0.f;
         for (int k = 0; k < A; ++k) {
-          const float u = sA[k * E + eslot<V>(i, E)];
+          const float u = sA[k * RW + eslot<V>(i, LG)];
           ctrl = __fmaf_rn(u, u, ctrl);
         }
         const float reward = __fadd_rn(__fadd_rn(__fdiv_rn(fwd, T.dt), T.survive), -__fmul_rn(T.ctrl_cost, ctrl));
@@ -323,13 +325,13 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         reset_body(a.dqp, a.masks, B, b, uint32_t(a.env_offset + e0 + env), sEp[env], key, T.noise_vel,
                    T.noise_ang, x, q, v, w);
         for (int k = 0; k < 3; ++k) {
-          sQ[qword<V>(b, env, 0, k, E)] = x[k];
-          sQ[qword<V>(b, env, 2, k, E)] = v[k];
-          sQ[qword<V>(b, env, 3, k, E)] = w[k];
+          sQ[qword<V>(b, env, 0, k, LG)] = x[k];
+          sQ[qword<V>(b, env, 2, k, LG)] = v[k];
+          sQ[qword<V>(b, env, 3, k, LG)] = w[k];
         }
-        for (int k = 0; k < 4; ++k) sQ[qword<V>(b, env, 1, k, E)] = q[k];
+        for (int k = 0; k < 4; ++k) sQ[qword<V>(b, env, 1, k, LG)] = q[k];
         if (save_co)
-          for (int k = 0; k < 6; ++k) sCo[(b * 6 + k) * E + eslot<V>(env, E)] = 0.f;
+          for (int k = 0; k < 6; ++k) sCo[(b * 6 + k) * RW + eslot<V>(env, LG)] = 0.f;
       }
       __syncthreads();
       if (a.obs) observe(a.obs + (step * a.n_envs + e0) * od);
@@ -344,7 +346,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   lap(2);
   __syncthreads();
   // S9: status bits, contact counts, and the single write-back of the QP (TMA bulk for full blocks)
-  block_extras<V>(a, sQ, sCnt, sStat, B, C, E, e0, nvalid);
+  block_extras<V>(a, sQ, sCnt, sStat, B, C, E, LG, e0, nvalid);
   if (bulk) {
     records_to_stg<V>(sQ, stg, B, E);
     fence_proxy_async();

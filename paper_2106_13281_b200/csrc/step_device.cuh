@@ -245,7 +245,7 @@ template <class S> __device__ __forceinline__ S asin_f(S x) {
 // (c0 env0, c0 env1, c1 env0, c1 env1 | c2 env0, c2 env1, c3 env0, c3 env1).
 template <class S> struct Lanes;
 template <> struct Lanes<F1> {
-  static constexpr int V = 1, M = 4;  // envs per lane, words per record field
+  static constexpr int V = 1, SL = 1, M = 4;  // layout id, words per lane slot, words per record field
   static constexpr int QS = kQS, JS = kJS, CS = kCS;
   static __device__ __forceinline__ V3T<F1> ld3(const float* p) {
     float4 a = *reinterpret_cast<const float4*>(p);
@@ -266,7 +266,7 @@ template <> struct Lanes<F1> {
   static __device__ __forceinline__ F1 w4(const float* p) { return {p[3]}; }  // 4th word of field 0
 };
 template <> struct Lanes<F2> {
-  static constexpr int V = 2, M = 8;
+  static constexpr int V = 2, SL = 2, M = 8;
   static constexpr int QS = kQS2, JS = kJS2, CS = kCS2;
   static __device__ __forceinline__ V3T<F2> ld3(const float* p) {
     float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
@@ -655,17 +655,21 @@ template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Ro
   }
 }
 
-// Word of (body b, env slot env, field f, component c) in the QP records (V envs per lane).
-template <int V> __device__ __forceinline__ int qword(int b, int env, int f, int c, int E) {
-  if (V == 1) return (b * E + env) * kQS + 4 * f + c;
-  const int LG = E >> 1, h = env >= LG ? 1 : 0, el = env - h * LG;
+// Word of (body b, env slot env, field f, component c) in the QP records for layout
+// V (1: F1; 2: F2, envs el and el + LG share lane el's record; 3: D1, value half of
+// the env's value/tangent record) with LG records per body.
+template <int V> __device__ __forceinline__ int qword(int b, int env, int f, int c, int LG) {
+  if (V == 1) return (b * LG + env) * kQS + 4 * f + c;
+  const int h = (V == 2 && env >= LG) ? 1 : 0, el = env - h * LG;
   return (b * LG + el) * kQS2 + 8 * f + 4 * (c >> 1) + 2 * (c & 1) + h;
 }
-// Position of env slot `env` in a per-env row of E words (actions, contact counts):
-// V = 2 keeps a lane's two envs (el, el + E/2) adjacent.
-template <int V> __device__ __forceinline__ int eslot(int env, int E) {
+// Position of env slot `env` in a per-env row (actions, contact counts, contact Δv):
+// V = 2 keeps a lane's two envs (el, el + LG) adjacent; V = 3 (D1) the value word of
+// the env's (value, tangent) pair.
+template <int V> __device__ __forceinline__ int eslot(int env, int LG) {
   if (V == 1) return env;
-  const int LG = E >> 1, h = env >= LG ? 1 : 0;
+  if (V == 3) return 2 * env;
+  const int h = env >= LG ? 1 : 0;
   return 2 * (env - h * LG) + h;
 }
 
@@ -681,7 +685,7 @@ __device__ __forceinline__ void stage(const float* gin, float* gout, float* sQ, 
     const int64_t g0 = (e0 + env) * row_len;
     for (int k = lane; k < row_len; k += 32) {
       const int b = k / K, c = k - (k / K) * K;
-      float* s = sQ + qword<V>(b, env, f, c, E);
+      float* s = sQ + qword<V>(b, env, f, c, V == 2 ? E / 2 : E);
       if (kLoad) *s = __ldg(gin + g0 + k);
       else gout[g0 + k] = *s;
     }
@@ -818,21 +822,23 @@ __device__ __forceinline__ void load_block(const StepArgs& a, float* sQ, int B, 
 
 // S1 (per step): this step's action [n][A] -> sA[k][eslot(env)] (one env row per warp iteration)
 template <int V>
-__device__ __forceinline__ void load_actions(const StepArgs& a, float* sA, int A, int E, int64_t step, int64_t e0,
-                                             int nvalid) {
+__device__ __forceinline__ void load_actions(const StepArgs& a, float* sA, int A, int E, int LG, int64_t step,
+                                             int64_t e0, int nvalid) {
   if (A <= 0) return;
+  const int RW = V == 1 ? LG : 2 * LG;
   const float* act = a.actions + (step * a.n_envs + e0) * A;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int env = warp; env < nvalid; env += nw) {
-    const int slot = eslot<V>(env, E);
-    for (int k = lane; k < A; k += 32) sA[k * E + slot] = __ldg(act + env * A + k);
+    const int slot = eslot<V>(env, LG);
+    for (int k = lane; k < A; k += 32) sA[k * RW + slot] = __ldg(act + env * A + k);
   }
 }
 
 // S9: status bits and contact counts (after a barrier)
 template <int V>
 __device__ __forceinline__ void block_extras(const StepArgs& a, const float* sQ, const float* sCnt, uint32_t* sStat,
-                                             int B, int C, int E, int64_t e0, int nvalid) {
+                                             int B, int C, int E, int LG, int64_t e0, int nvalid) {
+  const int RW = V == 1 ? LG : 2 * LG;
   auto word_bits = [](float v) -> uint32_t { return isfinite(v) ? (fabsf(v) > 1e6f ? 2u : 0u) : 1u; };
   if (a.status) {
     if (V == 1) {
@@ -866,7 +872,7 @@ __device__ __forceinline__ void block_extras(const StepArgs& a, const float* sQ,
   if (a.contact_active) {
     for (int i = threadIdx.x; i < nvalid * C; i += blockDim.x) {
       int env = i / C, c = i - env * C;
-      a.contact_active[(e0 + env) * C + c] = uint8_t(sCnt[c * E + eslot<V>(env, E)]);
+      a.contact_active[(e0 + env) * C + c] = uint8_t(sCnt[c * RW + eslot<V>(env, LG)]);
     }
   }
 }

@@ -395,8 +395,10 @@ System* build_host(const Config& cfg) {
 
   for (int pi = 0; pi < kNumPlans; ++pi) {
     DPlan& P = hd.plan[pi];
-    P.smem_bytes =
-        smem_layout(B, J, C, hd.A, P.E, P.V, hd.blob_words, hd.task.obs_dim, hd.task.contact_obs).total_words * 4;
+    const int LG = P.E / P.V;
+    P.smem_bytes = smem_layout(B, J, C, hd.A, P.E, LG, P.V == 2, hd.blob_words, hd.task.obs_dim,
+                               hd.task.contact_obs).total_words * 4;
+    P.smem_bytes_jvp = P.V == 1 ? smem_layout(B, J, C, hd.A, P.E, LG, 1, hd.blob_words, 0, 0).total_words * 4 : 0;
   }
   s->smem_bytes = size_t(hd.plan[0].smem_bytes);
   if (size_t(hd.plan[0].smem_bytes) > 227 * 1024)
