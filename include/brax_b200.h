@@ -197,6 +197,18 @@ typedef struct {
 brax_status brax_rollout_random(const brax_system *sys, brax_qp in, int64_t n_steps, brax_qp out, int64_t n_envs,
                                 const brax_random_actions *ra, const brax_step_extras *extras, void *stream);
 
+/* ---- NEXT-4: differentiable step, forward mode.  One step (as brax_step) that
+ * also propagates a tangent: dout = ∂step/∂(qp, a) · (din, daction), computed with
+ * (value, tangent) arithmetic through every operation of the kernel (exact
+ * derivative of the fp32 step, not a finite difference).  Conventions at kinks
+ * (R35): min / max / clamp follow the selected argument (the first on
+ * ties), a contact's activity and the friction cone's regime are those of the
+ * primal.  `out` is bit-identical to brax_step's output.  din members may be
+ * NULL (zero tangent); daction may be NULL (zero).  Columns of the full Jacobian
+ * ∂Q_out/∂(Q_in, a) are JVPs with unit tangents. */
+brax_status brax_step_jvp(const brax_system *sys, brax_qp in, const float *action, brax_qp din,
+                          const float *daction, brax_qp out, brax_qp dout, int64_t n_envs, void *stream);
+
 /* ---- NEXT-1: Gym-like env epilogue fused into the step (Table 1;
  * :505-509 rewards; R30-R35).  Needs a `task { ... }` block in the system
  * text.  Per step and env, after the last substep and while the bodies are still

@@ -25,7 +25,7 @@ __all__ = [
     "brax_system_get_info", "brax_system_slot_table", "brax_default_qp", "brax_reset", "brax_step",
     "brax_step_ex", "brax_rollout", "brax_qp", "brax_step_extras", "brax_system_info", "LIB_PATH", "lib",
     "brax_env_io", "brax_system_task_info", "brax_env_step", "brax_env_reset", "brax_env_observe",
-    "brax_random_actions", "brax_rollout_random", "brax_env_step_random",
+    "brax_random_actions", "brax_rollout_random", "brax_env_step_random", "brax_step_jvp",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbrax_b200.so")
@@ -94,6 +94,7 @@ _SIGS = {
     "brax_step_ex": ([_P, brax_qp, _P, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_rollout": ([_P, brax_qp, _P, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_system_task_info": ([_P, _i32p], C.c_int),
+    "brax_step_jvp": ([_P, brax_qp, _P, brax_qp, _P, brax_qp, brax_qp, C.c_int64, _P], C.c_int),
     "brax_rollout_random": ([_P, brax_qp, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_random_actions),
                              C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_env_step_random": ([_P, brax_qp, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_random_actions),
@@ -253,6 +254,17 @@ def brax_env_step_random(sys: int, qp_in, n_steps: int, qp_out, n_envs: int, obs
                                     _stream(stream)))
 
 
+def _qp_or_null(q) -> brax_qp:
+    if q is None:
+        return brax_qp(None, None, None, None)
+    return brax_qp(*(_ptr(q.get(k)) for k in ("pos", "rot", "vel", "ang")))
+
+
+def brax_step_jvp(sys: int, qp_in, action, dqp_in, daction, qp_out, dqp_out, n_envs: int, stream=None) -> None:
+    _check(lib.brax_step_jvp(sys, _qp(qp_in), _ptr(action), _qp_or_null(dqp_in), _ptr(daction), _qp(qp_out),
+                             _qp(dqp_out), n_envs, _stream(stream)))
+
+
 def brax_system_task_info(sys: int):
     out = (C.c_int32 * 4)()
     _check(lib.brax_system_task_info(sys, out))
@@ -395,6 +407,43 @@ class System:
         brax_rollout_random(self._sys, qp_in, n_steps, qp_out, qp_in["pos"].shape[0], seed, env_offset, step0,
                             status, contact_active, stream)
         return qp_out
+
+    # ---- NEXT-4 differentiable step (forward mode) ----
+    def step_jvp(self, qp_in, action, dqp_in, daction=None, *, stream=None):
+        """One step and its directional derivative: returns (qp_out, dqp_out)."""
+        n = qp_in["pos"].shape[0]
+        out, dout = self.alloc_qp(n), self.alloc_qp(n)
+        brax_step_jvp(self._sys, qp_in, action, dqp_in, daction, out, dout, n, stream)
+        return out, dout
+
+    def step_jacobian(self, qp_in, action, *, stream=None):
+        """∂Q_out/∂(Q_in, a) per env, [n, 13B, 13B + A] (rows and columns ordered
+        pos | rot | vel | ang (env-major, body-major) then actions), one JVP launch
+        per input coordinate."""
+        import torch
+        n, B, A = qp_in["pos"].shape[0], self.n_bodies, self.act_dim
+        widths = {"pos": 3, "rot": 4, "vel": 3, "ang": 3}
+        K = 13 * B + A
+        jac = torch.empty((n, 13 * B, K), device=qp_in["pos"].device)
+        zeros = {k: torch.zeros_like(v) for k, v in qp_in.items()}
+        dz_a = torch.zeros_like(action) if A else None
+        col = 0
+        for k in ("pos", "rot", "vel", "ang"):
+            for b in range(B):
+                for c in range(widths[k]):
+                    d = dict(zeros)
+                    d[k] = torch.zeros_like(qp_in[k])
+                    d[k][:, b, c] = 1.0
+                    _, dout = self.step_jvp(qp_in, action, d, dz_a, stream=stream)
+                    jac[:, :, col] = torch.cat([dout[f].reshape(n, -1) for f in ("pos", "rot", "vel", "ang")], 1)
+                    col += 1
+        for j in range(A):
+            da = torch.zeros_like(action)
+            da[:, j] = 1.0
+            _, dout = self.step_jvp(qp_in, action, zeros, da, stream=stream)
+            jac[:, :, col] = torch.cat([dout[f].reshape(n, -1) for f in ("pos", "rot", "vel", "ang")], 1)
+            col += 1
+        return jac
 
     def env_observe(self, qp, stream=None):
         import torch

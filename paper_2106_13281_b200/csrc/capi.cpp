@@ -320,6 +320,34 @@ brax_status brax_env_step_random(const brax_system* sys, brax_qp in, int64_t n_s
   return step_common(sys, in, nullptr, n_steps, out, n_envs, nullptr, stream, io, nullptr, ra);
 }
 
+brax_status brax_step_jvp(const brax_system* sys, brax_qp in, const float* action, brax_qp din,
+                          const float* daction, brax_qp out, brax_qp dout, int64_t n_envs, void* stream) {
+  if (!sys || !sys->impl) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
+  if (n_envs < 0) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs must be >= 0");
+  if (n_envs == 0) return BRAX_OK;
+  brax_status st = check_qp(in, "in");
+  if (st != BRAX_OK) return st;
+  if ((st = check_qp(out, "out")) != BRAX_OK) return st;
+  if ((st = check_qp(dout, "dout")) != BRAX_OK) return st;
+  const brax::System& s = *sys->impl;
+  if (s.hd.A > 0 && !action) return fail(BRAX_E_INVALID_ARGUMENT, "action is NULL but act_dim > 0");
+  brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, out.pos, out.rot, out.vel, out.ang, action,
+                   nullptr, nullptr, n_envs, 1, 0, 0, nullptr};
+  a.dpos_in = din.pos;
+  a.drot_in = din.rot;
+  a.dvel_in = din.vel;
+  a.dang_in = din.ang;
+  a.dactions = daction;
+  a.dpos_out = dout.pos;
+  a.drot_out = dout.rot;
+  a.dvel_out = dout.vel;
+  a.dang_out = dout.ang;
+  cudaSetDevice(s.device);
+  cudaError_t e = brax::launch_step_jvp(s, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorInvalidValue) return fail(BRAX_E_VALIDATION, "brax_step_jvp: system too large for the JVP kernel");
+  return cuda_status(e, "brax_step_jvp launch");
+}
+
 brax_status brax_system_task_info(const brax_system* sys, int32_t out[4]) {
   if (!sys || !out) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
   const brax::Config& c = sys->impl->cfg;

@@ -176,6 +176,9 @@ struct StepArgs {
   int32_t act_random;
   uint64_t act_seed;
   int64_t act_env_offset, act_step0;
+  // NEXT-4 JVP (lane type D1): tangents of the inputs (NULL = zero) and of the outputs
+  const float *dpos_in, *drot_in, *dvel_in, *dang_in, *dactions;
+  float *dpos_out, *drot_out, *dvel_out, *dang_out;
 };
 constexpr uint32_t kActTag = 0x41435431u;  // "ACT1": separates the action stream from the reset stream
 

@@ -98,7 +98,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const int grp = lane / LG, el = lane - grp * LG;  // lane group; this lane's record slot (envs el, el + LG)
   const int64_t e0 = int64_t(blockIdx.x) * E;
   const int nvalid = (a.n_envs - e0 < E) ? int(a.n_envs - e0) : E;
-  const bool bulk = a.bulk_ok && nvalid == E;          // block-uniform
+  constexpr bool kJvp = V == 3;                        // D1: value + tangent staging, per-row copies
+  const bool bulk = !kJvp && a.bulk_ok && nvalid == E;  // block-uniform
   const bool act_bulk = bulk && a.act_bulk_ok && A > 0;
   const uint32_t qp_bytes = uint32_t(E * B) * 13u * 4u, act_bytes = uint32_t(E * A) * 4u;
 
@@ -127,7 +128,10 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       tma_load(sAstg, a.actions + e0 * A, act_bytes, &bars[1]);
     }
   }
-  if (!bulk) load_block<V>(a, sQ, B, E, e0, nvalid);  // ragged tail / unaligned: per-row loads
+  if (!bulk) {  // ragged tail / unaligned / JVP: per-row loads
+    if constexpr (kJvp) load_block_d(a, sQ, B, E, e0, nvalid);
+    else load_block<V>(a, sQ, B, E, e0, nvalid);
+  }
   mbar_wait(&bars[0], 0);
   if (bulk) stg_to_records<V>(stg, sQ, B, E);
   for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
@@ -224,6 +228,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         const int env = i / A, k = i - env * A;
         sA[k * RW + eslot<V>(env, LG)] = sAstg[i];
       }
+    } else if (kJvp) {
+      load_actions_d(a, sA, A, E, step, e0, nvalid);
     } else if (a.act_random) {  // NEXT-2: this step's actions from the counter-based generator
       const uint2 key = make_uint2(uint32_t(a.act_seed & 0xffffffffu), uint32_t(a.act_seed >> 32));
       const int A4 = (A + 3) >> 2;
@@ -362,6 +368,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       tma_store(a.ang_out + e0 * B * 3, sw, uint32_t(E * B) * 12u);
       tma_store_commit_wait();
     }
+  } else if constexpr (kJvp) {
+    store_block_d(a, sQ, B, E, e0, nvalid);
   } else {
     store_block<V>(a, sQ, B, E, e0, nvalid);
   }
@@ -548,6 +556,23 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   return best;
 }
 }  // namespace
+
+// NEXT-4 JVP: lane type D1 on the one-env-per-lane plan of the heuristic's lane-group count
+cudaError_t launch_step_jvp(const System& sys, const StepArgs& a, cudaStream_t stream) {
+  if (a.n_envs <= 0 || a.n_steps <= 0) return cudaSuccess;
+  int p = choose_plan(sys, a.n_envs);
+  if (sys.hd.plan[p].V == 2) p -= 3;  // plans 3-5 are the V = 2 versions of plans 0-2
+  DPlan P = sys.hd.plan[p];
+  if (P.smem_bytes_jvp > 227 * 1024) return cudaErrorInvalidValue;
+  P.smem_bytes = P.smem_bytes_jvp;
+  KArgs ka{a, sys.d_blob, sys.hd, p};
+  ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
+  ka.a.phase_cycles = nullptr;
+  dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
+  const int regs = choose_regs(sys, P, int64_t(grid.x));
+  if (regs >= 255) return launch_variant<D1, 255>(ka, grid, block, size_t(P.smem_bytes), stream);
+  return launch_variant<D1, 128>(ka, grid, block, size_t(P.smem_bytes), stream);
+}
 
 LaunchConfig launch_config(const System& sys, int64_t n_envs) {
   if (std::getenv("BRAX_PLAN") || std::getenv("BRAX_MAXREG")) return heuristic_config(sys, n_envs);

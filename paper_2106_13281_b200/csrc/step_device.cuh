@@ -127,6 +127,69 @@ __device__ __forceinline__ F2 operator-(float c, M2 m) { return fma2(neg2(m.a), 
 __device__ __forceinline__ F2 operator+(M2 m, M2 n) { return fma2(n.a, n.b, F2(m)); }
 __device__ __forceinline__ F2 operator-(M2 m, M2 n) { return fma2(neg2(n.a), n.b, F2(m)); }
 
+// ---- D1: one env per lane carrying (value, tangent): the forward-mode derivative
+// (JVP) of the step (NEXT-4).  The value part rounds exactly like F1 (the same
+// contraction pattern), so the JVP's primal output is brax_step's, bit for bit.
+// Derivative conventions at the method's kinks (R35):
+// min / max / clamp take the tangent of the selected argument (the first on ties),
+// selects take the selected branch's tangent, comparisons use values.
+struct D1 { float v, t; };
+__device__ __forceinline__ D1 d1mul(D1 a, D1 b) {
+  return {__fmul_rn(a.v, b.v), __fmaf_rn(a.t, b.v, __fmul_rn(a.v, b.t))};
+}
+__device__ __forceinline__ D1 d1fma(D1 a, D1 b, D1 c) {
+  return {__fmaf_rn(a.v, b.v, c.v), __fmaf_rn(a.t, b.v, __fmaf_rn(a.v, b.t, c.t))};
+}
+__device__ __forceinline__ D1 d1neg(D1 a) { return {-a.v, -a.t}; }
+__device__ __forceinline__ D1 d1bc(float f) { return {f, 0.f}; }
+struct MD1 {  // the product a*b, not yet rounded
+  D1 a, b;
+  __device__ __forceinline__ operator D1() const { return d1mul(a, b); }
+};
+__device__ __forceinline__ MD1 operator*(D1 a, D1 b) { return {a, b}; }
+__device__ __forceinline__ MD1 operator*(float a, D1 b) { return {d1bc(a), b}; }
+__device__ __forceinline__ MD1 operator*(D1 a, float b) { return {a, d1bc(b)}; }
+__device__ __forceinline__ MD1 operator*(MD1 m, D1 b) { return {D1(m), b}; }
+__device__ __forceinline__ MD1 operator*(D1 a, MD1 m) { return {a, D1(m)}; }
+__device__ __forceinline__ MD1 operator*(MD1 m, float b) { return {D1(m), d1bc(b)}; }
+__device__ __forceinline__ MD1 operator*(float a, MD1 m) { return {d1bc(a), D1(m)}; }
+__device__ __forceinline__ MD1 operator*(MD1 m, MD1 n) { return {D1(m), D1(n)}; }
+__device__ __forceinline__ MD1 operator-(MD1 m) { return {d1neg(m.a), m.b}; }
+__device__ __forceinline__ D1 operator-(D1 a) { return d1neg(a); }
+__device__ __forceinline__ D1 operator+(D1 a, D1 b) { return {__fadd_rn(a.v, b.v), __fadd_rn(a.t, b.t)}; }
+__device__ __forceinline__ D1 operator-(D1 a, D1 b) { return {__fadd_rn(a.v, -b.v), __fadd_rn(a.t, -b.t)}; }
+__device__ __forceinline__ D1 operator+(D1 a, float b) { return {__fadd_rn(a.v, b), a.t}; }
+__device__ __forceinline__ D1 operator+(float a, D1 b) { return {__fadd_rn(a, b.v), b.t}; }
+__device__ __forceinline__ D1 operator-(D1 a, float b) { return {__fadd_rn(a.v, -b), a.t}; }
+__device__ __forceinline__ D1 operator-(float a, D1 b) { return {__fadd_rn(a, -b.v), -b.t}; }
+__device__ __forceinline__ D1 operator+(MD1 m, D1 c) { return d1fma(m.a, m.b, c); }
+__device__ __forceinline__ D1 operator+(D1 c, MD1 m) { return d1fma(m.a, m.b, c); }
+__device__ __forceinline__ D1 operator-(MD1 m, D1 c) { return d1fma(m.a, m.b, d1neg(c)); }
+__device__ __forceinline__ D1 operator-(D1 c, MD1 m) { return d1fma(d1neg(m.a), m.b, c); }
+__device__ __forceinline__ D1 operator+(MD1 m, float c) { return d1fma(m.a, m.b, d1bc(c)); }
+__device__ __forceinline__ D1 operator+(float c, MD1 m) { return d1fma(m.a, m.b, d1bc(c)); }
+__device__ __forceinline__ D1 operator-(MD1 m, float c) { return d1fma(m.a, m.b, d1bc(-c)); }
+__device__ __forceinline__ D1 operator-(float c, MD1 m) { return d1fma(d1neg(m.a), m.b, d1bc(c)); }
+__device__ __forceinline__ D1 operator+(MD1 m, MD1 n) { return d1fma(n.a, n.b, D1(m)); }
+__device__ __forceinline__ D1 operator-(MD1 m, MD1 n) { return d1fma(d1neg(n.a), n.b, D1(m)); }
+__device__ __forceinline__ D1 vmin(D1 a, D1 b) { return {fminf(a.v, b.v), b.v < a.v ? b.t : a.t}; }
+__device__ __forceinline__ D1 vmax(D1 a, D1 b) { return {fmaxf(a.v, b.v), b.v > a.v ? b.t : a.t}; }
+__device__ __forceinline__ D1 vabs(D1 a) { return {fabsf(a.v), a.v < 0.f ? -a.t : a.t}; }
+__device__ __forceinline__ D1 vrsqrt(D1 a) {  // d(a^-1/2) = −½ a^-3/2 da
+  const float r = rsqrtf(a.v);
+  return {r, __fmul_rn(__fmul_rn(-0.5f, __fmul_rn(r, __fmul_rn(r, r))), a.t)};
+}
+__device__ __forceinline__ D1 vdiv(D1 a, D1 b) {  // d(a/b) = (da − q db)/b
+  const float q = __fdividef(a.v, b.v);
+  return {q, __fdividef(__fmaf_rn(-q, b.t, a.t), b.v)};
+}
+__device__ __forceinline__ D1 vcopysign(D1 a, D1 b) {
+  return {copysignf(a.v, b.v), (signbit(a.v) != signbit(b.v)) ? -a.t : a.t};
+}
+__device__ __forceinline__ bool lt(D1 a, D1 b) { return a.v < b.v; }
+__device__ __forceinline__ bool gt(D1 a, D1 b) { return a.v > b.v; }
+__device__ __forceinline__ D1 sel(bool m, D1 a, D1 b) { return m ? a : b; }
+
 __device__ __forceinline__ F1 vmin(F1 a, F1 b) { return {fminf(a.x, b.x)}; }
 __device__ __forceinline__ F2 vmin(F2 a, F2 b) { return {fminf(a.x, b.x), fminf(a.y, b.y)}; }
 __device__ __forceinline__ F1 vmax(F1 a, F1 b) { return {fmaxf(a.x, b.x)}; }
@@ -154,6 +217,7 @@ __device__ __forceinline__ F2 as_count(B2 m) { return {m.x ? 1.f : 0.f, m.y ? 1.
 template <class S> __device__ __forceinline__ S bc(float f);
 template <> __device__ __forceinline__ F1 bc<F1>(float f) { return {f}; }
 template <> __device__ __forceinline__ F2 bc<F2>(float f) { return {f, f}; }
+template <> __device__ __forceinline__ D1 bc<D1>(float f) { return {f, 0.f}; }
 template <class S> __device__ __forceinline__ S clampv(S x, float lo, float hi) {
   return vmin(vmax(x, bc<S>(lo)), bc<S>(hi));
 }
@@ -291,6 +355,36 @@ template <> struct Lanes<F2> {
   }
   static __device__ __forceinline__ void st(float* p, F2 v) { *reinterpret_cast<float2*>(p) = make_float2(v.x, v.y); }
   static __device__ __forceinline__ F2 w4(const float* p) {
+    float2 a = *reinterpret_cast<const float2*>(p + 6);
+    return {a.x, a.y};
+  }
+};
+
+template <> struct Lanes<D1> {  // one env per lane; records hold (value, tangent) pairs like F2's env pairs
+  static constexpr int V = 3, SL = 2, M = 8;
+  static constexpr int QS = kQS2, JS = kJS2, CS = kCS2;
+  static __device__ __forceinline__ V3T<D1> ld3(const float* p) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    return {{a.x, a.y}, {a.z, a.w}, {b.x, b.y}};
+  }
+  static __device__ __forceinline__ Q4T<D1> ldq(const float* p) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    return {{a.x, a.y}, {a.z, a.w}, {b.x, b.y}, {b.z, b.w}};
+  }
+  static __device__ __forceinline__ void st3(float* p, V3T<D1> v, D1 w = {0.f, 0.f}) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.x.v, v.x.t, v.y.v, v.y.t);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v.z.v, v.z.t, w.v, w.t);
+  }
+  static __device__ __forceinline__ void stq(float* p, Q4T<D1> q) {
+    *reinterpret_cast<float4*>(p) = make_float4(q.w.v, q.w.t, q.x.v, q.x.t);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(q.y.v, q.y.t, q.z.v, q.z.t);
+  }
+  static __device__ __forceinline__ D1 ld(const float* p) {
+    float2 a = *reinterpret_cast<const float2*>(p);
+    return {a.x, a.y};
+  }
+  static __device__ __forceinline__ void st(float* p, D1 v) { *reinterpret_cast<float2*>(p) = make_float2(v.v, v.t); }
+  static __device__ __forceinline__ D1 w4(const float* p) {
     float2 a = *reinterpret_cast<const float2*>(p + 6);
     return {a.x, a.y};
   }
@@ -571,7 +665,7 @@ __device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, fl
       P = jn * n - jt * th;
       ta = cross(rA, P);
       tb = cross(rB, P);
-      active = as_count(act);
+      active = sel(act, bc<S>(1.f), bc<S>(0.f));
     }
   }
   constexpr int M = Lanes<S>::M;
@@ -852,6 +946,17 @@ __device__ __forceinline__ void block_extras(const StepArgs& a, const float* sQ,
         }
         if (bits) atomicOr(&sStat[i % E], bits);
       }
+    } else if (V == 3) {  // value words of the (value, tangent) records
+      for (int i = threadIdx.x; i < B * E; i += blockDim.x) {
+        const float* p = sQ + i * kQS2;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          if (k == 6 || k == 22 || k == 30) continue;
+          bits |= word_bits(p[k]);
+        }
+        if (bits) atomicOr(&sStat[i % E], bits);
+      }
     } else {
       const int LG = E >> 1;
       for (int i = threadIdx.x; i < B * LG; i += blockDim.x) {
@@ -875,6 +980,62 @@ __device__ __forceinline__ void block_extras(const StepArgs& a, const float* sQ,
       a.contact_active[(e0 + env) * C + c] = uint8_t(sCnt[c * RW + eslot<V>(env, LG)]);
     }
   }
+}
+
+// ---- JVP staging (lane type D1, layout 3): value and tangent of every QP word,
+// per-row loads / stores (a NULL tangent pointer reads as zero / is not written).
+template <int K, bool kLoad>
+__device__ __forceinline__ void stage_d(const float* gin, const float* dgin, float* gout, float* dgout, float* sQ,
+                                        int f, int64_t e0, int nvalid, int B, int LG) {
+  const int row_len = B * K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int env = warp; env < nvalid; env += nw) {
+    const int64_t g0 = (e0 + env) * row_len;
+    for (int k = lane; k < row_len; k += 32) {
+      const int b = k / K, c = k - (k / K) * K;
+      float* s = sQ + qword<3>(b, env, f, c, LG);
+      if (kLoad) {
+        s[0] = __ldg(gin + g0 + k);
+        s[1] = dgin ? __ldg(dgin + g0 + k) : 0.f;
+      } else {
+        gout[g0 + k] = s[0];
+        if (dgout) dgout[g0 + k] = s[1];
+      }
+    }
+  }
+}
+__device__ __forceinline__ void load_block_d(const StepArgs& a, float* sQ, int B, int E, int64_t e0, int nvalid) {
+  if (nvalid < E) {  // identity state, zero tangent
+    for (int i = threadIdx.x; i < B * E; i += blockDim.x) {
+      float4* p = reinterpret_cast<float4*>(sQ + i * kQS2);
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      p[0] = z; p[1] = z; p[2] = make_float4(1.f, 0.f, 0.f, 0.f); p[3] = z;
+      p[4] = z; p[5] = z; p[6] = z; p[7] = z;
+    }
+    __syncthreads();
+  }
+  stage_d<3, true>(a.pos_in, a.dpos_in, nullptr, nullptr, sQ, 0, e0, nvalid, B, E);
+  stage_d<4, true>(a.rot_in, a.drot_in, nullptr, nullptr, sQ, 1, e0, nvalid, B, E);
+  stage_d<3, true>(a.vel_in, a.dvel_in, nullptr, nullptr, sQ, 2, e0, nvalid, B, E);
+  stage_d<3, true>(a.ang_in, a.dang_in, nullptr, nullptr, sQ, 3, e0, nvalid, B, E);
+}
+__device__ __forceinline__ void store_block_d(const StepArgs& a, float* sQ, int B, int E, int64_t e0, int nvalid) {
+  stage_d<3, false>(nullptr, nullptr, a.pos_out, a.dpos_out, sQ, 0, e0, nvalid, B, E);
+  stage_d<4, false>(nullptr, nullptr, a.rot_out, a.drot_out, sQ, 1, e0, nvalid, B, E);
+  stage_d<3, false>(nullptr, nullptr, a.vel_out, a.dvel_out, sQ, 2, e0, nvalid, B, E);
+  stage_d<3, false>(nullptr, nullptr, a.ang_out, a.dang_out, sQ, 3, e0, nvalid, B, E);
+}
+// this step's action value and tangent -> sA[k][2·env + {0, 1}]
+__device__ __forceinline__ void load_actions_d(const StepArgs& a, float* sA, int A, int E, int64_t step, int64_t e0,
+                                               int nvalid) {
+  if (A <= 0) return;
+  const int64_t off = (step * a.n_envs + e0) * A;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int env = warp; env < nvalid; env += nw)
+    for (int k = lane; k < A; k += 32) {
+      sA[k * 2 * E + 2 * env] = __ldg(a.actions + off + env * A + k);
+      sA[k * 2 * E + 2 * env + 1] = a.dactions ? __ldg(a.dactions + off + env * A + k) : 0.f;
+    }
 }
 
 // S9 fallback (ragged tail / unaligned): per-row stores of the QP
