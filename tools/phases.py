@@ -16,10 +16,15 @@ p = argparse.ArgumentParser()
 p.add_argument("--scenes", default="ant")
 p.add_argument("--envs", default="2048,8192,65536")
 p.add_argument("--steps", type=int, default=50)
+p.add_argument("--plans", default="", help="comma-separated 'G:V' launch plans (default: the library's choice)")
 a = p.parse_args()
 for scene in a.scenes.split(","):
     s = bx.System(open(os.path.join(ROOT, "scenes", f"{scene}.bxc")).read())
-    for n in [int(x) for x in a.envs.split(",")]:
+    for n, plan in [(int(x), pl) for x in a.envs.split(",") for pl in (a.plans.split(",") if a.plans else [""])]:
+        if plan:
+            os.environ["BRAX_PLAN"] = plan.replace(":", ",")
+        else:
+            os.environ.pop("BRAX_PLAN", None)
         qp = s.alloc_qp(n)
         s.reset(qp, 0, 0.1, 0.1)
         acts = torch.from_numpy(synth.actions(1, a.steps, n, s.act_dim)).cuda() if s.act_dim else None
@@ -33,9 +38,10 @@ for scene in a.scenes.split(","):
         torch.cuda.synchronize()
         cyc = s.phase_cycles()
         s.set_tracing(False)
-        blocks = (n + 31) // 32
+        cfg = s.launch_config(n)
+        blocks = (n + cfg["E"] - 1) // cfg["E"]
         per = [c / (a.steps * blocks) for c in cyc]
         tot = sum(per)
-        print(json.dumps({"scene": scene, "envs": n, "cycles_per_block_step": [round(x) for x in per],
+        print(json.dumps({"scene": scene, "envs": n, "plan": [cfg["G"], cfg["V"]], "cycles_per_block_step": [round(x) for x in per],
                           "share": [round(x / tot, 3) for x in per],
                           "per_substep_B_C": [round(per[1] / s.substeps), round(per[2] / s.substeps)]}))
