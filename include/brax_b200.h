@@ -209,6 +209,14 @@ brax_status brax_rollout_random(const brax_system *sys, brax_qp in, int64_t n_st
 brax_status brax_step_jvp(const brax_system *sys, brax_qp in, const float *action, brax_qp din,
                           const float *daction, brax_qp out, brax_qp dout, int64_t n_envs, void *stream);
 
+/* Reverse mode (cotangent) of one step: g_in = (∂Q_out/∂Q_in)ᵀ·g_out and
+ * g_action = (∂Q_out/∂a)ᵀ·g_out per env, assembled from brax_step_jvp columns
+ * (13B + A JVP launches; exact, same conventions).  g_out members may be NULL
+ * (zero); g_action may be NULL (not written) and is [n][act_dim].  Synchronous
+ * allocation-free for the caller: scratch is stream-ordered (cudaMallocAsync). */
+brax_status brax_step_vjp(const brax_system *sys, brax_qp in, const float *action, brax_qp g_out, brax_qp g_in,
+                          float *g_action, int64_t n_envs, void *stream);
+
 /* ---- NEXT-1: Gym-like env epilogue fused into the step (Table 1;
  * :505-509 rewards; R30-R35).  Needs a `task { ... }` block in the system
  * text.  Per step and env, after the last substep and while the bodies are still

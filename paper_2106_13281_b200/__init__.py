@@ -26,6 +26,7 @@ __all__ = [
     "brax_step_ex", "brax_rollout", "brax_qp", "brax_step_extras", "brax_system_info", "LIB_PATH", "lib",
     "brax_env_io", "brax_system_task_info", "brax_env_step", "brax_env_reset", "brax_env_observe",
     "brax_random_actions", "brax_rollout_random", "brax_env_step_random", "brax_step_jvp",
+    "brax_step_vjp",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbrax_b200.so")
@@ -95,6 +96,7 @@ _SIGS = {
     "brax_rollout": ([_P, brax_qp, _P, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_system_task_info": ([_P, _i32p], C.c_int),
     "brax_step_jvp": ([_P, brax_qp, _P, brax_qp, _P, brax_qp, brax_qp, C.c_int64, _P], C.c_int),
+    "brax_step_vjp": ([_P, brax_qp, _P, brax_qp, brax_qp, _P, C.c_int64, _P], C.c_int),
     "brax_rollout_random": ([_P, brax_qp, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_random_actions),
                              C.POINTER(brax_step_extras), _P], C.c_int),
     "brax_env_step_random": ([_P, brax_qp, C.c_int64, brax_qp, C.c_int64, C.POINTER(brax_random_actions),
@@ -265,6 +267,11 @@ def brax_step_jvp(sys: int, qp_in, action, dqp_in, daction, qp_out, dqp_out, n_e
                              _qp(dqp_out), n_envs, _stream(stream)))
 
 
+def brax_step_vjp(sys: int, qp_in, action, g_out, g_in, g_action, n_envs: int, stream=None) -> None:
+    _check(lib.brax_step_vjp(sys, _qp(qp_in), _ptr(action), _qp_or_null(g_out), _qp(g_in), _ptr(g_action), n_envs,
+                             _stream(stream)))
+
+
 def brax_system_task_info(sys: int):
     out = (C.c_int32 * 4)()
     _check(lib.brax_system_task_info(sys, out))
@@ -415,6 +422,15 @@ class System:
         out, dout = self.alloc_qp(n), self.alloc_qp(n)
         brax_step_jvp(self._sys, qp_in, action, dqp_in, daction, out, dout, n, stream)
         return out, dout
+
+    def step_vjp(self, qp_in, action, g_out, *, stream=None):
+        """Cotangent of one step: returns (g_in qp dict, g_action [n, A] or None)."""
+        import torch
+        n = qp_in["pos"].shape[0]
+        g_in = self.alloc_qp(n)
+        g_a = torch.empty((n, self.act_dim), device=qp_in["pos"].device) if self.act_dim else None
+        brax_step_vjp(self._sys, qp_in, action, g_out, g_in, g_a, n, stream)
+        return g_in, g_a
 
     def step_jacobian(self, qp_in, action, *, stream=None):
         """∂Q_out/∂(Q_in, a) per env, [n, 13B, 13B + A] (rows and columns ordered

@@ -348,6 +348,26 @@ brax_status brax_step_jvp(const brax_system* sys, brax_qp in, const float* actio
   return cuda_status(e, "brax_step_jvp launch");
 }
 
+brax_status brax_step_vjp(const brax_system* sys, brax_qp in, const float* action, brax_qp g_out, brax_qp g_in,
+                          float* g_action, int64_t n_envs, void* stream) {
+  if (!sys || !sys->impl) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
+  if (n_envs < 0) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs must be >= 0");
+  if (n_envs == 0) return BRAX_OK;
+  brax_status st = check_qp(in, "in");
+  if (st != BRAX_OK) return st;
+  if ((st = check_qp(g_in, "g_in")) != BRAX_OK) return st;
+  const brax::System& s = *sys->impl;
+  if (s.hd.A > 0 && !action) return fail(BRAX_E_INVALID_ARGUMENT, "action is NULL but act_dim > 0");
+  brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, nullptr, nullptr, nullptr, nullptr, action,
+                   nullptr, nullptr, n_envs, 1, 0, 0, nullptr};
+  const float* go[4] = {g_out.pos, g_out.rot, g_out.vel, g_out.ang};
+  float* gi[4] = {g_in.pos, g_in.rot, g_in.vel, g_in.ang};
+  cudaSetDevice(s.device);
+  cudaError_t e = brax::launch_step_vjp(s, a, go, gi, g_action, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorInvalidValue) return fail(BRAX_E_VALIDATION, "brax_step_vjp: system too large for the JVP kernel");
+  return cuda_status(e, "brax_step_vjp");
+}
+
 brax_status brax_system_task_info(const brax_system* sys, int32_t out[4]) {
   if (!sys || !out) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
   const brax::Config& c = sys->impl->cfg;

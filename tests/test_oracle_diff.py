@@ -65,3 +65,24 @@ def test_kink_detection_at_contact_activation():
     dq["pos"][:, 1, 2] = 1.0
     _, kink = jvp_fd(o, qp, None, dq, None, eps=1e-6)
     assert kink[0] and not kink[1]
+
+
+def test_vjp_is_the_transposed_jvp():
+    """⟨g, J·v⟩ = ⟨Jᵀ·g, v⟩ for random g, v (the adjoint identity), on a jointed
+    scene with actions, and Jᵀg on the linear oscillator equals (M^S)ᵀ g."""
+    from oracle.diff import jacobian_fd, vjp_fd
+    o = oracle.Oracle(oracle.load_scene("chain2"))
+    qp = o.reset(3, 1, 0.2, 0.2)
+    rng = np.random.default_rng(2)
+    a = rng.uniform(-1, 1, size=(3, o.act_dim))
+    g = {k: rng.normal(size=v.shape) for k, v in qp.items()}
+    v = {k: rng.normal(size=vv.shape) for k, vv in qp.items()}
+    dv_a = rng.normal(size=(3, o.act_dim))
+    jv, _ = jvp_fd(o, qp, a, v, dv_a)
+    gin, ga, kink = vjp_fd(o, qp, a, g)
+    assert not kink.any()
+    lhs = sum((g[k] * jv[k]).reshape(3, -1).sum(1) for k in g)
+    rhs = sum((gin[k] * v[k]).reshape(3, -1).sum(1) for k in g) + (ga * dv_a).sum(1)
+    assert np.allclose(lhs, rhs, rtol=1e-6, atol=1e-6)
+    J, _ = jacobian_fd(o, qp, a)
+    assert J.shape == (3, 13 * o.n_bodies, 13 * o.n_bodies + o.act_dim)
