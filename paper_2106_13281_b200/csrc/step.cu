@@ -110,9 +110,15 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     mbar_fence_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {  // the tables are constant: load them before waiting for the previous grid
     mbar_expect_tx(&bars[0], uint32_t(H.blob_words) * 4u + (bulk ? qp_bytes : 0u));
     tma_load(sBlob, ka.blob, uint32_t(H.blob_words) * 4u, &bars[0]);
+  }
+  // programmatic dependent launch: everything above overlapped the previous kernel's
+  // tail; the QP and actions may be its outputs, so wait for it to complete here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (tid == 0) {
     if (bulk) {
       float* sp = stg;
       float* sr = sp + E * B * 3;
@@ -437,8 +443,17 @@ cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, 
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
-  brax_step_kernel<S, R, kEnv><<<grid, block, smem, stream>>>(ka);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: prologue overlaps the previous kernel
+  attr[0].val.programmaticStreamSerializationAllowed = std::getenv("BRAX_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, brax_step_kernel<S, R, kEnv>, ka);
 }
 
 cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream) {
