@@ -819,8 +819,10 @@ __device__ __forceinline__ void tma_store(void* dst, const void* src, uint32_t b
                "r"(bytes)
                : "memory");
 }
+// waits until the bulk stores have READ shared memory (the CTA may then exit; the
+// global writes complete with the grid, as for any store)
 __device__ __forceinline__ void tma_store_commit_wait() {
-  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
