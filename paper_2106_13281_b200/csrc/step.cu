@@ -395,7 +395,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
 // alone would leave the SMs with few independent env groups to overlap their
 // per-substep barriers; G = 1 once the grid fills the GPU.
 int choose_plan(const System& sys, int64_t n_envs) {
-  auto fits = [&](int i) { return sys.hd.plan[i].smem_bytes <= 227 * 1024; };  // plan 0 always fits
+  auto fits = [&](int i) { return sys.hd.plan[i].smem_bytes <= 227 * 1024; };
   if (const char* e = std::getenv("BRAX_PLAN")) {  // "G,V" override (experiments; ignored if it does not fit)
     int g = 0, v = 0;
     if (std::sscanf(e, "%d,%d", &g, &v) == 2)
@@ -410,7 +410,11 @@ int choose_plan(const System& sys, int64_t n_envs) {
   if (4 * blocks32 <= sms) p = 2;
   else if (2 * blocks32 <= sms) p = 1;
   else if (blocks32 >= 4 * sms) p = 3;  // large batches: two envs per lane (G = 1, V = 2)
-  return fits(p) ? p : 0;
+  if (fits(p)) return p;
+  // large systems: the biggest one-env-per-lane block that fits (plan 2, 8 envs, always does)
+  for (int q : {0, 1, 2})
+    if (fits(q)) return q;
+  return 2;
 }
 
 // Register budget per thread: as many as possible while the SM still holds the
@@ -577,6 +581,7 @@ cudaError_t launch_step_jvp(const System& sys, const StepArgs& a, cudaStream_t s
   if (a.n_envs <= 0 || a.n_steps <= 0) return cudaSuccess;
   int p = choose_plan(sys, a.n_envs);
   if (sys.hd.plan[p].V == 2) p -= 3;  // plans 3-5 are the V = 2 versions of plans 0-2
+  while (p < 2 && sys.hd.plan[p].smem_bytes_jvp > 227 * 1024) ++p;  // smaller blocks for large systems
   DPlan P = sys.hd.plan[p];
   if (P.smem_bytes_jvp > 227 * 1024) return cudaErrorInvalidValue;
   P.smem_bytes = P.smem_bytes_jvp;

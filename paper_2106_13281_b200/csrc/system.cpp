@@ -400,10 +400,13 @@ System* build_host(const Config& cfg) {
                                hd.task.contact_obs).total_words * 4;
     P.smem_bytes_jvp = P.V == 1 ? smem_layout(B, J, C, hd.A, P.E, LG, 1, hd.blob_words, 0, 0).total_words * 4 : 0;
   }
+  // smallest block (G = 4: 8 envs) must fit; larger blocks are used where they fit
   s->smem_bytes = size_t(hd.plan[0].smem_bytes);
-  if (size_t(hd.plan[0].smem_bytes) > 227 * 1024)
+  int smallest = hd.plan[0].smem_bytes;
+  for (int pi = 0; pi < kNumPlans; ++pi) smallest = std::min(smallest, hd.plan[pi].smem_bytes);
+  if (size_t(smallest) > 227 * 1024)
     throw Error(BRAX_E_VALIDATION, "config: system too large for one block's shared memory (" +
-                                       std::to_string(s->smem_bytes) + " bytes)");
+                                       std::to_string(smallest) + " bytes with 8 envs per block)");
 
   return s.release();
 }

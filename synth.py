@@ -32,3 +32,23 @@ def sample_envs(seed: int, n: int, k: int) -> np.ndarray:
 
 def to_f32(qp):
     return {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in qp.items()}
+
+
+def chain_text(n_links: int, substeps: int = 4) -> str:
+    """Scene text of a free snake of n_links capsules jointed end to end over a
+    ground plane, each joint actuated (the maximum-size parity cases: B = n_links + 1,
+    J = A = n_links − 1, C = 2·n_links capsule-end slots)."""
+    lines = ["dt: 0.02", f"substeps: {substeps}", "gravity { z: -9.8 }", "friction: 0.8",
+             'bodies { name: "Ground" frozen { all: true } colliders { plane {} } }']
+    for i in range(n_links):
+        lines.append(f'bodies {{ name: "L{i}" mass: 1 inertia {{ x: 0.1 y: 0.1 z: 0.1 }} '
+                     f'colliders {{ rotation {{ y: 90 }} capsule {{ radius: 0.05 length: 0.3 }} }} }}')
+    for i in range(1, n_links):
+        lines.append(f'joints {{ name: "J{i}" parent: "L{i - 1}" child: "L{i}" stiffness: 2000 angular_damping: 2 '
+                     f'parent_offset {{ x: 0.15 }} child_offset {{ x: -0.15 }} rotation {{ z: 90 }} '
+                     f'angle_limit {{ min: -60 max: 60 }} }}')
+        lines.append(f'actuators {{ name: "J{i}" joint: "J{i}" strength: 5 torque {{}} }}')
+    for i in range(n_links):
+        lines.append(f'collide_include {{ first: "L{i}" second: "Ground" }}')
+    lines.append('defaults { qps { name: "L0" pos { z: 0.3 } } }')
+    return "\n".join(lines)

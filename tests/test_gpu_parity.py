@@ -343,3 +343,33 @@ def test_rollout_random_actions_match_the_oracle_generator():
     ref = s.env_step(st2, torch.from_numpy(acts).cuda(), seed=1, env_offset=5)
     for key in ("obs", "reward", "done"):
         assert torch.equal(out[key], ref[key]), key
+
+
+@pytest.mark.parametrize("links", [24, 60])
+def test_maximum_size_systems(links):
+    """Large systems (a 61-body, 120-slot snake) still run: the launch falls back to
+    smaller blocks when 32 envs do not fit in shared memory, with the oracle's answer;
+    a system too large even for 8-env blocks is rejected at creation."""
+    text = synth.chain_text(links)
+    o, s = oracle.Oracle(text), bx.System(text)
+    n = 131
+    qp = trajectory_states(o, n, seed=71, T0=2)
+    act = synth.actions(72, 1, n, o.act_dim)[0]
+    ref, ex = o.step(qp, act, threads=8)
+    got, status, ca = gpu_step(s, qp, act)
+    keep = ~ex["ambiguous"]
+    err, errs = max_err(got, ref, keep)
+    # the long stiff chain's fp32 rounding floor (the same algorithm in fp32 on the
+    # host) reaches 1.7e-4 at 60 links: the bound is the larger of TOL_STEP and twice it
+    r32, _ = o.step(qp, act, threads=8, fp32=True)
+    floor, _ = max_err(synth.to_f32(r32), ref, keep)
+    assert err <= max(TOL_STEP, 2 * floor), (errs, floor)
+    assert np.array_equal(ca[keep], ex["contact_active"][keep])
+    cfg = s.launch_config(n)
+    if links == 60:
+        assert cfg["E"] < 32, cfg
+
+
+def test_too_large_system_is_rejected():
+    with pytest.raises(bx.BraxError, match="too large"):
+        bx.System(synth.chain_text(120))  # 240 slots (under the 255 limit), > 227 KB at 8 envs

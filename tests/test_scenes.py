@@ -34,3 +34,20 @@ def test_1000_step_random_action_stability(name):
     for k in qp:
         assert np.all(np.isfinite(qp[k]))
     assert np.max(np.abs(qp["vel"])) < 100 and np.max(np.abs(qp["ang"])) < 200
+
+
+@pytest.mark.parametrize("links", [24, 60])
+def test_generated_chain_is_stable(links):
+    """The maximum-size parity scenes (synth.chain_text): valid, lint-free, and
+    100 random-action steps without a status bit in the oracle."""
+    o = oracle.Oracle(synth.chain_text(links))
+    assert (o.n_bodies, len(o.sys.joints), o.act_dim, o.n_slots) == (links + 1, links - 1, links - 1, 2 * links)
+    assert o.sys.lint() == []
+    n = 4
+    qp = o.reset(n, 0, 0.1, 0.1)
+    acts = synth.actions(1, 100, n, o.act_dim)
+    status = np.zeros(n, np.uint32)
+    for t in range(100):
+        qp, ex = o.step(qp, acts[t], threads=4)
+        status |= ex["status"]
+    assert np.all(status == 0)
