@@ -24,8 +24,10 @@ for r in rows[1:]:
     ex.append((int(r[hdr["Address"]], 16), r[hdr["Source"]].strip(), int(r[hdr["Instructions Executed"]] or 0)))
 base = ex[0][0]
 # mangled-name match: template args of the profiled kernel
-m = re.search(r"brax_step_kernel<([\w:]+), \(int\)(\d+)>", kname)
-want = ("IfLi" if m.group(1) == "float" else "INS_3dev2F2ELi") + m.group(2) + "E"
+m = re.search(r"brax_step_kernel<(?:[\w:]+::)?(\w+), (?:\(int\))?(\d+)(?:, (?:\(bool\))?(\w+))?>", kname)
+lane, regs, env = m.group(1), m.group(2), m.group(3)
+envbit = "1" if env in ("1", "true") else "0"
+want = f"INS_3dev2{lane}ELi{regs}ELb{envbit}E" if env is not None else f"INS_3dev2{lane}ELi{regs}E"
 dis = subprocess.run(["nvdisasm", "-gi", "-c", cubin], capture_output=True, text=True).stdout
 loc = {}
 cur = None
