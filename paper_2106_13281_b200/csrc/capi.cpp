@@ -3,6 +3,7 @@
 // dispatch to the kernel launchers.  No compute happens here.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -363,7 +364,9 @@ brax_status brax_step_vjp(const brax_system* sys, brax_qp in, const float* actio
   const float* go[4] = {g_out.pos, g_out.rot, g_out.vel, g_out.ang};
   float* gi[4] = {g_in.pos, g_in.rot, g_in.vel, g_in.ang};
   cudaSetDevice(s.device);
-  cudaError_t e = brax::launch_step_vjp(s, a, go, gi, g_action, static_cast<cudaStream_t>(stream));
+  cudaError_t e = std::getenv("BRAX_VJP_COLUMNS")
+                      ? brax::launch_step_vjp(s, a, go, gi, g_action, static_cast<cudaStream_t>(stream))
+                      : brax::launch_step_vjp_fused(s, a, go, gi, g_action, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorInvalidValue) return fail(BRAX_E_VALIDATION, "brax_step_vjp: system too large for the JVP kernel");
   return cuda_status(e, "brax_step_vjp");
 }

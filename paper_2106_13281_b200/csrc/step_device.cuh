@@ -405,6 +405,16 @@ template <class S> struct Row {
 };
 
 // ---- S2: kinematic integrator (R3, R21) -------------------------
+// rotation part: q' = normalize(q + ½h (0, ω)⊗q) (ω already masked)
+template <class S> __device__ __forceinline__ Q4T<S> kin_rot(Q4T<S> q, V3T<S> w, float h) {
+  Q4T<S> dq = qmul(Q4T<S>{bc<S>(0.f), w.x, w.y, w.z}, q);
+  const float hh = 0.5f * h;
+  q = Q4T<S>{q.w + hh * dq.w, q.x + hh * dq.x, q.y + hh * dq.y, q.z + hh * dq.z};
+  S n2 = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+  S inv = vrsqrt(n2);
+  inv = inv * (1.5f - 0.5f * n2 * inv * inv);  // one Newton step: ≈ correctly rounded 1/√n2
+  return Q4T<S>{q.w * inv, q.x * inv, q.y * inv, q.z * inv};
+}
 template <class S> __device__ __forceinline__ void kinematic(const DBody& bd, Row<S> r, float h) {
   V3T<S> v = r.vel();
   if (!(bd.flags & kFlagFreePos)) v = had(bd.mpos, v);
@@ -412,22 +422,18 @@ template <class S> __device__ __forceinline__ void kinematic(const DBody& bd, Ro
   if (!bd.rot_frozen) {
     V3T<S> w = r.ang();
     if (!(bd.flags & kFlagFreeRot)) w = had(bd.mrot, w);
-    Q4T<S> q = r.rot();
-    Q4T<S> dq = qmul(Q4T<S>{bc<S>(0.f), w.x, w.y, w.z}, q);
-    const float hh = 0.5f * h;
-    q = Q4T<S>{q.w + hh * dq.w, q.x + hh * dq.x, q.y + hh * dq.y, q.z + hh * dq.z};
-    S n2 = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
-    S inv = vrsqrt(n2);
-    inv = inv * (1.5f - 0.5f * n2 * inv * inv);  // one Newton step: ≈ correctly rounded 1/√n2
-    r.set_rot(Q4T<S>{q.w * inv, q.x * inv, q.y * inv, q.z * inv});
+    r.set_rot(kin_rot(r.rot(), w, h));
   }
 }
 
 // ---- S3 + S4: joint spring/limits with its actuator (R5, R7-R12)
-// act: this lane's column of the block's actions sA[k][slot] (row stride E).
-// out: this (joint, lane) record: F on child | T child | T parent.
-template <class S>
-__device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, const float* act, int E, float* out) {
+// Computed by joint_f from any row type with pos() / rot() / vel() / ang() (shared-memory
+// records for the step, register rows for the adjoint's local derivatives) and an
+// action accessor act(k) for action component k; returns F on the child, T on the
+// child and T on the parent (already negated, as stored).
+template <class S> struct JointOut { V3T<S> f, tc, tp; };
+template <class S, class RowT, class ActF>
+__device__ __forceinline__ JointOut<S> joint_f(const DJoint& Jm, const RowT& P, const RowT& C, ActF act) {
   // the parameter record, read with LDS.128 (struct fields at fixed float4 slots)
   const float4* J4 = reinterpret_cast<const float4*>(&Jm);
   const int4 h0 = *reinterpret_cast<const int4*>(&Jm), h1 = reinterpret_cast<const int4*>(&Jm)[1];
@@ -463,7 +469,7 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       if (i < dof) {
-        S a = Lanes<S>::ld(act + (act_offset + i) * E);
+        S a = act(act_offset + i);
         tau[i] = tau[i] + ((act_kind == 0) ? ca_s.y * clampv(a, -1.f, 1.f)
                                            : ca_s.y * (clampv(a, lo[i], hi[i]) - th[i]));
       }
@@ -482,10 +488,17 @@ __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, cons
   if (!(flags & kJNoCa)) twd = axpy(ca_s.x, wp - wc, twd);
   V3T<S> tc = cross_add(rc, f, twd);
   V3T<S> tp = cross_add(rp, f, twd);
+  return JointOut<S>{f, tc, V3T<S>{-tp.x, -tp.y, -tp.z}};
+}
+// act: this lane's column of the block's actions sA[k][slot] (row stride E).
+// out: this (joint, lane) record: F on child | T child | T parent.
+template <class S>
+__device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, const float* act, int E, float* out) {
+  const JointOut<S> o = joint_f<S>(Jm, P, C, [&](int k) { return Lanes<S>::ld(act + k * E); });
   constexpr int M = Lanes<S>::M;
-  Lanes<S>::st3(out, f);
-  Lanes<S>::st3(out + M, tc);
-  Lanes<S>::st3(out + 2 * M, V3T<S>{-tp.x, -tp.y, -tp.z});
+  Lanes<S>::st3(out, o.f);
+  Lanes<S>::st3(out + M, o.tc);
+  Lanes<S>::st3(out + 2 * M, o.tp);
 }
 
 // ---- NEXT-1 observation of one joint (R32): its free axes' angles θ_i (R7) and
@@ -568,9 +581,10 @@ __device__ __forceinline__ void seg_seg(V3T<S> p1, V3T<S> q1, V3T<S> p2, V3T<S> 
 
 // ---- S5: contact slot, velocity-level impulse + Baumgarte (R13-R19)
 // out: this (slot, lane) record: P, active | r_A×P | r_B×P; cnt: substeps active.
-template <class S>
-__device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, float opl_e, float beta_over_h,
-                                        float mu, float* out, S& cnt) {
+template <class S> struct ContactOut { V3T<S> P; S active; V3T<S> ta, tb; };
+template <class S, class RowT>
+__device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT& A, const RowT& B, float opl_e,
+                                                   float beta_over_h, float mu) {
   // the parameter record, read with LDS.128 at its fixed float4 slots
   const float4* S4 = reinterpret_cast<const float4*>(&SLm);
   const int4 h0 = *reinterpret_cast<const int4*>(&SLm), h1 = reinterpret_cast<const int4*>(&SLm)[1];
@@ -668,11 +682,17 @@ __device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, fl
       active = sel(act, bc<S>(1.f), bc<S>(0.f));
     }
   }
+  return ContactOut<S>{P, active, ta, tb};
+}
+template <class S>
+__device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, float opl_e, float beta_over_h,
+                                        float mu, float* out, S& cnt) {
+  const ContactOut<S> o = contact_f<S>(SLm, A, B, opl_e, beta_over_h, mu);
   constexpr int M = Lanes<S>::M;
-  Lanes<S>::st3(out, P, active);
-  Lanes<S>::st3(out + M, ta);
-  Lanes<S>::st3(out + 2 * M, tb);
-  cnt = cnt + active;
+  Lanes<S>::st3(out, o.P, o.active);
+  Lanes<S>::st3(out + M, o.ta);
+  Lanes<S>::st3(out + 2 * M, o.tb);
+  cnt = cnt + o.active;
 }
 
 
@@ -737,15 +757,7 @@ template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Ro
   }
   if (kin) {  // next substep's kinematic integrator (v, ω already masked)
     r.set_pos(axpy(h, v, r.pos()));
-    if (!bd.rot_frozen) {
-      Q4T<S> dq = qmul(Q4T<S>{bc<S>(0.f), w.x, w.y, w.z}, q);
-      const float hh = 0.5f * h;
-      Q4T<S> qn{q.w + hh * dq.w, q.x + hh * dq.x, q.y + hh * dq.y, q.z + hh * dq.z};
-      S n2 = qn.w * qn.w + qn.x * qn.x + qn.y * qn.y + qn.z * qn.z;
-      S inv = vrsqrt(n2);
-      inv = inv * (1.5f - 0.5f * n2 * inv * inv);
-      r.set_rot(Q4T<S>{qn.w * inv, qn.x * inv, qn.y * inv, qn.z * inv});
-    }
+    if (!bd.rot_frozen) r.set_rot(kin_rot(q, w, h));
   }
 }
 

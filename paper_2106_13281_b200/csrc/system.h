@@ -61,7 +61,10 @@ LaunchConfig launch_config(const System& sys, int64_t n_envs);
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream);
 // Forward-mode derivative (JVP) of the step: StepArgs' d*_in tangents -> d*_out (NEXT-4).
 cudaError_t launch_step_jvp(const System& sys, const StepArgs& a, cudaStream_t stream);
-// Reverse-mode cotangent of one step from the JVP columns (diff.cu): g_in = Jᵀ·g_out.
+// Reverse-mode cotangent of one step in one launch (vjp.cu): g_in = Jᵀ·g_out.
+cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, const float* const g_out[4],
+                                  float* const g_in[4], float* g_action, cudaStream_t stream);
+// The same from the JVP columns (diff.cu), 13B + A JVP launches: the cross-check.
 cudaError_t launch_step_vjp(const System& sys, const StepArgs& primal, const float* const g_out[4],
                             float* const g_in[4], float* g_action, cudaStream_t stream);
 cudaError_t launch_reset(const System& sys, float* pos, float* rot, float* vel, float* ang, int64_t n,

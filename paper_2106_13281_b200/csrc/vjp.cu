@@ -1,0 +1,449 @@
+// vjp.cu — reverse mode of one step in ONE launch (NEXT-4).
+//
+// For every env: g_in = (∂Q_out/∂Q_in)ᵀ g_out and g_action = (∂Q_out/∂a)ᵀ g_out,
+// the exact transpose of brax_step_jvp's derivative (same conventions, R35).  A
+// block keeps E envs' states in shared memory and sweeps the substeps backwards:
+//   for s = S−1 … 0:
+//     recompute the state at the start of substep s from the step's input
+//     (checkpoint = the input; Σ s = S(S−1)/2 forward substeps in total), then
+//     S2(s) and the items of substep s (their contact counts and summed forces);
+//     integrator adjoint (S7, S8: linear in v, ω, F, T, dV, dW; I_w⁻¹(q) by local
+//       forward derivatives for anisotropic bodies)        — one thread per (body, env)
+//     item adjoints: each joint / contact slot's local Jacobian-transpose product,
+//       from value+tangent (D1) evaluations of the same item code along each of its
+//       26 (+dof) inputs                                    — warp (lane group) per item
+//     gather of the item input adjoints onto the bodies (fixed incidence order)
+//     S2 adjoint (kinematic integrator; the rotation update by local D1 derivatives)
+// Costs O(26) item evaluations per item and substep instead of the column method's
+// O(13B + A) whole steps.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdlib>
+
+#include "step_device.cuh"
+#include "system.h"
+
+namespace brax {
+
+int choose_regs(const System& sys, const DPlan& P, int64_t grid);
+
+namespace {
+
+using namespace dev;
+
+struct VjpIO {
+  const float *pos, *rot, *vel, *ang, *actions;  // primal inputs [n][B][w], [n][A]
+  const float *gpos, *grot, *gvel, *gang;        // output cotangents (NULL = zero)
+  float *opos, *orot, *ovel, *oang, *oact;       // input cotangents (oact NULL = skip)
+  int64_t n_envs;
+};
+
+struct VjpArgs {
+  VjpIO io;
+  const uint32_t* blob;
+  DHeader hd;
+  int32_t plan;
+};
+
+// shared-memory layout (words) for E envs per block, one per lane
+struct VjpLayout {
+  int32_t blob, q, q0, qk, gq, fw, fa, rec, a, ga, cnt, total;
+};
+__host__ __device__ inline VjpLayout vjp_layout(int B, int J, int C, int A, int E, int blob_words) {
+  VjpLayout L;
+  const int rq = B * E * kQS;
+  L.blob = 0;
+  L.q = L.blob + round4(blob_words);
+  L.q0 = L.q + rq;
+  L.qk = L.q0 + rq;
+  L.gq = L.qk + rq;
+  L.fw = L.gq + rq;
+  L.fa = L.fw + B * E * 16;
+  L.rec = L.fa + B * E * 16;
+  int recs = (J + C) * E * 12, ia = (J + C) * E * 26;
+  L.a = L.rec + round4(recs > ia ? recs : ia);
+  L.ga = L.a + round4(A * E);
+  L.cnt = L.ga + round4(A * E);
+  L.total = L.cnt + round4(C * E);
+  return L;
+}
+
+// a body state in registers with a unit tangent on coordinate j (0-2 pos, 3-6 rot,
+// 7-9 vel, 10-12 ang; j < 0: no tangent), read from an F1 record
+template <class S> struct RegRow {
+  V3T<S> p;
+  Q4T<S> q;
+  V3T<S> v, w;
+  __device__ __forceinline__ V3T<S> pos() const { return p; }
+  __device__ __forceinline__ Q4T<S> rot() const { return q; }
+  __device__ __forceinline__ V3T<S> vel() const { return v; }
+  __device__ __forceinline__ V3T<S> ang() const { return w; }
+};
+__device__ __forceinline__ RegRow<D1> load_d1(const float* rec, int j) {
+  auto t = [&](int k) { return k == j ? 1.f : 0.f; };
+  RegRow<D1> r;
+  r.p = {{rec[0], t(0)}, {rec[1], t(1)}, {rec[2], t(2)}};
+  r.q = {{rec[4], t(3)}, {rec[5], t(4)}, {rec[6], t(5)}, {rec[7], t(6)}};
+  r.v = {{rec[8], t(7)}, {rec[9], t(8)}, {rec[10], t(9)}};
+  r.w = {{rec[12], t(10)}, {rec[13], t(11)}, {rec[14], t(12)}};
+  return r;
+}
+__device__ __forceinline__ float dot_t(V3T<D1> a, const float* g) {
+  return __fmaf_rn(a.x.t, g[0], __fmaf_rn(a.y.t, g[1], __fmul_rn(a.z.t, g[2])));
+}
+
+template <int R>
+__global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs ka) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const DHeader& H = ka.hd;
+  const DPlan& P = H.plan[ka.plan];
+  const VjpIO& io = ka.io;
+  const int B = H.B, J = H.J, C = H.C, A = H.A, E = P.E, G = P.G;
+  const VjpLayout L = vjp_layout(B, J, C, A, E, H.blob_words);
+  uint32_t* sBlob = smem + L.blob;
+  float* Q = reinterpret_cast<float*>(smem + L.q);
+  float* Q0 = reinterpret_cast<float*>(smem + L.q0);
+  float* QK = reinterpret_cast<float*>(smem + L.qk);
+  float* GQ = reinterpret_cast<float*>(smem + L.gq);
+  float* FW = reinterpret_cast<float*>(smem + L.fw);
+  float* FA = reinterpret_cast<float*>(smem + L.fa);
+  float* REC = reinterpret_cast<float*>(smem + L.rec);  // item records, then item input adjoints
+  float* IA = REC;
+  float* sA = reinterpret_cast<float*>(smem + L.a);
+  float* GA = reinterpret_cast<float*>(smem + L.ga);
+  float* sCnt = reinterpret_cast<float*>(smem + L.cnt);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  const int LG = 32 / G, grp = lane / LG, el = lane - grp * LG;
+  const int64_t e0 = int64_t(blockIdx.x) * E;
+  const int nvalid = (io.n_envs - e0 < E) ? int(io.n_envs - e0) : E;
+  const float h = H.h;
+
+  // ---- tables, primal state (identity in padded slots), cotangents, actions
+  for (int i = tid; i < H.blob_words / 4; i += nt)
+    reinterpret_cast<uint4*>(sBlob)[i] = reinterpret_cast<const uint4*>(ka.blob)[i];
+  for (int i = tid; i < B * E; i += nt) {
+    const int b = i / E, env = i - b * E;
+    float* q0 = Q0 + i * kQS;
+    float* gq = GQ + i * kQS;
+    for (int k = 0; k < kQS; ++k) q0[k] = gq[k] = 0.f;
+    q0[4] = 1.f;
+    if (env < nvalid) {
+      const int64_t g = e0 + env;
+      for (int k = 0; k < 3; ++k) {
+        q0[k] = io.pos[(g * B + b) * 3 + k];
+        q0[8 + k] = io.vel[(g * B + b) * 3 + k];
+        q0[12 + k] = io.ang[(g * B + b) * 3 + k];
+        gq[k] = io.gpos ? io.gpos[(g * B + b) * 3 + k] : 0.f;
+        gq[8 + k] = io.gvel ? io.gvel[(g * B + b) * 3 + k] : 0.f;
+        gq[12 + k] = io.gang ? io.gang[(g * B + b) * 3 + k] : 0.f;
+      }
+      for (int k = 0; k < 4; ++k) {
+        q0[4 + k] = io.rot[(g * B + b) * 4 + k];
+        gq[4 + k] = io.grot ? io.grot[(g * B + b) * 4 + k] : 0.f;
+      }
+    }
+  }
+  for (int i = tid; i < A * E; i += nt) {
+    const int k = i / E, env = i - k * E;
+    sA[i] = env < nvalid ? io.actions[(e0 + env) * A + k] : 0.f;
+    GA[i] = 0.f;
+  }
+  __syncthreads();
+
+  const DBody* bodies = reinterpret_cast<const DBody*>(sBlob + H.off_bodies);
+  const DJoint* joints = reinterpret_cast<const DJoint*>(sBlob + H.off_joints);
+  const DSlot* slots = reinterpret_cast<const DSlot*>(sBlob + H.off_slots);
+  const int32_t* item_begin = reinterpret_cast<const int32_t*>(sBlob + P.off_item_begin);
+  const int32_t* items = reinterpret_cast<const int32_t*>(sBlob + P.off_items) + grp;
+  const int32_t* body_begin = reinterpret_cast<const int32_t*>(sBlob + P.off_body_begin);
+  const int32_t* bodies_of_warp = reinterpret_cast<const int32_t*>(sBlob + P.off_bodies_of_warp) + grp;
+  const int32_t* jinc_begin = reinterpret_cast<const int32_t*>(sBlob + H.off_jinc_begin);
+  const int32_t* jinc = reinterpret_cast<const int32_t*>(sBlob + H.off_jinc);
+  const int32_t* cinc_begin = reinterpret_cast<const int32_t*>(sBlob + H.off_cinc_begin);
+  const int32_t* cinc = reinterpret_cast<const int32_t*>(sBlob + H.off_cinc);
+  const int it0 = item_begin[warp], it1 = item_begin[warp + 1];
+  const int bw0 = body_begin[warp], bw1 = body_begin[warp + 1];
+  float* sJ = REC;
+  float* sC = REC + J * E * kJS;
+
+  // ---- forward pieces on the F1 records (the step kernel's arithmetic, unfused S2)
+  auto fwd_kin = [&]() {
+    for (int i = bw0; i < bw1; ++i) {
+      const int b = bodies_of_warp[i * G];
+      if (b >= 0) kinematic<F1>(bodies[b], Row<F1>{Q + (b * LG + el) * kQS}, h);
+    }
+  };
+  auto fwd_items = [&]() {
+    for (int it = it0; it < it1; ++it) {
+      const int item = items[it * G];
+      if (item < 0) continue;
+      if (item < J) {
+        const DJoint& jt = joints[item];
+        joint<F1>(jt, Row<F1>{Q + (jt.parent * LG + el) * kQS}, Row<F1>{Q + (jt.child * LG + el) * kQS}, sA + el,
+                  E, sJ + (item * LG + el) * kJS);
+      } else {
+        const int c = item - J;
+        const DSlot& sl = slots[c];
+        F1 cnt = {0.f};
+        contact<F1>(sl, Row<F1>{Q + (sl.a * LG + el) * kQS}, Row<F1>{Q + (sl.b * LG + el) * kQS}, 1.f + H.e,
+                    H.beta_over_h, H.mu, sC + (c * LG + el) * kCS, cnt);
+      }
+    }
+  };
+  auto gather = [&](int b) {
+    Acc<F1> acc;
+    for (int k = jinc_begin[b]; k < jinc_begin[b + 1]; ++k) {
+      const int e = jinc[k];
+      acc.joint(sJ + el * kJS + (e >> 4) * (LG * kJS), e);
+    }
+    for (int k = cinc_begin[b]; k < cinc_begin[b + 1]; ++k) {
+      const int e = cinc[k];
+      acc.slot(sC + el * kCS + (e >> 4) * (LG * kCS), e);
+    }
+    return acc;
+  };
+  auto fwd_integrate = [&]() {
+    for (int i = bw0; i < bw1; ++i) {
+      const int b = bodies_of_warp[i * G];
+      if (b < 0) continue;
+      Acc<F1> acc = gather(b);
+      integrate<F1>(bodies[b], Row<F1>{Q + (b * LG + el) * kQS}, acc, h, H.g, false, nullptr, E);
+    }
+  };
+
+  for (int s = H.S - 1; s >= 0; --s) {
+    // ---- recompute: the state at the start of substep s, S2(s), the items of s
+    for (int i = tid; i < B * E * kQS / 4; i += nt)
+      reinterpret_cast<float4*>(Q)[i] = reinterpret_cast<const float4*>(Q0)[i];
+    __syncthreads();
+    for (int k = 0; k < s; ++k) {
+      fwd_kin();
+      __syncthreads();
+      fwd_items();
+      __syncthreads();
+      fwd_integrate();
+      __syncthreads();
+    }
+    for (int i = tid; i < B * E * kQS / 4; i += nt)
+      reinterpret_cast<float4*>(QK)[i] = reinterpret_cast<const float4*>(Q)[i];
+    __syncthreads();
+    fwd_kin();
+    __syncthreads();
+    fwd_items();
+    __syncthreads();
+    for (int i = bw0; i < bw1; ++i) {  // the summed forces / impulses and contact counts of s
+      const int b = bodies_of_warp[i * G];
+      if (b < 0) continue;
+      const Acc<F1> acc = gather(b);
+      float* fw = FW + (b * E + el) * 16;
+      fw[0] = acc.F.x.x; fw[1] = acc.F.y.x; fw[2] = acc.F.z.x; fw[3] = acc.cnt.x;
+      fw[4] = acc.T.x.x; fw[5] = acc.T.y.x; fw[6] = acc.T.z.x;
+      fw[8] = acc.dV.x.x; fw[9] = acc.dV.y.x; fw[10] = acc.dV.z.x;
+      fw[12] = acc.dW.x.x; fw[13] = acc.dW.y.x; fw[14] = acc.dW.z.x;
+    }
+    __syncthreads();
+
+    // ---- S7 + S8 adjoint (one thread per (body, env)): GQ holds ḡ(x', q', v'', ω'')
+    for (int i = tid; i < B * E; i += nt) {
+      const int b = i / E;
+      const DBody& bd = bodies[b];
+      float* fa = FA + i * 16;
+      for (int k = 0; k < 16; ++k) fa[k] = 0.f;
+      if (bd.is_static) continue;
+      const float* fw = FW + i * 16;
+      float* gq = GQ + i * kQS;
+      const float* q = Q + i * kQS + 4;
+      const bool iso = bd.flags & kFlagIso;
+      const float cnt = fw[3];
+      const bool hit = cnt > 0.f;
+      const float ic = hit ? __fdividef(1.f, cnt) : 0.f;
+      const float mic = __fmul_rn(bd.inv_mass, ic);
+      float av[3], aw[3], bv[3], bw[3];
+      for (int k = 0; k < 3; ++k) {
+        av[k] = hit ? bd.mpos[k] * gq[8 + k] : gq[8 + k];
+        aw[k] = hit ? bd.mrot[k] * gq[12 + k] : gq[12 + k];
+        bv[k] = bd.mpos[k] * av[k];
+        bw[k] = bd.mrot[k] * aw[k];
+      }
+      const Q4T<F1> qf{{q[0]}, {q[1]}, {q[2]}, {q[3]}};
+      const V3T<F1> gt = iw(qf, bd.inv_inertia, iso, V3T<F1>{{bw[0]}, {bw[1]}, {bw[2]}});
+      const V3T<F1> gw = iw(qf, bd.inv_inertia, iso, V3T<F1>{{aw[0]}, {aw[1]}, {aw[2]}});
+      const float gtv[3] = {gt.x.x, gt.y.x, gt.z.x}, gwv[3] = {gw.x.x, gw.y.x, gw.z.x};
+      for (int k = 0; k < 3; ++k) {
+        fa[k] = h * bd.inv_mass * bv[k];           // ḡF
+        fa[4 + k] = h * gtv[k];                    // ḡT
+        fa[8 + k] = hit ? mic * av[k] : 0.f;       // ḡdV
+        fa[12 + k] = hit ? ic * gwv[k] : 0.f;      // ḡdW
+        gq[8 + k] = bv[k];                         // ḡv (before S7)
+        gq[12 + k] = bw[k];                        // ḡω
+      }
+      if (!iso) {  // ∂(I_w⁻¹(q)·T)/∂q and ∂(I_w⁻¹(q)·dW)/∂q by local forward derivatives
+        const V3T<D1> T{{fw[4], 0.f}, {fw[5], 0.f}, {fw[6], 0.f}}, dW{{fw[12], 0.f}, {fw[13], 0.f}, {fw[14], 0.f}};
+        for (int k = 0; k < 4; ++k) {
+          Q4T<D1> qd{{q[0], k == 0 ? 1.f : 0.f}, {q[1], k == 1 ? 1.f : 0.f}, {q[2], k == 2 ? 1.f : 0.f},
+                     {q[3], k == 3 ? 1.f : 0.f}};
+          const V3T<D1> r1 = iw(qd, bd.inv_inertia, false, T);
+          float g = h * (r1.x.t * bw[0] + r1.y.t * bw[1] + r1.z.t * bw[2]);
+          if (hit) {
+            const V3T<D1> r2 = iw(qd, bd.inv_inertia, false, dW);
+            g += ic * (r2.x.t * aw[0] + r2.y.t * aw[1] + r2.z.t * aw[2]);
+          }
+          gq[4 + k] += g;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- item adjoints (warp lane group per item, lane = env): IA[item][env][26]
+    for (int it = it0; it < it1; ++it) {
+      const int item = items[it * G];
+      if (item < 0) continue;
+      float* ia = IA + (item * E + el) * 26;
+      if (item < J) {
+        const DJoint& jt = joints[item];
+        const float* fc = FA + (jt.child * E + el) * 16;
+        const float* fp = FA + (jt.parent * E + el) * 16;
+        const float gF[3] = {fc[0] - fp[0], fc[1] - fp[1], fc[2] - fp[2]};
+        const float* recP = Q + (jt.parent * LG + el) * kQS;
+        const float* recC = Q + (jt.child * LG + el) * kQS;
+        const int4 h0 = *reinterpret_cast<const int4*>(&jt), h1 = reinterpret_cast<const int4*>(&jt)[1];
+        const int n_act = h0.w >= 0 ? h0.z : 0, act_off = h1.x;
+        for (int j = 0; j < 26 + n_act; ++j) {
+          const int aj = j >= 26 ? act_off + (j - 26) : -1;
+          const JointOut<D1> o = joint_f<D1>(jt, load_d1(recP, j < 13 ? j : -1), load_d1(recC, j >= 13 ? j - 13 : -1),
+                                             [&](int k) { return D1{sA[k * E + el], k == aj ? 1.f : 0.f}; });
+          const float g = dot_t(o.f, gF) + dot_t(o.tc, fc + 4) + dot_t(o.tp, fp + 4);
+          if (j < 26) ia[j] = g;
+          else GA[aj * E + el] += g;
+        }
+      } else {
+        const DSlot& sl = slots[item - J];
+        const float* fa_ = FA + (sl.a * E + el) * 16;
+        const float* fb_ = FA + (sl.b * E + el) * 16;
+        const float gP[3] = {fa_[8] - fb_[8], fa_[9] - fb_[9], fa_[10] - fb_[10]};
+        const float gtb[3] = {-fb_[12], -fb_[13], -fb_[14]};
+        const float* recA = Q + (sl.a * LG + el) * kQS;
+        const float* recB = Q + (sl.b * LG + el) * kQS;
+        for (int j = 0; j < 26; ++j) {
+          const ContactOut<D1> o = contact_f<D1>(sl, load_d1(recA, j < 13 ? j : -1),
+                                                 load_d1(recB, j >= 13 ? j - 13 : -1), 1.f + H.e, H.beta_over_h,
+                                                 H.mu);
+          ia[j] = dot_t(o.P, gP) + dot_t(o.ta, fa_ + 12) + dot_t(o.tb, gtb);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- gather the item input adjoints onto the bodies (all bodies, fixed order)
+    for (int i = tid; i < B * E; i += nt) {
+      const int b = i / E, env = i - b * E;
+      float* gq = GQ + i * kQS;
+      auto add = [&](const float* src) {
+        for (int m = 0; m < 3; ++m) gq[m] += src[m];
+        for (int m = 0; m < 4; ++m) gq[4 + m] += src[3 + m];
+        for (int m = 0; m < 3; ++m) gq[8 + m] += src[7 + m];
+        for (int m = 0; m < 3; ++m) gq[12 + m] += src[10 + m];
+      };
+      for (int k = jinc_begin[b]; k < jinc_begin[b + 1]; ++k) {  // child side 4: inputs 13-25; parent 8: 0-12
+        const int e = jinc[k];
+        add(IA + ((e >> 4) * E + env) * 26 + ((e & 8) ? 0 : 13));
+      }
+      for (int k = cinc_begin[b]; k < cinc_begin[b + 1]; ++k) {  // A side 4: inputs 0-12; B side 8: 13-25
+        const int e = cinc[k];
+        add(IA + ((J + (e >> 4)) * E + env) * 26 + ((e & 8) ? 13 : 0));
+      }
+    }
+    __syncthreads();
+
+    // ---- S2 adjoint: (x', q') = K(x, q, v, ω) with the pre-S2 state in QK
+    for (int i = tid; i < B * E; i += nt) {
+      const int b = i / E;
+      const DBody& bd = bodies[b];
+      if (bd.is_static) continue;
+      float* gq = GQ + i * kQS;
+      const float* pre = QK + i * kQS;
+      for (int k = 0; k < 3; ++k) gq[8 + k] += h * bd.mpos[k] * gq[k];  // x' = x + h·m⊙v
+      if (!bd.rot_frozen) {
+        float gr[4], gw[3] = {0.f, 0.f, 0.f};
+        for (int j = 0; j < 7; ++j) {
+          auto t = [&](int k) { return k == j ? 1.f : 0.f; };
+          Q4T<D1> qd{{pre[4], t(0)}, {pre[5], t(1)}, {pre[6], t(2)}, {pre[7], t(3)}};
+          V3T<D1> wd{{pre[12], t(4)}, {pre[13], t(5)}, {pre[14], t(6)}};
+          if (!(bd.flags & kFlagFreeRot)) wd = had(bd.mrot, wd);
+          const Q4T<D1> qn = kin_rot(qd, wd, h);
+          const float g = qn.w.t * gq[4] + qn.x.t * gq[5] + qn.y.t * gq[6] + qn.z.t * gq[7];
+          if (j < 4) gr[j] = g;
+          else gw[j - 4] = g;
+        }
+        for (int k = 0; k < 4; ++k) gq[4 + k] = gr[k];
+        for (int k = 0; k < 3; ++k) gq[12 + k] += gw[k];
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- write the input cotangents
+  for (int i = tid; i < B * E; i += nt) {
+    const int b = i / E, env = i - b * E;
+    if (env >= nvalid) continue;
+    const int64_t g = e0 + env;
+    const float* gq = GQ + i * kQS;
+    for (int k = 0; k < 3; ++k) {
+      io.opos[(g * B + b) * 3 + k] = gq[k];
+      io.ovel[(g * B + b) * 3 + k] = gq[8 + k];
+      io.oang[(g * B + b) * 3 + k] = gq[12 + k];
+    }
+    for (int k = 0; k < 4; ++k) io.orot[(g * B + b) * 4 + k] = gq[4 + k];
+  }
+  if (io.oact)
+    for (int i = tid; i < A * E; i += nt) {
+      const int k = i / E, env = i - k * E;
+      if (env < nvalid) io.oact[(e0 + env) * A + k] = GA[i];
+    }
+}
+
+template <int R>
+cudaError_t launch_vjp_variant(const VjpArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(brax_vjp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  brax_vjp_kernel<R><<<grid, block, smem, stream>>>(ka);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, const float* const g_out[4],
+                                  float* const g_in[4], float* g_action, cudaStream_t stream) {
+  const int64_t n = primal.n_envs;
+  if (n <= 0) return cudaSuccess;
+  const DHeader& H = sys.hd;
+  int p = -1;  // the largest one-env-per-lane block whose layout fits
+  for (int q : {0, 1, 2}) {
+    const VjpLayout L = vjp_layout(H.B, H.J, H.C, H.A, H.plan[q].E, H.blob_words);
+    if (L.total * 4 <= 227 * 1024) {
+      p = q;
+      break;
+    }
+  }
+  if (p < 0) return cudaErrorInvalidValue;
+  const DPlan& P = H.plan[p];
+  const VjpLayout L = vjp_layout(H.B, H.J, H.C, H.A, P.E, H.blob_words);
+  VjpArgs ka{{primal.pos_in, primal.rot_in, primal.vel_in, primal.ang_in, primal.actions, g_out[0], g_out[1],
+              g_out[2], g_out[3], g_in[0], g_in[1], g_in[2], g_in[3], g_action, n},
+             sys.d_blob, H, p};
+  dim3 grid(unsigned((n + P.E - 1) / P.E)), block(unsigned(P.W * 32));
+  DPlan Pv = P;
+  Pv.smem_bytes = L.total * 4;
+  const int regs = choose_regs(sys, Pv, int64_t(grid.x));
+  if (regs >= 255) return launch_vjp_variant<255>(ka, grid, block, size_t(L.total) * 4, stream);
+  return launch_vjp_variant<128>(ka, grid, block, size_t(L.total) * 4, stream);
+}
+
+}  // namespace brax

@@ -136,3 +136,31 @@ def test_vjp_matches_transposed_central_differences(name):
     if o.act_dim:
         rhs = rhs + (ga.cpu().numpy() * da).sum(1)
     assert np.allclose(lhs, rhs, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("name", ["coverage", "humanoid", "grasp"])
+def test_fused_vjp_matches_the_column_vjp(name):
+    """The one-launch reverse kernel (vjp.cu) and the JVP-column assembly (diff.cu)
+    compute the same Jᵀ·g (two independent routes through the same derivative)."""
+    import os
+    text = oracle.load_scene(name)
+    o, s = oracle.Oracle(text), bx.System(text)
+    n = 70
+    qp = states(o, n, seed=11, T0=4)
+    act = synth.actions(12, 1, n, o.act_dim)[0]
+    rng = np.random.default_rng(13)
+    g = {k: rng.normal(size=v.shape).astype(np.float32) for k, v in qp.items()}
+    a_t = torch.from_numpy(act).cuda()
+    fused, fa = s.step_vjp(dev(qp), a_t, dev(g))
+    os.environ["BRAX_VJP_COLUMNS"] = "1"
+    try:
+        cols, ca = s.step_vjp(dev(qp), a_t, dev(g))
+    finally:
+        os.environ.pop("BRAX_VJP_COLUMNS")
+    for k in FIELDS:
+        x, y = fused[k].cpu().numpy(), cols[k].cpu().numpy()
+        scale = 1.0 + np.abs(y).reshape(n, -1).max(1)
+        err = np.abs(x - y).reshape(n, -1).max(1)
+        assert np.all(err <= 1e-4 * scale), (k, float((err / scale).max()))
+    x, y = fa.cpu().numpy(), ca.cpu().numpy()
+    assert np.all(np.abs(x - y).max(1) <= 1e-4 * (1 + np.abs(y).max(1)))

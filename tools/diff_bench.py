@@ -39,7 +39,11 @@ def timed(fn, reps):
 
 t_step = timed(lambda: s.step(qp, act, out), 200)
 t_jvp = timed(lambda: s.step_jvp(qp, act, dq), 50)
-t_vjp = timed(lambda: s.step_vjp(qp, act, dq), 3)
+t_vjp = timed(lambda: s.step_vjp(qp, act, dq), 10)
+os.environ["BRAX_VJP_COLUMNS"] = "1"
+t_cols = timed(lambda: s.step_vjp(qp, act, dq), 3)
+os.environ.pop("BRAX_VJP_COLUMNS")
 print(json.dumps({"scene": a.scene, "envs": n, "step_us": t_step, "jvp_us": t_jvp, "vjp_us": t_vjp,
-                  "jvp_over_step": t_jvp / t_step, "vjp_over_step": t_vjp / t_step,
-                  "vjp_launches": 2 * (13 * s.n_bodies + s.act_dim)}))
+                  "vjp_columns_us": t_cols, "jvp_over_step": t_jvp / t_step, "vjp_over_step": t_vjp / t_step,
+                  "vjp_columns_over_step": t_cols / t_step, "vjp_launches": 1,
+                  "vjp_columns_launches": 3 * (13 * s.n_bodies + s.act_dim)}))
