@@ -432,6 +432,26 @@ class System:
         brax_step_vjp(self._sys, qp_in, action, g_out, g_in, g_a, n, stream)
         return g_in, g_a
 
+    def rollout_vjp(self, qp0, actions, g_final, *, stream=None):
+        """Reverse mode through a T-step rollout (APG's "gradient of the loss through a
+        short trajectory"): forward T brax_step calls keeping every
+        state on the device, then T brax_step_vjp calls backwards.  actions [T, n, A];
+        g_final: cotangent of the final QP.  Returns (g_qp0, g_actions [T, n, A])."""
+        import torch
+        T = actions.shape[0] if actions is not None else 0
+        states = [qp0]
+        for t in range(T):
+            nxt = self.alloc_qp(qp0["pos"].shape[0])
+            self.step(states[-1], actions[t], nxt, stream=stream)
+            states.append(nxt)
+        g = g_final
+        g_a = torch.zeros_like(actions) if (actions is not None and self.act_dim) else None
+        for t in reversed(range(T)):
+            g, ga = self.step_vjp(states[t], actions[t], g, stream=stream)
+            if g_a is not None:
+                g_a[t] = ga
+        return g, g_a
+
     def step_jacobian(self, qp_in, action, *, stream=None):
         """∂Q_out/∂(Q_in, a) per env, [n, 13B, 13B + A] (rows and columns ordered
         pos | rot | vel | ang (env-major, body-major) then actions), one JVP launch

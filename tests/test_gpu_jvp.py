@@ -164,3 +164,32 @@ def test_fused_vjp_matches_the_column_vjp(name):
         assert np.all(err <= 1e-4 * scale), (k, float((err / scale).max()))
     x, y = fa.cpu().numpy(), ca.cpu().numpy()
     assert np.all(np.abs(x - y).max(1) <= 1e-4 * (1 + np.abs(y).max(1)))
+
+
+@pytest.mark.parametrize("name,T", [("pendulum", 20), ("chain2", 10), ("ant", 3)])
+def test_trajectory_gradient_matches_oracle_rollout_differences(name, T):
+    """APG-style gradient through a short trajectory: the loss
+    L = Σ (final x of body 1) over envs; ⟨∇_a L, d⟩ from rollout_vjp equals the
+    oracle rollout's central difference along random action directions d."""
+    text = oracle.load_scene(name)
+    o, s = oracle.Oracle(text), bx.System(text)
+    n = 16
+    qp = states(o, n, seed=21, T0=2)
+    acts = synth.actions(22, T, n, o.act_dim)
+    g_final = {k: torch.zeros(v.shape, device="cuda") for k, v in qp.items()}
+    g_final["pos"][:, 1, 0] = 1.0
+    _, g_a = s.rollout_vjp(dev(qp), torch.from_numpy(acts).cuda(), g_final)
+    g_a = g_a.cpu().numpy().astype(np.float64)
+    rng = np.random.default_rng(23)
+    d = rng.normal(size=acts.shape)
+
+    def loss(a):
+        q = {k: np.asarray(v, dtype=np.float64) for k, v in qp.items()}
+        for t in range(T):
+            q, _ = o.step(q, a[t], threads=8)
+        return q["pos"][:, 1, 0]
+
+    eps = 1e-5
+    fd = (loss(acts + eps * d) - loss(acts - eps * d)) / (2 * eps)
+    got = (g_a * d).sum(axis=(0, 2))
+    assert np.allclose(got, fd, rtol=2e-3, atol=2e-4 * (1 + np.abs(fd).max())), np.abs(got - fd).max()
