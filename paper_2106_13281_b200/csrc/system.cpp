@@ -3,6 +3,8 @@
 #include "system.h"
 
 #include <algorithm>
+#include <functional>
+#include <tuple>
 #include <cmath>
 #include <cstddef>
 #include <cstdlib>
@@ -294,6 +296,24 @@ System* build_host(const Config& cfg) {
     for (int c = 0; c < C; ++c)
       add({1, dslots[c].type, dslots[c].flags, dslots[c].a_static, dslots[c].b_static}, J + c);
   }
+  // dynamic bodies ordered by shape: (#joints, #contact slots incident, integrator flags)
+  std::vector<int> dyn_shaped = dyn;
+  std::function<std::tuple<int, int, int, int>(int)> body_key;
+  {
+    std::vector<int> nj(B, 0), nc(B, 0);
+    for (const Joint& j : cfg.joints) {
+      ++nj[j.parent];
+      ++nj[j.child];
+    }
+    for (const Slot& sl : cfg.slots) {
+      ++nc[sl.a];
+      ++nc[sl.b];
+    }
+    body_key = [nj, nc, &bodies](int b) {
+      return std::make_tuple(nj[b], nc[b], bodies[b].flags, bodies[b].rot_frozen);
+    };
+    std::stable_sort(dyn_shaped.begin(), dyn_shaped.end(), [&](int a, int b) { return body_key(a) < body_key(b); });
+  }
   const int env_w = [] {
     const char* e = std::getenv("BRAX_WARPS_PER_BLOCK");
     int v = e ? std::atoi(e) : 0;
@@ -314,7 +334,15 @@ System* build_host(const Config& cfg) {
         steps.push_back(st);
         step_cost.push_back(cl[k] < J ? 5 : 3);
       }
-    const int n_body_steps = (int(dyn.size()) + G - 1) / G;
+    // body steps: G bodies of one shape class each (idle slots pad a class to G)
+    std::vector<std::vector<int>> bsteps;
+    for (size_t k = 0; k < dyn_shaped.size();) {
+      std::vector<int> st(G, -1);
+      const auto cls = body_key(dyn_shaped[k]);
+      for (int g = 0; g < G && k < dyn_shaped.size() && body_key(dyn_shaped[k]) == cls; ++g) st[g] = dyn_shaped[k++];
+      bsteps.push_back(st);
+    }
+    const int n_body_steps = int(bsteps.size());
     // G = 1 (large batches, throughput-bound): ~2 item steps per warp; G > 1 (small
     // batches, latency-bound): one item step per warp (measured, profiles/)
     int W = G == 1 ? std::max(1, std::max(n_body_steps, (int(steps.size()) + 1) / 2))
@@ -345,7 +373,8 @@ System* build_host(const Config& cfg) {
       for (int k : per_warp[w])
         for (int g = 0; g < G; ++g) blob.push_back(uint32_t(steps[k][g]));
     }
-    // dynamic bodies, G per step, steps round-robin over warps
+    // dynamic bodies, G per step (bodies with the same gather / integrator shape share a
+    // step, so a warp's lane groups do not diverge), steps round-robin over warps
     std::vector<std::vector<int>> wb(W);
     for (int k = 0; k < n_body_steps; ++k) wb[k % W].push_back(k);
     P.off_body_begin = int32_t(blob.size());
@@ -357,10 +386,7 @@ System* build_host(const Config& cfg) {
     P.off_bodies_of_warp = int32_t(blob.size());
     for (int w = 0; w < W; ++w)
       for (int k : wb[w])
-        for (int g = 0; g < G; ++g) {
-          size_t i = size_t(k) * G + g;
-          blob.push_back(uint32_t(i < dyn.size() ? dyn[i] : -1));
-        }
+        for (int g = 0; g < G; ++g) blob.push_back(uint32_t(bsteps[k][g]));
   }
   // incidence lists: joints by index (child / parent side), then slots by index (A / B side)
   std::vector<std::vector<int32_t>> jinc(B), cinc(B);
