@@ -284,16 +284,27 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       for (int i = bw0; i < bw1; ++i) {
         int b = bodies_of_warp[i * G];
         if (b < 0) continue;
-        Acc<S> acc;
+        Acc<S> acc{typename Acc<S>::NoInit{}};
+        const int j0 = jinc_begin[b], j1 = jinc_begin[b + 1], c0 = cinc_begin[b], c1 = cinc_begin[b + 1];
+        if (j1 > j0) {
+          acc.joint_first(sJe + (jinc[j0] >> 4) * (LG * JS), jinc[j0]);
 #pragma unroll 4
-        for (int k = jinc_begin[b]; k < jinc_begin[b + 1]; ++k) {
-          int e = jinc[k];
-          acc.joint(sJe + (e >> 4) * (LG * JS), e);
+          for (int k = j0 + 1; k < j1; ++k) {
+            int e = jinc[k];
+            acc.joint(sJe + (e >> 4) * (LG * JS), e);
+          }
+        } else {
+          acc.zero_joints();
         }
+        if (c1 > c0) {
+          acc.slot_first(sCe + (cinc[c0] >> 4) * (LG * CS), cinc[c0]);
 #pragma unroll 4
-        for (int k = cinc_begin[b]; k < cinc_begin[b + 1]; ++k) {
-          int e = cinc[k];
-          acc.slot(sCe + (e >> 4) * (LG * CS), e);
+          for (int k = c0 + 1; k < c1; ++k) {
+            int e = cinc[k];
+            acc.slot(sCe + (e >> 4) * (LG * CS), e);
+          }
+        } else {
+          acc.zero_slots();
         }
         const bool last = s + 1 == H.S;
         const bool kin = !(last && (envm || step + 1 == a.n_steps));  // fused S2 of the next substep

@@ -719,6 +719,29 @@ template <class S> struct Acc {
     dW = axpy(sg, Lanes<S>::ld3(rec + (e & 15) * (M / 4)), dW);
     cnt = cnt + Lanes<S>::w4(rec);
   }
+  // the first entry of a list initialises the sums (no zero registers, one op less)
+  __device__ __forceinline__ void joint_first(const float* rec, int e) {
+    const float sg = (e & 8) ? -1.f : 1.f;
+    F = scale(sg, Lanes<S>::ld3(rec));
+    T = Lanes<S>::ld3(rec + (e & 15) * (M / 4));
+  }
+  __device__ __forceinline__ void slot_first(const float* rec, int e) {
+    const float sg = (e & 8) ? -1.f : 1.f;
+    dV = scale(sg, Lanes<S>::ld3(rec));
+    dW = scale(sg, Lanes<S>::ld3(rec + (e & 15) * (M / 4)));
+    cnt = Lanes<S>::w4(rec);
+  }
+  struct NoInit {};
+  __device__ __forceinline__ explicit Acc(NoInit) {}
+  __device__ __forceinline__ void zero_joints() {
+    const S z = bc<S>(0.f);
+    F = T = V3T<S>{z, z, z};
+  }
+  __device__ __forceinline__ void zero_slots() {
+    const S z = bc<S>(0.f);
+    dV = dW = V3T<S>{z, z, z};
+    cnt = z;
+  }
 };
 
 // ---- S7 + S8: potential integrator then collision integrator (R14, R21),
