@@ -86,13 +86,18 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // tracing (brax_system_phase_cycles): thread 0 times prologue / joints+contacts /
   // integrate / epilogue with clock64 (uniform branch; off unless requested)
+  // (the sums live in shared memory, not in registers held across the whole kernel)
   const bool trace = a.phase_cycles != nullptr && tid == 0;
-  long long tr_mark = trace ? clock64() : 0, tr[4] = {0, 0, 0, 0};
+  __shared__ long long sTr[5];  // per-phase sums, last mark
+  if (trace) {
+    for (int k = 0; k < 4; ++k) sTr[k] = 0;
+    sTr[4] = clock64();
+  }
   auto lap = [&](int k) {
     if (trace) {
-      long long t = clock64();
-      tr[k] += t - tr_mark;
-      tr_mark = t;
+      const long long t = clock64();
+      sTr[k] += t - sTr[4];
+      sTr[4] = t;
     }
   };
   const int grp = lane / LG, el = lane - grp * LG;  // lane group; this lane's record slot (envs el, el + LG)
@@ -396,7 +401,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   }
   if (trace) {
     lap(3);
-    for (int k = 0; k < 4; ++k) atomicAdd(&a.phase_cycles[k], (unsigned long long)tr[k]);
+    for (int k = 0; k < 4; ++k) atomicAdd(&a.phase_cycles[k], (unsigned long long)sTr[k]);
   }
 }
 
@@ -406,7 +411,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
 // alone would leave the SMs with few independent env groups to overlap their
 // per-substep barriers; G = 1 once the grid fills the GPU.
 int choose_plan(const System& sys, int64_t n_envs) {
-  auto fits = [&](int i) { return sys.hd.plan[i].smem_bytes <= 227 * 1024; };
+  auto fits = [&](int i) { return sys.hd.plan[i].smem_bytes <= kMaxDynSmem; };
   if (const char* e = std::getenv("BRAX_PLAN")) {  // "G,V" override (experiments; ignored if it does not fit)
     int g = 0, v = 0;
     if (std::sscanf(e, "%d,%d", &g, &v) == 2)
@@ -454,7 +459,7 @@ cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, 
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(brax_step_kernel<S, R, kEnv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+                                         kMaxDynSmem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
@@ -514,7 +519,7 @@ int variant_regs(int V, int regs) {
   return t[n - 1];
 }
 
-bool plan_fits(const System& sys, int p) { return sys.hd.plan[p].smem_bytes <= 227 * 1024; }
+bool plan_fits(const System& sys, int p) { return sys.hd.plan[p].smem_bytes <= kMaxDynSmem; }
 
 int64_t grid_of(const System& sys, int p, int64_t n) { return (n + sys.hd.plan[p].E - 1) / sys.hd.plan[p].E; }
 
@@ -592,9 +597,9 @@ cudaError_t launch_step_jvp(const System& sys, const StepArgs& a, cudaStream_t s
   if (a.n_envs <= 0 || a.n_steps <= 0) return cudaSuccess;
   int p = choose_plan(sys, a.n_envs);
   if (sys.hd.plan[p].V == 2) p -= 3;  // plans 3-5 are the V = 2 versions of plans 0-2
-  while (p < 2 && sys.hd.plan[p].smem_bytes_jvp > 227 * 1024) ++p;  // smaller blocks for large systems
+  while (p < 2 && sys.hd.plan[p].smem_bytes_jvp > kMaxDynSmem) ++p;  // smaller blocks for large systems
   DPlan P = sys.hd.plan[p];
-  if (P.smem_bytes_jvp > 227 * 1024) return cudaErrorInvalidValue;
+  if (P.smem_bytes_jvp > kMaxDynSmem) return cudaErrorInvalidValue;
   P.smem_bytes = P.smem_bytes_jvp;
   KArgs ka{a, sys.d_blob, sys.hd, p};
   ka.a.bulk_ok = ka.a.act_bulk_ok = 0;

@@ -430,7 +430,7 @@ System* build_host(const Config& cfg) {
   s->smem_bytes = size_t(hd.plan[0].smem_bytes);
   int smallest = hd.plan[0].smem_bytes;
   for (int pi = 0; pi < kNumPlans; ++pi) smallest = std::min(smallest, hd.plan[pi].smem_bytes);
-  if (size_t(smallest) > 227 * 1024)
+  if (size_t(smallest) > kMaxDynSmem)
     throw Error(BRAX_E_VALIDATION, "config: system too large for one block's shared memory (" +
                                        std::to_string(smallest) + " bytes with 8 envs per block)");
 

@@ -409,7 +409,7 @@ cudaError_t launch_vjp_variant(const VjpArgs& ka, dim3 grid, dim3 block, size_t 
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(brax_vjp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(brax_vjp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
@@ -427,7 +427,7 @@ cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, con
   int p = -1;  // the largest one-env-per-lane block whose layout fits
   for (int q : {0, 1, 2}) {
     const VjpLayout L = vjp_layout(H.B, H.J, H.C, H.A, H.plan[q].E, H.blob_words);
-    if (L.total * 4 <= 227 * 1024) {
+    if (L.total * 4 <= kMaxDynSmem) {
       p = q;
       break;
     }
