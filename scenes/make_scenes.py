@@ -230,9 +230,53 @@ def fetch():
     return "\n".join(out) + "\n"
 
 
+# env epilogue blocks (NEXT-1; R30-R34)
+TASKS = {
+    "ant": """# Env epilogue (NEXT-1; PAPER.md:505 "Brax's reward function ignores the contact
+# cost"; SPEC.md:366 ant reward and done): 87 observations (Table 1).
+task {
+  torso: "Torso"
+  forward { x: 1 }
+  survive_reward: 1
+  ctrl_cost: 0.5
+  healthy_z { min: 0.2 max: 1.0 }
+  episode_length: 1000
+  contact_obs: true
+  reset_noise { vel: 0.1 ang: 0.1 }
+}
+""",
+    "humanoid": """# Env epilogue (NEXT-1; PAPER.md:509: control cost 0.01, done when the torso
+# leaves [0.6, 2.1]).  Observation layout of DESIGN.md R32 (117 values; Table 1's
+# 299 uses MuJoCo-specific features the paper does not define).
+task {
+  torso: "Torso"
+  forward { x: 1 }
+  survive_reward: 1
+  ctrl_cost: 0.01
+  healthy_z { min: 0.6 max: 2.1 }
+  episode_length: 1000
+  contact_obs: true
+  reset_noise { vel: 0.1 ang: 0.1 }
+}
+""",
+    "halfcheetah": """# Env epilogue (NEXT-1; SPEC.md:366: forward velocity − 0.1·‖a‖², no survive
+# bonus, no height-based done): 25 observations (Table 1).
+task {
+  torso: "Torso"
+  forward { x: 1 }
+  survive_reward: 0
+  ctrl_cost: 0.1
+  episode_length: 1000
+  contact_obs: false
+  reset_noise { vel: 0.1 ang: 0.1 }
+}
+""",
+}
+
+
 if __name__ == "__main__":
     for name, fn in (("ant", ant), ("humanoid", humanoid), ("halfcheetah", halfcheetah),
                      ("grasp", grasp), ("fetch", fetch)):
         with open(os.path.join(HERE, f"{name}.bxc"), "w") as fh:
-            fh.write(fn())
+            fh.write(fn() + TASKS.get(name, ""))
         print("wrote", name)
