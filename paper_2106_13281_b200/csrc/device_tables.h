@@ -194,7 +194,7 @@ struct DPlan {
   int32_t G, V, E, W;  // lane groups per warp, envs per lane, envs per block E = 32·V/G, warps
   int32_t off_item_begin, off_items;          // per warp: item steps [begin, end); items[step*G + g]
   int32_t off_body_begin, off_bodies_of_warp;  // per warp: body steps; bodies[step*G + g]
-  int32_t smem_bytes, smem_bytes_jvp, pad1, pad2;  // jvp: value + tangent records (V = 1 plans)
+  int32_t smem_bytes, smem_bytes_jvp, smem_bytes_env, pad2;  // physics | JVP (V = 1 plans) | env epilogue
 };
 
 struct DHeader {            // passed by value as a kernel argument

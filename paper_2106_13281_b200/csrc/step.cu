@@ -486,7 +486,7 @@ cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs
   ka.a.phase_cycles = sys.trace ? sys.d_phase_cycles : nullptr;
   const DPlan& P = sys.hd.plan[plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
-  const size_t smem = size_t(P.smem_bytes);
+  const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);
   if (a.env) {  // env-epilogue instantiations (fewer register variants)
     if (P.V == 2) {
       if (regs >= 128) return launch_variant<F2, 128, true>(ka, grid, block, smem, stream);
@@ -623,6 +623,14 @@ LaunchConfig launch_config(const System& sys, int64_t n_envs) {
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream) {
   if (a.n_envs <= 0 || (a.n_steps <= 0 && !a.env)) return cudaSuccess;
   LaunchConfig c = launch_config(sys, a.n_envs);
+  if (a.env && sys.hd.plan[c.plan].smem_bytes_env > kMaxDynSmem) {  // epilogue regions: smaller blocks
+    int q = -1;
+    for (int p = kNumPlans - 1; p >= 0; --p)
+      if (sys.hd.plan[p].smem_bytes_env <= kMaxDynSmem && (q < 0 || sys.hd.plan[p].E > sys.hd.plan[q].E)) q = p;
+    if (q < 0) return cudaErrorInvalidValue;
+    c.plan = q;
+    c.regs = variant_regs(sys.hd.plan[q].V, choose_regs(sys, sys.hd.plan[q], grid_of(sys, q, a.n_envs)));
+  }
   // first launch of this batch size outside graph capture: measure every plan once
   if (!c.tuned && sys.autotune && a.n_envs >= 256 && a.n_steps > 0 && !std::getenv("BRAX_PLAN") &&
       !std::getenv("BRAX_MAXREG")) {
