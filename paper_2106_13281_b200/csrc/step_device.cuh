@@ -300,7 +300,7 @@ template <class S> __device__ __forceinline__ S atan2_f(S y, S x) {
 // asin(x) = atan2(x, √((1−x)(1+x))), x already clamped to [−1, 1]
 template <class S> __device__ __forceinline__ S asin_f(S x) {
   S c2 = (1.f - x) * (1.f + x);  // ≥ 0; √ via rsqrt (no IEEE slow-path call), exact 0 at |x| = 1
-  return atan2_f(x, sel(gt(c2, bc<S>(0.f)), c2 * vrsqrt(c2), bc<S>(0.f)));
+  return atan2_f(x, sel(gt(c2, bc<S>(0.f)), S(c2 * vrsqrt(c2)), bc<S>(0.f)));
 }
 
 // ---- shared-memory access for V = 1 or 2 envs per lane ---------------------------
@@ -482,7 +482,7 @@ __device__ __forceinline__ JointOut<S> joint_f(const DJoint& Jm, const RowT& P, 
   S c2 = R12 * R12 + R22 * R22;  // cos² θ1
   S ic = sel(gt(c2, bc<S>(0.f)), vrsqrt(c2), bc<S>(0.f));
   S t1 = tau[1] * ic;
-  S u = (tau[2] - tau[0] * R02) * vmin(ic * ic, bc<S>(100.f));
+  S u = (tau[2] - tau[0] * R02) * vmin(S(ic * ic), bc<S>(100.f));
   V3T<S> tj{tau[0], u * R12 + t1 * R22, u * R22 - t1 * R12};
   V3T<S> twd = rotate(fp, tj);
   if (!(flags & kJNoCa)) twd = axpy(ca_s.x, wp - wc, twd);
@@ -675,7 +675,7 @@ __device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT&
       S st = st2 * ist;
       V3T<S> th = ist * ut;
       S kt = sel(sl, eff(th), bc<S>(1.f));
-      S jt = vmin(vdiv(st, kt), mu * jn);
+      S jt = vmin(vdiv(st, kt), S(mu * jn));
       P = jn * n - jt * th;
       ta = cross(rA, P);
       tb = cross(rB, P);

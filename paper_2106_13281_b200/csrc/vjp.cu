@@ -21,6 +21,7 @@
 
 #include <cstdlib>
 
+#include "dual_k.cuh"
 #include "step_device.cuh"
 #include "system.h"
 
@@ -91,6 +92,28 @@ __device__ __forceinline__ RegRow<D1> load_d1(const float* rec, int j) {
 }
 __device__ __forceinline__ float dot_t(V3T<D1> a, const float* g) {
   return __fmaf_rn(a.x.t, g[0], __fmaf_rn(a.y.t, g[1], __fmul_rn(a.z.t, g[2])));
+}
+// K tangents at once: tangent k on item input j0 + k; this row's inputs are base..base+12
+constexpr int KT = 2;  // tangents per local evaluation
+using DT = DK<KT>;
+__device__ __forceinline__ DT mk_dt(float v, int j, int j0) {
+  DT d;
+  d.v = v;
+#pragma unroll
+  for (int k = 0; k < KT; ++k) d.t[k] = (j == j0 + k) ? 1.f : 0.f;
+  return d;
+}
+__device__ __forceinline__ RegRow<DT> load_dt(const float* rec, int base, int j0) {
+  RegRow<DT> r;
+  r.p = {mk_dt(rec[0], base, j0), mk_dt(rec[1], base + 1, j0), mk_dt(rec[2], base + 2, j0)};
+  r.q = {mk_dt(rec[4], base + 3, j0), mk_dt(rec[5], base + 4, j0), mk_dt(rec[6], base + 5, j0),
+         mk_dt(rec[7], base + 6, j0)};
+  r.v = {mk_dt(rec[8], base + 7, j0), mk_dt(rec[9], base + 8, j0), mk_dt(rec[10], base + 9, j0)};
+  r.w = {mk_dt(rec[12], base + 10, j0), mk_dt(rec[13], base + 11, j0), mk_dt(rec[14], base + 12, j0)};
+  return r;
+}
+__device__ __forceinline__ float dot_tk(const V3T<DT>& a, const float* g, int k) {
+  return __fmaf_rn(a.x.t[k], g[0], __fmaf_rn(a.y.t[k], g[1], __fmul_rn(a.z.t[k], g[2])));
 }
 
 template <int R>
@@ -309,13 +332,19 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
         const float* recC = Q + (jt.child * LG + el) * kQS;
         const int4 h0 = *reinterpret_cast<const int4*>(&jt), h1 = reinterpret_cast<const int4*>(&jt)[1];
         const int n_act = h0.w >= 0 ? h0.z : 0, act_off = h1.x;
-        for (int j = 0; j < 26 + n_act; ++j) {
-          const int aj = j >= 26 ? act_off + (j - 26) : -1;
-          const JointOut<D1> o = joint_f<D1>(jt, load_d1(recP, j < 13 ? j : -1), load_d1(recC, j >= 13 ? j - 13 : -1),
-                                             [&](int k) { return D1{sA[k * E + el], k == aj ? 1.f : 0.f}; });
-          const float g = dot_t(o.f, gF) + dot_t(o.tc, fc + 4) + dot_t(o.tp, fp + 4);
-          if (j < 26) ia[j] = g;
-          else GA[aj * E + el] += g;
+        const int n_in = 26 + n_act;  // parent row 0-12, child row 13-25, the joint's actions 26-
+        for (int j0 = 0; j0 < n_in; j0 += KT) {
+          const JointOut<DT> o =
+              joint_f<DT>(jt, load_dt(recP, 0, j0), load_dt(recC, 13, j0),
+                          [&](int k) { return mk_dt(sA[k * E + el], 26 + (k - act_off), j0); });
+#pragma unroll
+          for (int k = 0; k < KT; ++k) {
+            const int j = j0 + k;
+            if (j >= n_in) break;
+            const float g = dot_tk(o.f, gF, k) + dot_tk(o.tc, fc + 4, k) + dot_tk(o.tp, fp + 4, k);
+            if (j < 26) ia[j] = g;
+            else GA[(act_off + j - 26) * E + el] += g;
+          }
         }
       } else {
         const DSlot& sl = slots[item - J];
@@ -325,11 +354,12 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
         const float gtb[3] = {-fb_[12], -fb_[13], -fb_[14]};
         const float* recA = Q + (sl.a * LG + el) * kQS;
         const float* recB = Q + (sl.b * LG + el) * kQS;
-        for (int j = 0; j < 26; ++j) {
-          const ContactOut<D1> o = contact_f<D1>(sl, load_d1(recA, j < 13 ? j : -1),
-                                                 load_d1(recB, j >= 13 ? j - 13 : -1), 1.f + H.e, H.beta_over_h,
-                                                 H.mu);
-          ia[j] = dot_t(o.P, gP) + dot_t(o.ta, fa_ + 12) + dot_t(o.tb, gtb);
+        for (int j0 = 0; j0 < 26; j0 += KT) {
+          const ContactOut<DT> o =
+              contact_f<DT>(sl, load_dt(recA, 0, j0), load_dt(recB, 13, j0), 1.f + H.e, H.beta_over_h, H.mu);
+#pragma unroll
+          for (int k = 0; k < KT; ++k)
+            if (j0 + k < 26) ia[j0 + k] = dot_tk(o.P, gP, k) + dot_tk(o.ta, fa_ + 12, k) + dot_tk(o.tb, gtb, k);
         }
       }
     }
@@ -443,6 +473,7 @@ cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, con
   Pv.smem_bytes = L.total * 4;
   const int regs = choose_regs(sys, Pv, int64_t(grid.x));
   if (regs >= 255) return launch_vjp_variant<255>(ka, grid, block, size_t(L.total) * 4, stream);
+  if (regs >= 168) return launch_vjp_variant<168>(ka, grid, block, size_t(L.total) * 4, stream);
   return launch_vjp_variant<128>(ka, grid, block, size_t(L.total) * 4, stream);
 }
 
