@@ -643,44 +643,45 @@ __device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT&
     pt = scale(0.5f, axpy(-ra, n, pa) + axpy(rb, n, pb));
   }
   auto pen = gt(d, zero);  // R16: strict d > 0
+  // the impulse is evaluated for every env of a warp in which any env penetrates and
+  // masked (no lane divergence, no merge moves; a non-penetrating env gets jn = 0,
+  // hence P = 0); warps without a penetrating env skip it
   V3T<S> P{zero, zero, zero}, ta{zero, zero, zero}, tb{zero, zero, zero};
   S active = zero;
-  if (any(pen)) {
-    V3T<S> rA = pt - xa, rB = pt - xb;
-    V3T<S> u = cross_add(A.ang(), rA, A.vel()) - cross_add(B.ang(), rB, B.vel());
-    S un = dot(u, n);
-    const bool isa = fl & kSIsoA, isb = fl & kSIsoB;
-    const float4 iia4 = S4[8], iib4 = S4[9];
-    const float iia[3] = {iia4.x, iia4.y, iia4.z}, iib[3] = {iib4.x, iib4.y, iib4.z};
-    auto eff = [&](V3T<S> dir) {  // k(dir) = Σ_X not static [1/m_X + (r_X×dir)·I_w⁻¹(r_X×dir)]
-      S k = zero;
-      if (!a_static) {
-        V3T<S> rn = cross(rA, dir);
-        k = k + ells.z + dot(rn, iw(qa, iia, isa, rn));
-      }
-      if (!b_static) {
-        V3T<S> rn = cross(rB, dir);
-        k = k + ells.w + dot(rn, iw(qb, iib, isb, rn));
-      }
-      return k;
-    };
-    S jn = vmax(zero, vdiv(-opl_e * un + beta_over_h * d, eff(n)));
-    auto act = both(pen, gt(jn, zero));  // R15
-    if (any(act)) {
-      jn = sel(act, jn, zero);
-      V3T<S> ut = u - un * n;
-      S st2 = dot(ut, ut);
-      auto sl = gt(st2, zero);  // R16: j_t = 0 when s_t = 0
-      S ist = sel(sl, vrsqrt(st2), zero);
-      S st = st2 * ist;
-      V3T<S> th = ist * ut;
-      S kt = sel(sl, eff(th), bc<S>(1.f));
-      S jt = vmin(vdiv(st, kt), S(mu * jn));
-      P = jn * n - jt * th;
-      ta = cross(rA, P);
-      tb = cross(rB, P);
-      active = sel(act, bc<S>(1.f), bc<S>(0.f));
+  if (__any_sync(__activemask(), any(pen))) {
+  V3T<S> rA = pt - xa, rB = pt - xb;
+  V3T<S> u = cross_add(A.ang(), rA, A.vel()) - cross_add(B.ang(), rB, B.vel());
+  S un = dot(u, n);
+  const bool isa = fl & kSIsoA, isb = fl & kSIsoB;
+  const float4 iia4 = S4[8], iib4 = S4[9];
+  const float iia[3] = {iia4.x, iia4.y, iia4.z}, iib[3] = {iib4.x, iib4.y, iib4.z};
+  auto eff = [&](V3T<S> dir) {  // k(dir) = Σ_X not static [1/m_X + (r_X×dir)·I_w⁻¹(r_X×dir)]
+    S k = zero;
+    if (!a_static) {
+      V3T<S> rn = cross(rA, dir);
+      k = k + ells.z + dot(rn, iw(qa, iia, isa, rn));
     }
+    if (!b_static) {
+      V3T<S> rn = cross(rB, dir);
+      k = k + ells.w + dot(rn, iw(qb, iib, isb, rn));
+    }
+    return k;
+  };
+  S jn = vmax(zero, vdiv(-opl_e * un + beta_over_h * d, eff(n)));
+  auto act = both(pen, gt(jn, zero));  // R15
+  jn = sel(act, jn, zero);
+  V3T<S> ut = u - un * n;
+  S st2 = dot(ut, ut);
+  auto sl = gt(st2, zero);  // R16: j_t = 0 when s_t = 0
+  S ist = sel(sl, vrsqrt(st2), zero);
+  S st = st2 * ist;
+  V3T<S> th = ist * ut;
+  S kt = sel(sl, eff(th), bc<S>(1.f));
+  S jt = vmin(vdiv(st, kt), S(mu * jn));
+  P = jn * n - jt * th;
+  ta = cross(rA, P);
+  tb = cross(rB, P);
+  active = sel(act, bc<S>(1.f), bc<S>(0.f));
   }
   return ContactOut<S>{P, active, ta, tb};
 }
