@@ -328,6 +328,11 @@ template <> struct Lanes<F1> {
   static __device__ __forceinline__ F1 ld(const float* p) { return {*p}; }  // per-env scalar arrays
   static __device__ __forceinline__ void st(float* p, F1 v) { *p = v.x; }
   static __device__ __forceinline__ F1 w4(const float* p) { return {p[3]}; }  // 4th word of field 0
+  static __device__ __forceinline__ V3T<F1> ld3w(const float* p, F1& w) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    w = {a.w};
+    return {{a.x}, {a.y}, {a.z}};
+  }
 };
 template <> struct Lanes<F2> {
   static constexpr int V = 2, SL = 2, M = 8;
@@ -358,6 +363,11 @@ template <> struct Lanes<F2> {
     float2 a = *reinterpret_cast<const float2*>(p + 6);
     return {a.x, a.y};
   }
+  static __device__ __forceinline__ V3T<F2> ld3w(const float* p, F2& w) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    w = {b.z, b.w};
+    return {{a.x, a.y}, {a.z, a.w}, {b.x, b.y}};
+  }
 };
 
 template <> struct Lanes<D1> {  // one env per lane; records hold (value, tangent) pairs like F2's env pairs
@@ -387,6 +397,11 @@ template <> struct Lanes<D1> {  // one env per lane; records hold (value, tangen
   static __device__ __forceinline__ D1 w4(const float* p) {
     float2 a = *reinterpret_cast<const float2*>(p + 6);
     return {a.x, a.y};
+  }
+  static __device__ __forceinline__ V3T<D1> ld3w(const float* p, D1& w) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    w = {b.z, b.w};
+    return {{a.x, a.y}, {a.z, a.w}, {b.x, b.y}};
   }
 };
 
@@ -716,9 +731,10 @@ template <class S> struct Acc {
   }
   __device__ __forceinline__ void slot(const float* rec, int e) {
     const float sg = (e & 8) ? -1.f : 1.f;
-    dV = axpy(sg, Lanes<S>::ld3(rec), dV);
+    S act;
+    dV = axpy(sg, Lanes<S>::ld3w(rec, act), dV);  // P with its "active" word in the same loads
     dW = axpy(sg, Lanes<S>::ld3(rec + (e & 15) * (M / 4)), dW);
-    cnt = cnt + Lanes<S>::w4(rec);
+    cnt = cnt + act;
   }
   // the first entry of a list initialises the sums (no zero registers, one op less)
   __device__ __forceinline__ void joint_first(const float* rec, int e) {
@@ -728,9 +744,8 @@ template <class S> struct Acc {
   }
   __device__ __forceinline__ void slot_first(const float* rec, int e) {
     const float sg = (e & 8) ? -1.f : 1.f;
-    dV = scale(sg, Lanes<S>::ld3(rec));
+    dV = scale(sg, Lanes<S>::ld3w(rec, cnt));
     dW = scale(sg, Lanes<S>::ld3(rec + (e & 15) * (M / 4)));
-    cnt = Lanes<S>::w4(rec);
   }
   struct NoInit {};
   __device__ __forceinline__ explicit Acc(NoInit) {}
@@ -869,9 +884,11 @@ template <int V> __device__ __forceinline__ void stg_to_records(const float* stg
   const float* sr = stg + E * B * 3;
   const float* sv = sr + E * B * 4;
   const float* sw = sv + E * B * 3;
+  // consecutive threads take consecutive envs of one body: the record stores are
+  // bank-conflict free (record stride 20 / 36 words)
   if (V == 1) {
-    for (int i = threadIdx.x; i < E * B; i += blockDim.x) {
-      const int env = i / B, b = i - env * B;
+    for (int t = threadIdx.x; t < E * B; t += blockDim.x) {
+      const int b = t / E, env = t - b * E, i = env * B + b;
       float4* r = reinterpret_cast<float4*>(sQ + (b * E + env) * kQS);
       r[0] = make_float4(sp[3 * i], sp[3 * i + 1], sp[3 * i + 2], 0.f);
       r[1] = make_float4(sr[4 * i], sr[4 * i + 1], sr[4 * i + 2], sr[4 * i + 3]);
@@ -880,8 +897,8 @@ template <int V> __device__ __forceinline__ void stg_to_records(const float* stg
     }
   } else {
     const int LG = E >> 1;
-    for (int i = threadIdx.x; i < LG * B; i += blockDim.x) {
-      const int el = i / B, b = i - el * B;
+    for (int t = threadIdx.x; t < LG * B; t += blockDim.x) {
+      const int b = t / LG, el = t - b * LG, i = el * B + b;
       const int i0 = i, i1 = i + LG * B;  // staging rows of envs el and el + LG
       float4* r = reinterpret_cast<float4*>(sQ + (b * LG + el) * kQS2);
       r[0] = make_float4(sp[3 * i0], sp[3 * i1], sp[3 * i0 + 1], sp[3 * i1 + 1]);
@@ -901,8 +918,8 @@ template <int V> __device__ __forceinline__ void records_to_stg(const float* sQ,
   float* sv = sr + E * B * 4;
   float* sw = sv + E * B * 3;
   if (V == 1) {
-    for (int i = threadIdx.x; i < E * B; i += blockDim.x) {
-      const int env = i / B, b = i - env * B;
+    for (int t = threadIdx.x; t < E * B; t += blockDim.x) {
+      const int b = t / E, env = t - b * E, i = env * B + b;
       const float4* r = reinterpret_cast<const float4*>(sQ + (b * E + env) * kQS);
       float4 p = r[0], q = r[1], v = r[2], w = r[3];
       sp[3 * i] = p.x; sp[3 * i + 1] = p.y; sp[3 * i + 2] = p.z;
@@ -912,8 +929,8 @@ template <int V> __device__ __forceinline__ void records_to_stg(const float* sQ,
     }
   } else {
     const int LG = E >> 1;
-    for (int i = threadIdx.x; i < LG * B; i += blockDim.x) {
-      const int el = i / B, b = i - el * B;
+    for (int t = threadIdx.x; t < LG * B; t += blockDim.x) {
+      const int b = t / LG, el = t - b * LG, i = el * B + b;
       const int i0 = i, i1 = i + LG * B;
       const float4* r = reinterpret_cast<const float4*>(sQ + (b * LG + el) * kQS2);
       float4 p0 = r[0], p1 = r[1], q0 = r[2], q1 = r[3], v0 = r[4], v1 = r[5], w0 = r[6], w1 = r[7];
