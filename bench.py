@@ -435,7 +435,7 @@ def run_b200(args):
                    "kernel_config": system.launch_config(n)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K, "clocks": clocks,
         "env_epilogue": env_line,
-        "blowups": total_blowups,
+        "blowups": total_blowups, "substeps_per_s": value * system.substeps,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
