@@ -4,9 +4,9 @@
 // the exact transpose of brax_step_jvp's derivative (same conventions, R35).  A
 // block keeps E envs' states in shared memory and sweeps the substeps backwards:
 //   for s = S−1 … 0:
-//     recompute the state at the start of substep s from the step's input
-//     (checkpoint = the input; Σ s = S(S−1)/2 forward substeps in total), then
-//     S2(s) and the items of substep s (their contact counts and summed forces);
+//     the state at the start of substep s from a checkpoint (one forward sweep
+//     wrote all S of them to HBM), then S2(s) and the items of substep s (their
+//     contact counts and summed forces);
 //     integrator adjoint (S7, S8: linear in v, ω, F, T, dV, dW; I_w⁻¹(q) by local
 //       forward derivatives for anisotropic bodies)        — one thread per (body, env)
 //     item adjoints: each joint / contact slot's local Jacobian-transpose product,
@@ -38,6 +38,7 @@ struct VjpIO {
   const float *gpos, *grot, *gvel, *gang;        // output cotangents (NULL = zero)
   float *opos, *orot, *ovel, *oang, *oact;       // input cotangents (oact NULL = skip)
   int64_t n_envs;
+  float4* ckpt;  // [blocks][S][B·E·kQS/4]: the state at the start of every substep (one forward sweep)
 };
 
 struct VjpArgs {
@@ -235,21 +236,30 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
     }
   };
 
-  for (int s = H.S - 1; s >= 0; --s) {
-    // ---- recompute: the state at the start of substep s, S2(s), the items of s
-    for (int i = tid; i < B * E * kQS / 4; i += nt)
-      reinterpret_cast<float4*>(Q)[i] = reinterpret_cast<const float4*>(Q0)[i];
+  // ---- one forward sweep: the state at the start of every substep -> checkpoints (HBM)
+  const int nq4 = B * E * kQS / 4;
+  float4* ck = io.ckpt + int64_t(blockIdx.x) * H.S * nq4;
+  for (int i = tid; i < nq4; i += nt) reinterpret_cast<float4*>(Q)[i] = reinterpret_cast<const float4*>(Q0)[i];
+  __syncthreads();
+  for (int k = 0; k < H.S; ++k) {
+    for (int i = tid; i < nq4; i += nt) ck[int64_t(k) * nq4 + i] = reinterpret_cast<const float4*>(Q)[i];
+    if (k + 1 == H.S) break;
+    fwd_kin();
     __syncthreads();
-    for (int k = 0; k < s; ++k) {
-      fwd_kin();
-      __syncthreads();
-      fwd_items();
-      __syncthreads();
-      fwd_integrate();
-      __syncthreads();
+    fwd_items();
+    __syncthreads();
+    fwd_integrate();
+    __syncthreads();
+  }
+  __syncthreads();
+
+  for (int s = H.S - 1; s >= 0; --s) {
+    // ---- the state at the start of substep s (checkpoint), S2(s), the items of s
+    for (int i = tid; i < nq4; i += nt) {
+      const float4 v = ck[int64_t(s) * nq4 + i];
+      reinterpret_cast<float4*>(QK)[i] = v;
+      reinterpret_cast<float4*>(Q)[i] = v;
     }
-    for (int i = tid; i < B * E * kQS / 4; i += nt)
-      reinterpret_cast<float4*>(QK)[i] = reinterpret_cast<const float4*>(Q)[i];
     __syncthreads();
     fwd_kin();
     __syncthreads();
@@ -465,16 +475,22 @@ cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, con
   if (p < 0) return cudaErrorInvalidValue;
   const DPlan& P = H.plan[p];
   const VjpLayout L = vjp_layout(H.B, H.J, H.C, H.A, P.E, H.blob_words);
-  VjpArgs ka{{primal.pos_in, primal.rot_in, primal.vel_in, primal.ang_in, primal.actions, g_out[0], g_out[1],
-              g_out[2], g_out[3], g_in[0], g_in[1], g_in[2], g_in[3], g_action, n},
-             sys.d_blob, H, p};
   dim3 grid(unsigned((n + P.E - 1) / P.E)), block(unsigned(P.W * 32));
+  float4* ckpt = nullptr;
+  const size_t ck_bytes = size_t(grid.x) * H.S * H.B * P.E * kQS * 4;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ckpt), ck_bytes, stream);
+  if (e != cudaSuccess) return e;
+  VjpArgs ka{{primal.pos_in, primal.rot_in, primal.vel_in, primal.ang_in, primal.actions, g_out[0], g_out[1],
+              g_out[2], g_out[3], g_in[0], g_in[1], g_in[2], g_in[3], g_action, n, ckpt},
+             sys.d_blob, H, p};
   DPlan Pv = P;
   Pv.smem_bytes = L.total * 4;
   const int regs = choose_regs(sys, Pv, int64_t(grid.x));
-  if (regs >= 255) return launch_vjp_variant<255>(ka, grid, block, size_t(L.total) * 4, stream);
-  if (regs >= 168) return launch_vjp_variant<168>(ka, grid, block, size_t(L.total) * 4, stream);
-  return launch_vjp_variant<128>(ka, grid, block, size_t(L.total) * 4, stream);
+  if (regs >= 255) e = launch_vjp_variant<255>(ka, grid, block, size_t(L.total) * 4, stream);
+  else if (regs >= 168) e = launch_vjp_variant<168>(ka, grid, block, size_t(L.total) * 4, stream);
+  else e = launch_vjp_variant<128>(ka, grid, block, size_t(L.total) * 4, stream);
+  cudaError_t f = cudaFreeAsync(ckpt, stream);
+  return e != cudaSuccess ? e : f;
 }
 
 }  // namespace brax
