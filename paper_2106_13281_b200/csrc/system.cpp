@@ -447,6 +447,15 @@ System* build_system(const Config& cfg, int device) {
   std::memcpy(bodies.data(), blob.data() + s->hd.off_bodies, sizeof(DBody) * B);
   // ---- upload ----
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  {  // stream-ordered scratch (autotuner, reverse-mode checkpoints): keep freed blocks in the
+     // device's default pool instead of returning them to the driver at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   cuda_check(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
   cuda_check(cudaMalloc(&s->d_blob, blob.size() * 4), "cudaMalloc(blob)");
   cuda_check(cudaMemcpy(s->d_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy(blob)");

@@ -39,6 +39,7 @@ struct VjpIO {
   float *opos, *orot, *ovel, *oang, *oact;       // input cotangents (oact NULL = skip)
   int64_t n_envs;
   float4* ckpt;  // [blocks][S][B·E·kQS/4]: the state at the start of every substep (one forward sweep)
+  int32_t local_ad;  // 1: joint adjoints from value+tangent evaluations too (cross-check)
 };
 
 struct VjpArgs {
@@ -117,6 +118,164 @@ __device__ __forceinline__ float dot_tk(const V3T<DT>& a, const float* g, int k)
   return __fmaf_rn(a.x.t[k], g[0], __fmaf_rn(a.y.t[k], g[1], __fmul_rn(a.z.t[k], g[2])));
 }
 
+// ---- hand-derived adjoint of joint_f (step_device.cuh) for one env, plain fp32:
+// given the cotangents of (F, T_child, T_parent-as-stored) returns those of the
+// parent's and the child's (pos, rot, vel, ang) and of the joint's actions.  Same
+// conventions as the value+tangent path (R35): clamps pass the derivative where the
+// argument is selected (ties included), the joint angles' derivatives are the
+// analytic ones of atan2 / asin (the kernel's polynomials agree to ~1e-6).
+struct V3f { float x, y, z; };
+__device__ __forceinline__ V3f v3(float x, float y, float z) { return {x, y, z}; }
+__device__ __forceinline__ V3f operator+(V3f a, V3f b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ V3f operator-(V3f a, V3f b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3f operator*(float s, V3f a) { return {s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ float dot3(V3f a, V3f b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ V3f cross3(V3f a, V3f b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+struct Qf { float w, x, y, z; };
+__device__ __forceinline__ Qf qmulf(Qf a, Qf b) {
+  return {a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
+          a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x, a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w};
+}
+__device__ __forceinline__ Qf qconjf(Qf q) { return {q.w, -q.x, -q.y, -q.z}; }
+__device__ __forceinline__ V3f rotf(Qf q, V3f v) {
+  const V3f u{q.x, q.y, q.z};
+  return v + (2.f * q.w) * cross3(u, v) + 2.f * cross3(u, cross3(u, v));
+}
+// cotangent of q for r = rotate(q, v) (any q, not only unit ones)
+__device__ __forceinline__ Qf rot_adj_q(Qf q, V3f v, V3f g) {
+  const V3f u{q.x, q.y, q.z};
+  const V3f gu = (2.f * q.w) * cross3(v, g) + 2.f * (dot3(u, v) * g + dot3(u, g) * v - (2.f * dot3(v, g)) * u);
+  return {2.f * dot3(g, cross3(u, v)), gu.x, gu.y, gu.z};
+}
+__device__ __forceinline__ void joint_adj(const DJoint& Jm, const float* recP, const float* recC, const float* act,
+                                          int act_stride, const float* gF, const float* gTc, const float* gTp,
+                                          float* ia, float* g_act) {
+  const float4* J4 = reinterpret_cast<const float4*>(&Jm);
+  const int4 h0 = *reinterpret_cast<const int4*>(&Jm), h1 = reinterpret_cast<const int4*>(&Jm)[1];
+  const int dof = h0.z, act_kind = h0.w, act_offset = h1.x, flags = h1.y;
+  const float4 op_k = J4[2], oc_cl = J4[3], jpv = J4[4], jcv = J4[5], lo_kl = J4[6], hi_ka = J4[7], ca_s = J4[8];
+  const float lo[3] = {lo_kl.x, lo_kl.y, lo_kl.z}, hi[3] = {hi_ka.x, hi_ka.y, hi_ka.z};
+  const V3f xp{recP[0], recP[1], recP[2]}, vp{recP[8], recP[9], recP[10]}, wp{recP[12], recP[13], recP[14]};
+  const V3f xc{recC[0], recC[1], recC[2]}, vc{recC[8], recC[9], recC[10]}, wc{recC[12], recC[13], recC[14]};
+  const Qf qp{recP[4], recP[5], recP[6], recP[7]}, qc{recC[4], recC[5], recC[6], recC[7]};
+  const Qf jp{jpv.x, jpv.y, jpv.z, jpv.w}, jc{jcv.x, jcv.y, jcv.z, jcv.w};
+  const V3f op{op_k.x, op_k.y, op_k.z}, oc{oc_cl.x, oc_cl.y, oc_cl.z};
+  // ---- forward intermediates
+  const V3f rp = rotf(qp, op), rc = rotf(qc, oc);
+  const V3f dx = (xp - xc) + (rp - rc);
+  V3f f = op_k.w * dx;
+  const bool cl = !(flags & kJNoCl), ca = !(flags & kJNoCa);
+  if (cl) f = f + oc_cl.w * ((cross3(wp, rp) + vp) - (cross3(wc, rc) + vc));
+  const Qf fp = qmulf(qp, jp), fc = qmulf(qc, jc);
+  const Qf qr0 = qmulf(qconjf(fp), fc);
+  const float sg = qr0.w < 0.f ? -1.f : 1.f;
+  const Qf qr{sg * qr0.w, sg * qr0.x, sg * qr0.y, sg * qr0.z};
+  const float R02 = 2.f * (qr.x * qr.z + qr.w * qr.y), R12 = 2.f * (qr.y * qr.z - qr.w * qr.x);
+  const float R22 = 1.f - 2.f * (qr.x * qr.x + qr.y * qr.y), R01 = 2.f * (qr.x * qr.y - qr.w * qr.z);
+  const float R00 = 1.f - 2.f * (qr.y * qr.y + qr.z * qr.z);
+  const float s1 = fminf(fmaxf(R02, -1.f), 1.f);
+  const float th[3] = {atan2_f(F1{-R12}, F1{R22}).x, asin_f(F1{s1}).x, atan2_f(F1{-R01}, F1{R00}).x};
+  float tau[3];
+  for (int i = 0; i < 3; ++i) tau[i] = i < dof ? lo_kl.w * (fminf(fmaxf(th[i], lo[i]), hi[i]) - th[i]) : -(hi_ka.w * th[i]);
+  if (act_kind >= 0)
+    for (int i = 0; i < dof; ++i) {
+      const float a = act[(act_offset + i) * act_stride];
+      tau[i] += act_kind == 0 ? ca_s.y * fminf(fmaxf(a, -1.f), 1.f) : ca_s.y * (fminf(fmaxf(a, lo[i]), hi[i]) - th[i]);
+    }
+  const float c2 = R12 * R12 + R22 * R22;
+  const float ic = c2 > 0.f ? rsqrtf(c2) : 0.f;
+  const float t1 = tau[1] * ic, m = fminf(ic * ic, 100.f), u = (tau[2] - tau[0] * R02) * m;
+  const V3f tj{tau[0], u * R12 + t1 * R22, u * R22 - t1 * R12};
+  // ---- reverse
+  const V3f gTcv{gTc[0], gTc[1], gTc[2]}, gtp{-gTp[0], -gTp[1], -gTp[2]};  // tp_pos = −T_parent
+  V3f gf = v3(gF[0], gF[1], gF[2]) + cross3(gTcv, rc) + cross3(gtp, rp);
+  V3f grc = cross3(f, gTcv), grp = cross3(f, gtp);
+  const V3f gtwd = gTcv + gtp;
+  V3f gwp{0.f, 0.f, 0.f}, gwc{0.f, 0.f, 0.f}, gvp{0.f, 0.f, 0.f}, gvc{0.f, 0.f, 0.f};
+  if (ca) {
+    gwp = ca_s.x * gtwd;
+    gwc = (-ca_s.x) * gtwd;
+  }
+  Qf gfp = rot_adj_q(fp, tj, gtwd);
+  const V3f gtj = rotf(qconjf(fp), gtwd);
+  float gtau[3] = {gtj.x, 0.f, 0.f}, gR02 = 0.f, gR12 = 0.f, gR22 = 0.f, gR01 = 0.f, gR00 = 0.f;
+  const float gu = gtj.y * R12 + gtj.z * R22, gt1 = gtj.y * R22 - gtj.z * R12;
+  gR12 += gtj.y * u - gtj.z * t1;
+  gR22 += gtj.y * t1 + gtj.z * u;
+  gtau[2] += gu * m;
+  gtau[0] -= gu * m * R02;
+  gR02 -= gu * m * tau[0];
+  float gic = 0.f;
+  if (ic * ic <= 100.f) gic += gu * (tau[2] - tau[0] * R02) * 2.f * ic;
+  gtau[1] += gt1 * ic;
+  gic += gt1 * tau[1];
+  if (c2 > 0.f) {
+    const float gc2 = gic * (-0.5f * ic * ic * ic);
+    gR12 += 2.f * R12 * gc2;
+    gR22 += 2.f * R22 * gc2;
+  }
+  float gth[3] = {0.f, 0.f, 0.f};
+  if (act_kind >= 0)
+    for (int i = 0; i < dof; ++i) {
+      const float a = act[(act_offset + i) * act_stride];
+      const float l = act_kind == 0 ? -1.f : lo[i], h = act_kind == 0 ? 1.f : hi[i];
+      const float ga = (a >= l && a <= h) ? ca_s.y * gtau[i] : 0.f;
+      g_act[i] += ga;
+      if (act_kind == 1) gth[i] -= ca_s.y * gtau[i];
+    }
+  for (int i = 0; i < 3; ++i) {
+    if (i < dof) gth[i] += (th[i] >= lo[i] && th[i] <= hi[i]) ? 0.f : -lo_kl.w * gtau[i];
+    else gth[i] -= hi_ka.w * gtau[i];
+  }
+  {  // th0 = atan2(−R12, R22), th1 = asin(clamp R02), th2 = atan2(−R01, R00)
+    const float n0 = R12 * R12 + R22 * R22, n2 = R01 * R01 + R00 * R00;
+    if (n0 > 0.f) {
+      const float g0 = __fdividef(gth[0], n0);
+      gR12 -= g0 * R22;
+      gR22 += g0 * R12;
+    }
+    if (R02 > -1.f && R02 < 1.f) gR02 += gth[1] * rsqrtf((1.f - s1) * (1.f + s1));
+    if (n2 > 0.f) {
+      const float g2 = __fdividef(gth[2], n2);
+      gR01 -= g2 * R00;
+      gR00 += g2 * R01;
+    }
+  }
+  Qf gqr{2.f * qr.y * gR02 - 2.f * qr.x * gR12 - 2.f * qr.z * gR01,
+         2.f * qr.z * gR02 - 2.f * qr.w * gR12 - 4.f * qr.x * gR22 + 2.f * qr.y * gR01,
+         2.f * qr.w * gR02 + 2.f * qr.z * gR12 - 4.f * qr.y * gR22 + 2.f * qr.x * gR01 - 4.f * qr.y * gR00,
+         2.f * qr.x * gR02 + 2.f * qr.y * gR12 - 2.f * qr.w * gR01 - 4.f * qr.z * gR00};
+  const Qf gqr0{sg * gqr.w, sg * gqr.x, sg * gqr.y, sg * gqr.z};
+  // qr0 = conj(fp) ⊗ fc
+  const Qf gcf = qmulf(gqr0, qconjf(fc));
+  const Qf gfc = qmulf(fp, gqr0);
+  gfp = {gfp.w + gcf.w, gfp.x - gcf.x, gfp.y - gcf.y, gfp.z - gcf.z};
+  Qf gqp = qmulf(gfp, qconjf(jp)), gqc = qmulf(gfc, qconjf(jc));
+  if (cl) {
+    const V3f gd = oc_cl.w * gf;
+    gvp = gvp + gd;
+    gvc = gvc - gd;
+    gwp = gwp + cross3(rp, gd);
+    grp = grp + cross3(gd, wp);
+    gwc = gwc - cross3(rc, gd);
+    grc = grc - cross3(gd, wc);
+  }
+  const V3f gdx = op_k.w * gf;
+  grp = grp + gdx;
+  grc = grc - gdx;
+  const Qf a1 = rot_adj_q(qp, op, grp), a2 = rot_adj_q(qc, oc, grc);
+  gqp = {gqp.w + a1.w, gqp.x + a1.x, gqp.y + a1.y, gqp.z + a1.z};
+  gqc = {gqc.w + a2.w, gqc.x + a2.x, gqc.y + a2.y, gqc.z + a2.z};
+  const float outP[13] = {gdx.x, gdx.y, gdx.z, gqp.w, gqp.x, gqp.y, gqp.z, gvp.x, gvp.y, gvp.z, gwp.x, gwp.y, gwp.z};
+  const float outC[13] = {-gdx.x, -gdx.y, -gdx.z, gqc.w, gqc.x, gqc.y, gqc.z, gvc.x, gvc.y, gvc.z, gwc.x, gwc.y, gwc.z};
+  for (int j = 0; j < 13; ++j) {
+    ia[j] = outP[j];
+    ia[13 + j] = outC[j];
+  }
+}
+
 template <int R>
 __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs ka) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -142,6 +301,7 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
   const int64_t e0 = int64_t(blockIdx.x) * E;
   const int nvalid = (io.n_envs - e0 < E) ? int(io.n_envs - e0) : E;
   const float h = H.h;
+  const bool hand_adj = !io.local_ad;
 
   // ---- tables, primal state (identity in padded slots), cotangents, actions
   for (int i = tid; i < H.blob_words / 4; i += nt)
@@ -343,6 +503,12 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
         const int4 h0 = *reinterpret_cast<const int4*>(&jt), h1 = reinterpret_cast<const int4*>(&jt)[1];
         const int n_act = h0.w >= 0 ? h0.z : 0, act_off = h1.x;
         const int n_in = 26 + n_act;  // parent row 0-12, child row 13-25, the joint's actions 26-
+        if (hand_adj) {
+          float ga[3] = {0.f, 0.f, 0.f};
+          joint_adj(jt, recP, recC, sA + el, E, gF, fc + 4, fp + 4, ia, ga);
+          for (int k = 0; k < n_act; ++k) GA[(act_off + k) * E + el] += ga[k];
+          continue;
+        }
         for (int j0 = 0; j0 < n_in; j0 += KT) {
           const JointOut<DT> o =
               joint_f<DT>(jt, load_dt(recP, 0, j0), load_dt(recC, 13, j0),
@@ -481,7 +647,8 @@ cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, con
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ckpt), ck_bytes, stream);
   if (e != cudaSuccess) return e;
   VjpArgs ka{{primal.pos_in, primal.rot_in, primal.vel_in, primal.ang_in, primal.actions, g_out[0], g_out[1],
-              g_out[2], g_out[3], g_in[0], g_in[1], g_in[2], g_in[3], g_action, n, ckpt},
+              g_out[2], g_out[3], g_in[0], g_in[1], g_in[2], g_in[3], g_action, n, ckpt,
+              std::getenv("BRAX_VJP_LOCAL_AD") ? 1 : 0},
              sys.d_blob, H, p};
   DPlan Pv = P;
   Pv.smem_bytes = L.total * 4;
