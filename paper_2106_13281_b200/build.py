@@ -34,7 +34,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(os.path.dirname(OUT), f"obj.{os.getpid()}")
     os.makedirs(objdir, exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v" if verbose else "-O3"]
+              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v" if verbose else "-O3",
+              *os.environ.get("BRAX_NVCC_FLAGS", "").split()]  # e.g. -DBRAX_DIAG (kernel diagnostics)
 
     def compile_one(src):  # translation units compile in parallel, then one link
         obj = os.path.join(objdir, os.path.basename(src) + ".o")

@@ -161,6 +161,7 @@ struct StepArgs {
   int32_t bulk_ok;             // all QP pointers 16-byte aligned: TMA bulk staging for full blocks
   int32_t act_bulk_ok;         // actions 16-byte aligned and n·A % 4 == 0: TMA bulk action staging
   unsigned long long* phase_cycles;  // [4] per-phase SM cycles summed over blocks (tracing), or NULL
+  int32_t diag_block;          // diagnostics (BRAX_DIAG_BLOCK=b+1): block b prints per-warp clock stamps of one substep
   // env epilogue (NEXT-1): env == 0 -> physics only.  With env == 1 every step also
   // writes reward [t][n], done [t][n], obs [t][n][obs_dim] and auto-resets done envs;
   // n_steps == 0 with env == 1 only observes (obs [n][obs_dim], QP not written).

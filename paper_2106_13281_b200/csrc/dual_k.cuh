@@ -110,7 +110,7 @@ template <int K> __device__ __forceinline__ DK<K> vabs(DK<K> a) {
   return r;
 }
 template <int K> __device__ __forceinline__ DK<K> vrsqrt(DK<K> a) {  // d(a^-1/2) = −½ a^-3/2 da
-  const float r = rsqrtf(a.v);
+  const float r = rsqrt_mufu(a.v);
   const float d = __fmul_rn(-0.5f, __fmul_rn(r, __fmul_rn(r, r)));
   DK<K> o;
   o.v = r;
@@ -120,9 +120,9 @@ template <int K> __device__ __forceinline__ DK<K> vrsqrt(DK<K> a) {  // d(a^-1/2
 }
 template <int K> __device__ __forceinline__ DK<K> vdiv(DK<K> a, DK<K> b) {  // d(a/b) = (da − q db)/b
   DK<K> o;
-  o.v = __fdividef(a.v, b.v);
+  o.v = div_mufu(a.v, b.v);
 #pragma unroll
-  for (int k = 0; k < K; ++k) o.t[k] = __fdividef(__fmaf_rn(-o.v, b.t[k], a.t[k]), b.v);
+  for (int k = 0; k < K; ++k) o.t[k] = div_mufu(__fmaf_rn(-o.v, b.t[k], a.t[k]), b.v);
   return o;
 }
 template <int K> __device__ __forceinline__ DK<K> vcopysign(DK<K> a, DK<K> b) {

@@ -37,6 +37,10 @@ namespace {
 
 using namespace dev;
 
+__device__ __forceinline__ float diag_val(F1 v) { return v.x; }
+__device__ __forceinline__ float diag_val(F2 v) { return v.x; }
+__device__ __forceinline__ float diag_val(D1 v) { return v.v; }
+
 struct KArgs {
   StepArgs a;
   const uint32_t* blob;
@@ -89,6 +93,9 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   // (the sums live in shared memory, not in registers held across the whole kernel)
   const bool trace = a.phase_cycles != nullptr && tid == 0;
   __shared__ long long sTr[5];  // per-phase sums, last mark
+#ifdef BRAX_DIAG
+  __shared__ float sDiag[kMaxWarps];  // diagnostics (a.diag_block) only
+#endif
   if (trace) {
     for (int k = 0; k < 4; ++k) sTr[k] = 0;
     sTr[4] = clock64();
@@ -263,6 +270,10 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     for (int s = 0; s < H.S; ++s) {
       __syncthreads();
       lap(2);
+#ifdef BRAX_DIAG  // per-warp clock stamps of substep 3 of step 0 in one block (build with BRAX_NVCC_FLAGS=-DBRAX_DIAG)
+      const bool dg = a.diag_block && step == 0 && s == 3 && int(blockIdx.x) == a.diag_block - 1 && lane == 0;
+      long long dt0 = dg ? clock64() : 0, dt1 = 0, dt2 = 0, dtg = 0, dts = 0;
+#endif
       if (act_bulk && s == 0 && tid == 0 && step + 1 < a.n_steps) {  // prefetch next step's actions
         mbar_expect_tx(&bars[1], act_bytes);
         tma_load(sAstg, a.actions + ((step + 1) * a.n_envs + e0) * A, act_bytes, &bars[1]);
@@ -284,38 +295,44 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
           Lanes<S>::st(cp, cnt);
         }
       }
+#ifdef BRAX_DIAG
+      if (dg) dt1 = clock64();
+#endif
       __syncthreads();
       lap(1);
+#ifdef BRAX_DIAG
+      if (dg) dt2 = clock64();
+#endif
       for (int i = bw0; i < bw1; ++i) {
         int b = bodies_of_warp[i * G];
         if (b < 0) continue;
         Acc<S> acc{typename Acc<S>::NoInit{}};
         const int j0 = jinc_begin[b], j1 = jinc_begin[b + 1], c0 = cinc_begin[b], c1 = cinc_begin[b + 1];
-        if (j1 > j0) {
-          acc.joint_first(sJe + (jinc[j0] >> 4) * (LG * JS), jinc[j0]);
-#pragma unroll 4
-          for (int k = j0 + 1; k < j1; ++k) {
-            int e = jinc[k];
-            acc.joint(sJe + (e >> 4) * (LG * JS), e);
-          }
-        } else {
-          acc.zero_joints();
+        if (j1 > j0) acc.template gather<false>(jinc + j0, j1 - j0, sJe, LG * JS);
+        else acc.zero_joints();
+        if (c1 > c0) acc.template gather<true>(cinc + c0, c1 - c0, sCe, LG * CS);
+        else acc.zero_slots();
+#ifdef BRAX_DIAG
+        if (dg) {  // stamp once the gathered sums exist (the store waits for them)
+          dts = clock64();
+          sDiag[warp] = diag_val(acc.F.x) + diag_val(acc.dV.x) + diag_val(acc.cnt);
+          dtg = clock64();
         }
-        if (c1 > c0) {
-          acc.slot_first(sCe + (cinc[c0] >> 4) * (LG * CS), cinc[c0]);
-#pragma unroll 4
-          for (int k = c0 + 1; k < c1; ++k) {
-            int e = cinc[k];
-            acc.slot(sCe + (e >> 4) * (LG * CS), e);
-          }
-        } else {
-          acc.zero_slots();
-        }
+#endif
         const bool last = s + 1 == H.S;
         const bool kin = !(last && (envm || step + 1 == a.n_steps));  // fused S2 of the next substep
         integrate<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, acc, H.h, H.g, kin,
                      save_co && last ? sCo + b * 6 * RW + el * SL : nullptr, RW);
       }
+#ifdef BRAX_DIAG
+      if (dg) {
+        unsigned smid, wid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+        printf("DIAG sm %u warp %d slot %u items %d bodies %d: p1 %lld wait1 %lld p2 %lld (setup+gather issue %lld, ready %lld)\n",
+               smid, warp, wid, it1 - it0, bw1 - bw0, dt1 - dt0, dt2 - dt1, clock64() - dt2, dts - dt2, dtg - dt2);
+      }
+#endif
     }
     if (envm) {
       __syncthreads();
@@ -484,6 +501,7 @@ cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs
   ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * sys.hd.A) % 4 == 0);
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
   ka.a.phase_cycles = sys.trace ? sys.d_phase_cycles : nullptr;
+  if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
   const DPlan& P = sys.hd.plan[plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);

@@ -133,6 +133,23 @@ __device__ __forceinline__ F2 operator-(M2 m, M2 n) { return fma2(neg2(n.a), n.b
 // Derivative conventions at the method's kinks (R35):
 // min / max / clamp take the tangent of the selected argument (the first on ties),
 // selects take the selected branch's tangent, comparisons use values.
+// One MUFU instruction each: the .ftz forms skip the denormal-input rescaling that
+// rsqrtf / __fdividef wrap around MUFU.RSQ / MUFU.RCP (4 extra instructions per call).
+// For normal inputs the result is the same MUFU value (and a/b the same single-rounded
+// product a·rcp(b)); the inputs here (squared norms, clamped ratios, effective masses,
+// contact counts) are normal or exactly 0, which every call site guards.
+__device__ __forceinline__ float rsqrt_mufu(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_mufu(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float div_mufu(float a, float b) { return __fmul_rn(a, rcp_mufu(b)); }
+
 struct D1 { float v, t; };
 __device__ __forceinline__ D1 d1mul(D1 a, D1 b) {
   return {__fmul_rn(a.v, b.v), __fmaf_rn(a.t, b.v, __fmul_rn(a.v, b.t))};
@@ -176,12 +193,12 @@ __device__ __forceinline__ D1 vmin(D1 a, D1 b) { return {fminf(a.v, b.v), b.v < 
 __device__ __forceinline__ D1 vmax(D1 a, D1 b) { return {fmaxf(a.v, b.v), b.v > a.v ? b.t : a.t}; }
 __device__ __forceinline__ D1 vabs(D1 a) { return {fabsf(a.v), a.v < 0.f ? -a.t : a.t}; }
 __device__ __forceinline__ D1 vrsqrt(D1 a) {  // d(a^-1/2) = −½ a^-3/2 da
-  const float r = rsqrtf(a.v);
+  const float r = rsqrt_mufu(a.v);
   return {r, __fmul_rn(__fmul_rn(-0.5f, __fmul_rn(r, __fmul_rn(r, r))), a.t)};
 }
 __device__ __forceinline__ D1 vdiv(D1 a, D1 b) {  // d(a/b) = (da − q db)/b
-  const float q = __fdividef(a.v, b.v);
-  return {q, __fdividef(__fmaf_rn(-q, b.t, a.t), b.v)};
+  const float q = div_mufu(a.v, b.v);
+  return {q, div_mufu(__fmaf_rn(-q, b.t, a.t), b.v)};
 }
 __device__ __forceinline__ D1 vcopysign(D1 a, D1 b) {
   return {copysignf(a.v, b.v), (signbit(a.v) != signbit(b.v)) ? -a.t : a.t};
@@ -196,10 +213,10 @@ __device__ __forceinline__ F1 vmax(F1 a, F1 b) { return {fmaxf(a.x, b.x)}; }
 __device__ __forceinline__ F2 vmax(F2 a, F2 b) { return {fmaxf(a.x, b.x), fmaxf(a.y, b.y)}; }
 __device__ __forceinline__ F1 vabs(F1 a) { return {fabsf(a.x)}; }
 __device__ __forceinline__ F2 vabs(F2 a) { return {fabsf(a.x), fabsf(a.y)}; }
-__device__ __forceinline__ F1 vrsqrt(F1 a) { return {rsqrtf(a.x)}; }
-__device__ __forceinline__ F2 vrsqrt(F2 a) { return {rsqrtf(a.x), rsqrtf(a.y)}; }
-__device__ __forceinline__ F1 vdiv(F1 a, F1 b) { return {__fdividef(a.x, b.x)}; }
-__device__ __forceinline__ F2 vdiv(F2 a, F2 b) { return {__fdividef(a.x, b.x), __fdividef(a.y, b.y)}; }
+__device__ __forceinline__ F1 vrsqrt(F1 a) { return {rsqrt_mufu(a.x)}; }
+__device__ __forceinline__ F2 vrsqrt(F2 a) { return {rsqrt_mufu(a.x), rsqrt_mufu(a.y)}; }
+__device__ __forceinline__ F1 vdiv(F1 a, F1 b) { return {div_mufu(a.x, b.x)}; }
+__device__ __forceinline__ F2 vdiv(F2 a, F2 b) { return {div_mufu(a.x, b.x), div_mufu(a.y, b.y)}; }
 __device__ __forceinline__ F1 vcopysign(F1 a, F1 b) { return {copysignf(a.x, b.x)}; }
 __device__ __forceinline__ F2 vcopysign(F2 a, F2 b) { return {copysignf(a.x, b.x), copysignf(a.y, b.y)}; }
 __device__ __forceinline__ bool lt(F1 a, F1 b) { return a.x < b.x; }
@@ -746,6 +763,55 @@ template <class S> struct Acc {
     const float sg = (e & 8) ? -1.f : 1.f;
     dV = scale(sg, Lanes<S>::ld3w(rec, cnt));
     dW = scale(sg, Lanes<S>::ld3(rec + (e & 15) * (M / 4)));
+  }
+  // Gather of a whole incidence list (joints: jl[0..nj), slots: cl[0..nc)) in pairs:
+  // a pair's list entries and records are all loaded before the first of them is
+  // summed (one shared-memory round trip per chunk instead of one per entry; the sums
+  // keep the list order, R29).  jrec / crec: this lane's record of joint / slot 0;
+  // jstride / cstride: words between consecutive items' records.
+  template <bool kSlot>
+  __device__ __forceinline__ void add(const V3T<S>& a, const V3T<S>& b, S w, float sg) {
+    if (kSlot) {
+      dV = axpy(sg, a, dV);
+      dW = axpy(sg, b, dW);
+      cnt = cnt + w;
+    } else {
+      F = axpy(sg, a, F);
+      T = T + b;
+    }
+  }
+  template <bool kSlot>
+  __device__ __forceinline__ void ld(const float* rec0, int stride, int e, V3T<S>& a, V3T<S>& b, S& w) {
+    const float* rec = rec0 + (e >> 4) * stride;
+    if (kSlot) a = Lanes<S>::ld3w(rec, w);
+    else a = Lanes<S>::ld3(rec);
+    b = Lanes<S>::ld3(rec + (e & 15) * (M / 4));
+  }
+  template <bool kSlot>
+  __device__ __forceinline__ void gather(const int32_t* list, int n, const float* rec0, int stride) {
+    V3T<S> a0, b0, a1, b1;
+    S w0, w1;
+    int e0 = list[0], e1 = list[n > 1 ? 1 : 0];
+    ld<kSlot>(rec0, stride, e0, a0, b0, w0);
+    ld<kSlot>(rec0, stride, e1, a1, b1, w1);
+    const float s0 = (e0 & 8) ? -1.f : 1.f;
+    if (kSlot) {
+      dV = scale(s0, a0);
+      dW = scale(s0, b0);
+      cnt = w0;
+    } else {
+      F = scale(s0, a0);
+      T = b0;
+    }
+    if (n > 1) add<kSlot>(a1, b1, w1, (e1 & 8) ? -1.f : 1.f);
+    for (int k = 2; k < n; k += 2) {
+      e0 = list[k];
+      e1 = list[k + 1 < n ? k + 1 : k];
+      ld<kSlot>(rec0, stride, e0, a0, b0, w0);
+      ld<kSlot>(rec0, stride, e1, a1, b1, w1);
+      add<kSlot>(a0, b0, w0, (e0 & 8) ? -1.f : 1.f);
+      if (k + 1 < n) add<kSlot>(a1, b1, w1, (e1 & 8) ? -1.f : 1.f);
+    }
   }
   struct NoInit {};
   __device__ __forceinline__ explicit Acc(NoInit) {}

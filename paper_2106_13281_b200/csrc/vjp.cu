@@ -185,7 +185,7 @@ __device__ __forceinline__ void joint_adj(const DJoint& Jm, const float* recP, c
       tau[i] += act_kind == 0 ? ca_s.y * fminf(fmaxf(a, -1.f), 1.f) : ca_s.y * (fminf(fmaxf(a, lo[i]), hi[i]) - th[i]);
     }
   const float c2 = R12 * R12 + R22 * R22;
-  const float ic = c2 > 0.f ? rsqrtf(c2) : 0.f;
+  const float ic = c2 > 0.f ? rsqrt_mufu(c2) : 0.f;
   const float t1 = tau[1] * ic, m = fminf(ic * ic, 100.f), u = (tau[2] - tau[0] * R02) * m;
   const V3f tj{tau[0], u * R12 + t1 * R22, u * R22 - t1 * R12};
   // ---- reverse
@@ -232,13 +232,13 @@ __device__ __forceinline__ void joint_adj(const DJoint& Jm, const float* recP, c
   {  // th0 = atan2(−R12, R22), th1 = asin(clamp R02), th2 = atan2(−R01, R00)
     const float n0 = R12 * R12 + R22 * R22, n2 = R01 * R01 + R00 * R00;
     if (n0 > 0.f) {
-      const float g0 = __fdividef(gth[0], n0);
+      const float g0 = div_mufu(gth[0], n0);
       gR12 -= g0 * R22;
       gR22 += g0 * R12;
     }
-    if (R02 > -1.f && R02 < 1.f) gR02 += gth[1] * rsqrtf((1.f - s1) * (1.f + s1));
+    if (R02 > -1.f && R02 < 1.f) gR02 += gth[1] * rsqrt_mufu((1.f - s1) * (1.f + s1));
     if (n2 > 0.f) {
-      const float g2 = __fdividef(gth[2], n2);
+      const float g2 = div_mufu(gth[2], n2);
       gR01 -= g2 * R00;
       gR00 += g2 * R01;
     }
@@ -450,7 +450,7 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
       const bool iso = bd.flags & kFlagIso;
       const float cnt = fw[3];
       const bool hit = cnt > 0.f;
-      const float ic = hit ? __fdividef(1.f, cnt) : 0.f;
+      const float ic = hit ? div_mufu(1.f, cnt) : 0.f;
       const float mic = __fmul_rn(bd.inv_mass, ic);
       float av[3], aw[3], bv[3], bw[3];
       for (int k = 0; k < 3; ++k) {

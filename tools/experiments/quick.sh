@@ -1,4 +1,4 @@
+# quick kernel timing: ant 8192 / 65536 with the autotuned configuration, then forced (G,V) = (2,2)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/sweep.py --scenes ant,humanoid,halfcheetah,grasp,fetch --envs 2048,4096,8192,65536 > gpurun_out/sweep_def.log 2>&1
-timeout 300 python tools/phases.py --scenes ant --envs 8192 > gpurun_out/phases.log 2>&1
+timeout 300 python tools/sweep.py --scenes ant --envs 8192,65536 --steps 200 > gpurun_out/quick.log 2>&1
+BRAX_MAXREG=96 timeout 300 python tools/sweep.py --scenes ant,humanoid,grasp --envs 8192 --groups 2:2 --steps 200 >> gpurun_out/quick.log 2>&1
