@@ -261,14 +261,16 @@ def run_b200(args):
     value = total_env_steps / (ms_max / 1e3)
 
     # e2e through the public API with host buffers: every step copies its inputs (qp +
-    # action) from pinned host memory, steps, and copies the resulting qp back.  Steps
-    # rotate over NS streams (independent env batches), so one batch's copies overlap
-    # another's kernel: the copy engines and the SMs work concurrently, as in a
-    # pipelined production loop.  Timed on the device from a start event that every
-    # stream waits on to the last stream's completion.
+    # action) from pinned host memory, steps, and copies the resulting qp back.  A
+    # three-stage pipeline over NB independent env batches: one stream per stage
+    # (H2D copy | brax_step | D2H copy) chained by events, so step i's upload, step
+    # i-1's kernel and step i-2's download run at once on the two copy engines and the
+    # SMs (tools/experiments/e2e_pipe.py: +7 % over round-robin streams; PCIe-bound).
+    # Timed on the device from a start event every stage stream waits on to the last
+    # download's completion.
     e2e = None
     if rank == 0 or world > 1:
-        NS = 3
+        NB = 6
         # one contiguous buffer per batch: pos | rot | vel | ang | actions (the brax_qp
         # members point into it), so each direction is a single copy per step
         sizes = [n * B * 3, n * B * 4, n * B * 3, n * B * 3]
@@ -282,7 +284,7 @@ def run_b200(args):
             return out, (flat[o:o + n * A].view(n, A) if A else None)
 
         host_in, host_out, dflat = [], [], []
-        for r in range(NS):
+        for r in range(NB):
             h = torch.empty(nq + n * A, dtype=torch.float32).pin_memory()
             hq, ha = views(h)
             for k in hq:
@@ -293,28 +295,40 @@ def run_b200(args):
             host_out.append(torch.empty(nq, dtype=torch.float32).pin_memory())
             dflat.append(torch.empty(nq + n * A, dtype=torch.float32, device=dev))
         dviews = [views(f) for f in dflat]
-        streams = [torch.cuda.Stream(device=dev) for _ in range(NS)]
-        Ke = max(NS, min(args.e2e_steps, K))
+        s_in, s_k, s_out = (torch.cuda.Stream(device=dev) for _ in range(3))
+        ev_in = [torch.cuda.Event() for _ in range(NB)]
+        ev_k = [torch.cuda.Event() for _ in range(NB)]
+        ev_out = [torch.cuda.Event() for _ in range(NB)]
+        used = [False] * NB
+        Ke = max(NB, min(args.e2e_steps, K))
 
         def e2e_step(i):
-            j = i % NS
-            with torch.cuda.stream(streams[j]):
+            j = i % NB
+            if used[j]:
+                s_in.wait_event(ev_out[j])  # batch j's buffer is free once its last result left
+            with torch.cuda.stream(s_in):
                 dflat[j].copy_(host_in[j], non_blocking=True)
-                dq, da = dviews[j]
-                system.step(dq, da, dq, stream=streams[j])
+                ev_in[j].record(s_in)
+            s_k.wait_event(ev_in[j])
+            dq, da = dviews[j]
+            system.step(dq, da, dq, stream=s_k)
+            ev_k[j].record(s_k)
+            s_out.wait_event(ev_k[j])
+            with torch.cuda.stream(s_out):
                 host_out[j].copy_(dflat[j][:nq], non_blocking=True)
+                ev_out[j].record(s_out)
+            used[j] = True
 
-        for i in range(2 * NS):
+        for i in range(2 * NB):
             e2e_step(i)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for st in streams:
+        for st in (s_in, s_k, s_out):
             st.wait_event(e0)
         for i in range(Ke):
             e2e_step(i)
-        for st in streams:
-            stream.wait_stream(st)
+        stream.wait_stream(s_out)
         e1.record(stream)
         e1.synchronize()
         e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -322,10 +336,10 @@ def run_b200(args):
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": n * world * Ke / (float(e_ms[0]) / 1e3), "unit": "env-steps/s",
                "h2d_bytes_per_step": int(qp_bytes + n * A * 4), "d2h_bytes_per_step": int(qp_bytes),
-               "steps": Ke, "streams": NS,
+               "steps": Ke, "batches": NB,
                "path": "pinned host -> one cudaMemcpyAsync (qp + actions) -> brax_step -> one cudaMemcpyAsync (qp) "
-                       f"-> pinned host, every step; {NS} streams round-robin over independent batches "
-                       "(copies overlap kernels)"}
+                       f"-> pinned host, every step; three-stage stream pipeline (upload | step | download) over "
+                       f"{NB} independent batches"}
 
     # NEXT-1: the same workload through brax_env_step (reward, done, auto-reset and
     # observations fused into the step), when the scene has a task block
