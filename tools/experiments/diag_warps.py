@@ -1,6 +1,6 @@
-"""Per-warp clock stamps of one substep (BRAX_DIAG_BLOCK): phase-1 work, wait at the
-mid barrier, phase-2 work (+ wait at the next barrier is the remainder).
-    BRAX_DIAG_BLOCK=1 BRAX_PLAN=2,2 python tools/experiments/diag_warps.py [n_envs] [scene]"""
+"""Per-warp clock stamps of one substep (build with BRAX_NVCC_FLAGS=-DBRAX_DIAG):
+phase-1 work, wait at the mid barrier, phase-2 work.
+    BRAX_DIAG_BLOCK=1 BRAX_PLAN=2,2 python tools/experiments/diag_warps.py [n_envs] [scene | path.bxc]"""
 import os
 import sys
 
@@ -13,7 +13,8 @@ import synth  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 scene = sys.argv[2] if len(sys.argv) > 2 else "ant"
-s = bx.System(open(os.path.join(ROOT, "scenes", f"{scene}.bxc")).read())
+path = scene if scene.endswith(".bxc") else os.path.join(ROOT, "scenes", f"{scene}.bxc")
+s = bx.System(open(path).read())
 qp = s.alloc_qp(n)
 s.reset(qp, 0, 0.1, 0.1)
 acts = torch.from_numpy(synth.actions(1, 20, n, s.act_dim)).cuda()
