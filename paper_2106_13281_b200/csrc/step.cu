@@ -100,8 +100,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     for (int k = 0; k < 4; ++k) sTr[k] = 0;
     sTr[4] = clock64();
   }
-  auto lap = [&](int k) {
-    if (trace) {
+  auto lap = [&](int k) {  // re-tests the (uniform) argument instead of holding `trace` in a register
+    if (a.phase_cycles != nullptr && threadIdx.x == 0) {
       const long long t = clock64();
       sTr[k] += t - sTr[4];
       sTr[4] = t;
@@ -267,6 +267,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         for (int k = 0; k < SL; ++k) sCnt[(item - J) * RW + el * SL + k] = 0.f;
       }
     }
+    const bool pf_act = act_bulk && tid == 0 && step + 1 < a.n_steps;
     for (int s = 0; s < H.S; ++s) {
       __syncthreads();
       lap(2);
@@ -274,7 +275,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       const bool dg = a.diag_block && step == 0 && s == 3 && int(blockIdx.x) == a.diag_block - 1 && lane == 0;
       long long dt0 = dg ? clock64() : 0, dt1 = 0, dt2 = 0, dtg = 0, dts = 0;
 #endif
-      if (act_bulk && s == 0 && tid == 0 && step + 1 < a.n_steps) {  // prefetch next step's actions
+      if (s == 0 && pf_act) {  // prefetch next step's actions
         mbar_expect_tx(&bars[1], act_bytes);
         tma_load(sAstg, a.actions + ((step + 1) * a.n_envs + e0) * A, act_bytes, &bars[1]);
       }
