@@ -320,6 +320,34 @@ template <class S> __device__ __forceinline__ S asin_f(S x) {
   return atan2_f(x, sel(gt(c2, bc<S>(0.f)), S(c2 * vrsqrt(c2)), bc<S>(0.f)));
 }
 
+// Small-argument forms for the joint angles of the constrained (alignment) axes, whose
+// values are small: odd Taylor polynomials, truncation ≤ 3e-10 (|x| ≤ 0.25) — exact to
+// fp32 like the general forms above.  joint_f evaluates the general forms only when a
+// lane of the warp is outside the range and selects per lane, so an env's result
+// depends on its own state alone (bitwise the same under every launch plan).
+template <class S> __device__ __forceinline__ S asin_small(S x) {  // |x| ≤ 0.25
+  S s = x * x;
+  S p = bc<S>(0.017352764423076924f);  // 231/13312
+  p = p * s + 0.022372159090909091f;    // 63/2816
+  p = p * s + 0.030381944444444444f;    // 35/1152
+  p = p * s + 0.044642857142857144f;    // 5/112
+  p = p * s + 0.075f;                   // 3/40
+  p = p * s + 0.16666666666666666f;     // 1/6
+  return S(x * s) * p + x;
+}
+template <class S> __device__ __forceinline__ S atan_small(S t) {  // |t| ≤ 0.25
+  S s = t * t;
+  S p = bc<S>(0.07692307692307693f);  // 1/13
+  p = p * s + -0.09090909090909091f;   // −1/11
+  p = p * s + 0.1111111111111111f;     // 1/9
+  p = p * s + -0.14285714285714285f;   // −1/7
+  p = p * s + 0.2f;                    // 1/5
+  p = p * s + -0.3333333333333333f;    // −1/3
+  return S(t * s) * p + t;
+}
+__device__ __forceinline__ bool allv(bool m) { return m; }
+__device__ __forceinline__ bool allv(B2 m) { return m.x && m.y; }
+
 // ---- shared-memory access for V = 1 or 2 envs per lane ---------------------------
 // Records (device_tables.h): V = 1 — field f at words 4f..4f+3 of the env's record;
 // V = 2 — one record per lane, both envs interleaved: field f at words 8f..8f+7 as
@@ -490,7 +518,16 @@ __device__ __forceinline__ JointOut<S> joint_f(const DJoint& Jm, const RowT& P, 
   S R22 = 1.f - 2.f * (qr.x * qr.x + qr.y * qr.y);
   S R01 = 2.f * (qr.x * qr.y - qr.w * qr.z);
   S R00 = 1.f - 2.f * (qr.y * qr.y + qr.z * qr.z);
-  S th[3] = {atan2_f(-R12, R22), asin_f(clampv(R02, -1.f, 1.f)), atan2_f(-R01, R00)};
+  // θ1 and θ2: small-argument forms where every lane's argument is small (the
+  // alignment errors of constrained axes), else the general forms, selected per lane
+  const S x1 = clampv(R02, -1.f, 1.f);
+  const auto small1 = gt(bc<S>(0.25f), vabs(x1));
+  const auto small2 = both(gt(R00, bc<S>(0.f)), gt(S(0.25f * R00), vabs(R01)));
+  S th[3] = {atan2_f(-R12, R22), asin_small(x1), atan_small(vdiv(-R01, R00))};
+  if (__any_sync(__activemask(), !(allv(small1) && allv(small2)))) {
+    th[1] = sel(small1, th[1], asin_f(x1));
+    th[2] = sel(small2, th[2], atan2_f(-R01, R00));
+  }
   S tau[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
