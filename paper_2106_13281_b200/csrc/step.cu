@@ -304,6 +304,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
 #ifdef BRAX_DIAG
       if (dg) dt2 = clock64();
 #endif
+      const bool last = s + 1 == H.S;
+      const bool kin = !(last && (envm || step + 1 == a.n_steps));  // fused S2 of the next substep
       for (int i = bw0; i < bw1; ++i) {
         int b = bodies_of_warp[i * G];
         if (b < 0) continue;
@@ -320,8 +322,6 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
           dtg = clock64();
         }
 #endif
-        const bool last = s + 1 == H.S;
-        const bool kin = !(last && (envm || step + 1 == a.n_steps));  // fused S2 of the next substep
         integrate<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, acc, H.h, H.g, kin,
                      save_co && last ? sCo + b * 6 * RW + el * SL : nullptr, RW);
       }
