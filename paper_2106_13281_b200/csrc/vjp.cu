@@ -276,6 +276,197 @@ __device__ __forceinline__ void joint_adj(const DJoint& Jm, const float* recP, c
   }
 }
 
+// ---- hand-derived adjoint of contact_f (step_device.cuh) for the plane contacts
+// (types 0-2: sphere, capsule end, box corner vs a plane), one env, plain fp32 reverse
+// after a forward pass that repeats contact_f<F1>'s operations (so every decision —
+// penetration, activity, the friction clamp — is taken on the same values).  Given the
+// cotangents of (P, r_A×P, r_B×P) returns those of body A's and body B's (pos, rot,
+// vel, ang).  Conventions as in the value+tangent path (R35): max / min pass the
+// derivative to the selected argument (the first on ties), an inactive slot has zero
+// derivative.  Returns false for the shape–shape types (the caller then uses the
+// local value+tangent evaluations).
+__device__ __forceinline__ V3f v3of(V3T<F1> a) { return {a.x.x, a.y.x, a.z.x}; }
+__device__ __forceinline__ V3T<F1> v3t(V3f a) { return {{a.x}, {a.y}, {a.z}}; }
+// cotangent of q for n = rotate(q, ẑ) (contact_f's rotate_z)
+__device__ __forceinline__ Qf rotz_adj_q(Qf q, V3f g) {
+  return {2.f * (q.y * g.x - q.x * g.y), 2.f * (q.z * g.x - q.w * g.y) - 4.f * q.x * g.z,
+          2.f * (q.w * g.x + q.z * g.y) - 4.f * q.y * g.z, 2.f * (q.x * g.x + q.y * g.y)};
+}
+__device__ __forceinline__ Qf qaddf(Qf a, Qf b) { return {a.w + b.w, a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ bool contact_adj(const DSlot& SLm, const float* recA, const float* recB, float opl_e,
+                                            float beta_over_h, float mu, const float* gPv, const float* gtav,
+                                            const float* gtbv, float* ia) {
+  const float4* S4 = reinterpret_cast<const float4*>(&SLm);
+  const int4 h0 = *reinterpret_cast<const int4*>(&SLm), h1 = reinterpret_cast<const int4*>(&SLm)[1];
+  const int type = h0.x, a_static = h1.x, b_static = h1.y, fl = h1.z;
+  if (type > 2) return false;
+  for (int j = 0; j < 26; ++j) ia[j] = 0.f;
+  const float4 ca = S4[2], cb = S4[4], ells = S4[6], ra4 = S4[3], rb4 = S4[5], k4 = S4[7];
+  const float ra = ca.w;
+  const float4 iia4 = S4[8], iib4 = S4[9];
+  const float iia[3] = {iia4.x, iia4.y, iia4.z}, iib[3] = {iib4.x, iib4.y, iib4.z};
+  const bool isa = fl & kSIsoA, isb = fl & kSIsoB;
+  const Row<F1> A{const_cast<float*>(recA)}, B{const_cast<float*>(recB)};
+  // ---- forward, as contact_f<F1>
+  const Q4T<F1> qa = A.rot(), qb = B.rot();
+  const V3T<F1> xa = A.pos(), xb = B.pos();
+  const V3T<F1> cA = (fl & kSZeroPa) ? xa : xa + rotate(qa, V3T<F1>{{ca.x}, {ca.y}, {ca.z}});
+  const V3T<F1> cB = (fl & kSZeroPb) ? xb : xb + rotate(qb, V3T<F1>{{cb.x}, {cb.y}, {cb.z}});
+  Q4T<F1> qA = qa, qB = qb;
+  if (!(fl & kSIdentA)) qA = qmul(qa, Q4T<F1>{{ra4.x}, {ra4.y}, {ra4.z}, {ra4.w}});
+  if (!(fl & kSIdentB)) qB = qmul(qb, Q4T<F1>{{rb4.x}, {rb4.y}, {rb4.z}, {rb4.w}});
+  const V3T<F1> n = rotate_z(qB);
+  V3T<F1> c, pt;
+  F1 d;
+  if (type == 2) {
+    c = cA + rotate(qA, V3T<F1>{{k4.x}, {k4.y}, {k4.z}});
+    d = -dot(c - cB, n);
+    pt = c;
+  } else {
+    c = (type == 1) ? axpy(ells.x, rotate_z(qA), cA) : cA;
+    d = ra - dot(c - cB, n);
+    pt = axpy(-ra, n, c);
+  }
+  if (!(d.x > 0.f)) return true;  // R16: not penetrating, zero derivative
+  const V3T<F1> rA = pt - xa, rB = pt - xb;
+  const V3T<F1> u = cross_add(A.ang(), rA, A.vel()) - cross_add(B.ang(), rB, B.vel());
+  const F1 un = dot(u, n);
+  auto eff = [&](V3T<F1> dir) {
+    F1 k = {0.f};
+    if (!a_static) {
+      V3T<F1> rn = cross(rA, dir);
+      k = k + ells.z + dot(rn, iw(qa, iia, isa, rn));
+    }
+    if (!b_static) {
+      V3T<F1> rn = cross(rB, dir);
+      k = k + ells.w + dot(rn, iw(qb, iib, isb, rn));
+    }
+    return k;
+  };
+  const F1 kn = eff(n);
+  const F1 num = -opl_e * un + beta_over_h * d;
+  const F1 raw = vdiv(num, kn);
+  if (!(raw.x > 0.f)) return true;  // R15: inactive (jn = 0), zero derivative
+  const F1 jn = raw;
+  const V3T<F1> ut = u - un * n;
+  const F1 st2 = dot(ut, ut);
+  const bool sl = st2.x > 0.f;
+  const F1 ist = sl ? vrsqrt(st2) : F1{0.f};
+  const F1 st = st2 * ist;
+  const V3T<F1> th = ist * ut;
+  const F1 kt = sl ? eff(th) : F1{1.f};
+  const F1 q = vdiv(st, kt), mjn = mu * jn;
+  const bool fric_q = !(mjn.x < q.x);  // jt = min(q, μ·jn): q selected (first on ties)
+  const F1 jt = fric_q ? q : mjn;
+  const V3T<F1> Pv = jn * n - jt * th;
+  // ---- reverse (plain fp32)
+  const V3f P = v3of(Pv), vn = v3of(n), vrA = v3of(rA), vrB = v3of(rB), vu = v3of(u), vth = v3of(th), vut = v3of(ut);
+  const V3f gta{gtav[0], gtav[1], gtav[2]}, gtb{gtbv[0], gtbv[1], gtbv[2]};
+  V3f gP = v3(gPv[0], gPv[1], gPv[2]) + cross3(gta, vrA) + cross3(gtb, vrB);  // t = r×P: ḡP += ḡt×r
+  V3f grA = cross3(P, gta), grB = cross3(P, gtb);                               // ḡr += P×ḡt
+  // P = jn·n − jt·th
+  float gjn = dot3(gP, vn), gjt = -dot3(gP, vth);
+  V3f gn = jn.x * gP, gth = (-jt.x) * gP;
+  float gst = 0.f, gkt = 0.f;
+  if (fric_q) {  // q = st / kt
+    const float ikt = div_mufu(1.f, kt.x);
+    gst += gjt * ikt;
+    gkt -= gjt * q.x * ikt;
+  } else {
+    gjn += mu * gjt;
+  }
+  float gst2 = 0.f, gist = 0.f;
+  V3f gut{0.f, 0.f, 0.f};
+  // eff(dir): Σ_X not static (1/m_X + w·M_X w), w = r_X × dir, M_X = I_w⁻¹(q_X) (symmetric)
+  float gq_a[4] = {0.f, 0.f, 0.f, 0.f}, gq_b[4] = {0.f, 0.f, 0.f, 0.f};
+  auto eff_adj = [&](V3f dir, float g, V3f& gdir) {
+    auto side = [&](bool st_, const Q4T<F1>& qx, const float* ii, bool iso, V3f r, V3f& gr, float* gq) {
+      if (st_) return;
+      const V3f w = cross3(r, dir);
+      const V3f Mw = v3of(iw(qx, ii, iso, v3t(w)));
+      const V3f gw = (2.f * g) * Mw;
+      gr = gr + cross3(dir, gw);   // w = r×dir: ḡr += dir×ḡw
+      gdir = gdir + cross3(gw, r); // ḡdir += ḡw×r
+      if (!iso) {  // ∂(w·M(q)w)/∂q by local forward derivatives
+        for (int k = 0; k < 4; ++k) {
+          Q4T<D1> qd{{qx.w.x, k == 0 ? 1.f : 0.f}, {qx.x.x, k == 1 ? 1.f : 0.f}, {qx.y.x, k == 2 ? 1.f : 0.f},
+                     {qx.z.x, k == 3 ? 1.f : 0.f}};
+          const V3T<D1> wd{{w.x, 0.f}, {w.y, 0.f}, {w.z, 0.f}};
+          const V3T<D1> m = iw(qd, ii, false, wd);
+          gq[k] += g * (w.x * m.x.t + w.y * m.y.t + w.z * m.z.t);
+        }
+      }
+    };
+    side(a_static, qa, iia, isa, vrA, grA, gq_a);
+    side(b_static, qb, iib, isb, vrB, grB, gq_b);
+  };
+  if (sl) {
+    eff_adj(vth, gkt, gth);  // kt = eff(th)
+    // th = ist·ut, st = st2·ist, ist = rsqrt(st2), st2 = ut·ut
+    gut = gut + ist.x * gth;
+    gist += dot3(gth, vut) + st2.x * gst;
+    gst2 += ist.x * gst;
+    gst2 += gist * (-0.5f * ist.x * ist.x * ist.x);
+    gut = gut + (2.f * gst2) * vut;
+  }
+  // ut = u − un·n
+  V3f gu = gut;
+  float gun = -dot3(gut, vn);
+  gn = gn - un.x * gut;
+  // jn = num / kn (active)
+  const float ikn = div_mufu(1.f, kn.x);
+  const float gnum = gjn * ikn, gkn = -gjn * raw.x * ikn;
+  gun += -opl_e * gnum;
+  float gd = beta_over_h * gnum;
+  eff_adj(vn, gkn, gn);  // kn = eff(n)
+  // un = u·n
+  gu = gu + gun * vn;
+  gn = gn + gun * vu;
+  // u = (v_A + ω_A×r_A) − (v_B + ω_B×r_B)
+  const V3f wa{recA[12], recA[13], recA[14]}, wb{recB[12], recB[13], recB[14]};
+  const V3f gva = gu, gwa = cross3(vrA, gu), gvb = (-1.f) * gu, gwb = (-1.f) * cross3(vrB, gu);
+  grA = grA + cross3(gu, wa);
+  grB = grB - cross3(gu, wb);
+  // r_A = pt − x_A, r_B = pt − x_B
+  V3f gpt = grA + grB, gxa = (-1.f) * grA, gxb = (-1.f) * grB;
+  // narrowphase
+  V3f gc = gpt, gcA{0.f, 0.f, 0.f}, gcB{0.f, 0.f, 0.f};
+  Qf gqA{0.f, 0.f, 0.f, 0.f};
+  const V3f vc = v3of(c), vcB = v3of(cB);
+  if (type == 2) {  // pt = c, d = −(c − cB)·n
+    gc = gc - gd * vn;
+    gcB = gcB + gd * vn;
+    gn = gn - gd * (vc - vcB);
+    gcA = gc;
+    gqA = rot_adj_q(Qf{qA.w.x, qA.x.x, qA.y.x, qA.z.x}, v3(k4.x, k4.y, k4.z), gc);
+  } else {  // pt = c − r·n, d = r − (c − cB)·n
+    gn = gn - ra * gpt;
+    gc = gc - gd * vn;
+    gcB = gcB + gd * vn;
+    gn = gn - gd * (vc - vcB);
+    gcA = gc;
+    if (type == 1) gqA = rotz_adj_q(Qf{qA.w.x, qA.x.x, qA.y.x, qA.z.x}, ells.x * gc);  // c = cA + ℓ·rotate_z(qA)
+  }
+  Qf gqB = rotz_adj_q(Qf{qB.w.x, qB.x.x, qB.y.x, qB.z.x}, gn);  // n = rotate_z(qB)
+  // qA = qa ⊗ r_colA, qB = qb ⊗ r_colB
+  Qf gqa = (fl & kSIdentA) ? gqA : qmulf(gqA, qconjf(Qf{ra4.x, ra4.y, ra4.z, ra4.w}));
+  Qf gqb = (fl & kSIdentB) ? gqB : qmulf(gqB, qconjf(Qf{rb4.x, rb4.y, rb4.z, rb4.w}));
+  // cA = xa + rotate(qa, ca), cB = xb + rotate(qb, cb)
+  gxa = gxa + gcA;
+  gxb = gxb + gcB;
+  if (!(fl & kSZeroPa)) gqa = qaddf(gqa, rot_adj_q(Qf{qa.w.x, qa.x.x, qa.y.x, qa.z.x}, v3(ca.x, ca.y, ca.z), gcA));
+  if (!(fl & kSZeroPb)) gqb = qaddf(gqb, rot_adj_q(Qf{qb.w.x, qb.x.x, qb.y.x, qb.z.x}, v3(cb.x, cb.y, cb.z), gcB));
+  gqa = qaddf(gqa, Qf{gq_a[0], gq_a[1], gq_a[2], gq_a[3]});
+  gqb = qaddf(gqb, Qf{gq_b[0], gq_b[1], gq_b[2], gq_b[3]});
+  const float outA[13] = {gxa.x, gxa.y, gxa.z, gqa.w, gqa.x, gqa.y, gqa.z, gva.x, gva.y, gva.z, gwa.x, gwa.y, gwa.z};
+  const float outB[13] = {gxb.x, gxb.y, gxb.z, gqb.w, gqb.x, gqb.y, gqb.z, gvb.x, gvb.y, gvb.z, gwb.x, gwb.y, gwb.z};
+  for (int j = 0; j < 13; ++j) {
+    ia[j] = outA[j];
+    ia[13 + j] = outB[j];
+  }
+  return true;
+}
+
 template <int R>
 __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs ka) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -530,6 +721,7 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
         const float gtb[3] = {-fb_[12], -fb_[13], -fb_[14]};
         const float* recA = Q + (sl.a * LG + el) * kQS;
         const float* recB = Q + (sl.b * LG + el) * kQS;
+        if (hand_adj && contact_adj(sl, recA, recB, 1.f + H.e, H.beta_over_h, H.mu, gP, fa_ + 12, gtb, ia)) continue;
         for (int j0 = 0; j0 < 26; j0 += KT) {
           const ContactOut<DT> o =
               contact_f<DT>(sl, load_dt(recA, 0, j0), load_dt(recB, 13, j0), 1.f + H.e, H.beta_over_h, H.mu);
