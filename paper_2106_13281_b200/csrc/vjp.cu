@@ -49,7 +49,11 @@ struct VjpArgs {
   int32_t plan;
 };
 
-// shared-memory layout (words) for E envs per block, one per lane
+// shared-memory layout (words) for E envs per block, one per lane.  Per-(body, env)
+// force / adjoint rows and per-(item, env) input-adjoint rows use odd strides, so a
+// warp's scalar accesses (lane = env) hit 32 different banks.
+constexpr int kFS = 17;  // FW / FA rows: 16 used words
+constexpr int kIS = 27;  // IA rows: 26 item inputs
 struct VjpLayout {
   int32_t blob, q, q0, qk, gq, fw, fa, rec, a, ga, cnt, total;
 };
@@ -62,9 +66,9 @@ __host__ __device__ inline VjpLayout vjp_layout(int B, int J, int C, int A, int 
   L.qk = L.q0 + rq;
   L.gq = L.qk + rq;
   L.fw = L.gq + rq;
-  L.fa = L.fw + B * E * 16;
-  L.rec = L.fa + B * E * 16;
-  int recs = (J + C) * E * 12, ia = (J + C) * E * 26;
+  L.fa = L.fw + B * E * kFS;
+  L.rec = L.fa + B * E * kFS;
+  int recs = (J + C) * E * 12, ia = (J + C) * E * kIS;
   L.a = L.rec + round4(recs > ia ? recs : ia);
   L.ga = L.a + round4(A * E);
   L.cnt = L.ga + round4(A * E);
@@ -620,7 +624,7 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
       const int b = bodies_of_warp[i * G];
       if (b < 0) continue;
       const Acc<F1> acc = gather(b);
-      float* fw = FW + (b * E + el) * 16;
+      float* fw = FW + (b * E + el) * kFS;
       fw[0] = acc.F.x.x; fw[1] = acc.F.y.x; fw[2] = acc.F.z.x; fw[3] = acc.cnt.x;
       fw[4] = acc.T.x.x; fw[5] = acc.T.y.x; fw[6] = acc.T.z.x;
       fw[8] = acc.dV.x.x; fw[9] = acc.dV.y.x; fw[10] = acc.dV.z.x;
@@ -632,10 +636,10 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
     for (int i = tid; i < B * E; i += nt) {
       const int b = i / E;
       const DBody& bd = bodies[b];
-      float* fa = FA + i * 16;
+      float* fa = FA + i * kFS;
       for (int k = 0; k < 16; ++k) fa[k] = 0.f;
       if (bd.is_static) continue;
-      const float* fw = FW + i * 16;
+      const float* fw = FW + i * kFS;
       float* gq = GQ + i * kQS;
       const float* q = Q + i * kQS + 4;
       const bool iso = bd.flags & kFlagIso;
@@ -683,11 +687,11 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
     for (int it = it0; it < it1; ++it) {
       const int item = items[it * G];
       if (item < 0) continue;
-      float* ia = IA + (item * E + el) * 26;
+      float* ia = IA + (item * E + el) * kIS;
       if (item < J) {
         const DJoint& jt = joints[item];
-        const float* fc = FA + (jt.child * E + el) * 16;
-        const float* fp = FA + (jt.parent * E + el) * 16;
+        const float* fc = FA + (jt.child * E + el) * kFS;
+        const float* fp = FA + (jt.parent * E + el) * kFS;
         const float gF[3] = {fc[0] - fp[0], fc[1] - fp[1], fc[2] - fp[2]};
         const float* recP = Q + (jt.parent * LG + el) * kQS;
         const float* recC = Q + (jt.child * LG + el) * kQS;
@@ -715,8 +719,8 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
         }
       } else {
         const DSlot& sl = slots[item - J];
-        const float* fa_ = FA + (sl.a * E + el) * 16;
-        const float* fb_ = FA + (sl.b * E + el) * 16;
+        const float* fa_ = FA + (sl.a * E + el) * kFS;
+        const float* fb_ = FA + (sl.b * E + el) * kFS;
         const float gP[3] = {fa_[8] - fb_[8], fa_[9] - fb_[9], fa_[10] - fb_[10]};
         const float gtb[3] = {-fb_[12], -fb_[13], -fb_[14]};
         const float* recA = Q + (sl.a * LG + el) * kQS;
@@ -745,11 +749,11 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
       };
       for (int k = jinc_begin[b]; k < jinc_begin[b + 1]; ++k) {  // child side 4: inputs 13-25; parent 8: 0-12
         const int e = jinc[k];
-        add(IA + ((e >> 4) * E + env) * 26 + ((e & 8) ? 0 : 13));
+        add(IA + ((e >> 4) * E + env) * kIS + ((e & 8) ? 0 : 13));
       }
       for (int k = cinc_begin[b]; k < cinc_begin[b + 1]; ++k) {  // A side 4: inputs 0-12; B side 8: 13-25
         const int e = cinc[k];
-        add(IA + ((J + (e >> 4)) * E + env) * 26 + ((e & 8) ? 13 : 0));
+        add(IA + ((J + (e >> 4)) * E + env) * kIS + ((e & 8) ? 13 : 0));
       }
     }
     __syncthreads();
@@ -762,7 +766,7 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
       float* gq = GQ + i * kQS;
       const float* pre = QK + i * kQS;
       for (int k = 0; k < 3; ++k) gq[8 + k] += h * bd.mpos[k] * gq[k];  // x' = x + h·m⊙v
-      if (!bd.rot_frozen) {
+      if (!bd.rot_frozen && io.local_ad) {  // cross-check path: local value+tangent derivatives
         float gr[4], gw[3] = {0.f, 0.f, 0.f};
         for (int j = 0; j < 7; ++j) {
           auto t = [&](int k) { return k == j ? 1.f : 0.f; };
@@ -776,6 +780,36 @@ __global__ void __maxnreg__(R) brax_vjp_kernel(const __grid_constant__ VjpArgs k
         }
         for (int k = 0; k < 4; ++k) gq[4 + k] = gr[k];
         for (int k = 0; k < 3; ++k) gq[12 + k] += gw[k];
+      } else if (!bd.rot_frozen) {
+        // hand-derived adjoint of q' = normalize(p), p = q + (h/2)·(0, ω̃)⊗q, ω̃ = m⊙ω:
+        // ḡp = (ḡ − q'(q'·ḡ))/|p|; p.w = q.w − (h/2) ω̃·u, p.u = u + (h/2)(q.w ω̃ + ω̃×u)
+        const float hh = 0.5f * h;
+        const V3f u{pre[5], pre[6], pre[7]};
+        const float qw = pre[4];
+        V3f w{pre[12], pre[13], pre[14]};
+        if (!(bd.flags & kFlagFreeRot)) w = v3(bd.mrot[0] * w.x, bd.mrot[1] * w.y, bd.mrot[2] * w.z);
+        const float pw = qw - hh * dot3(w, u);
+        const V3f pu = u + hh * (qw * w + cross3(w, u));
+        const float n2 = pw * pw + dot3(pu, pu);
+        float inv = rsqrt_mufu(n2);
+        inv = inv * (1.5f - 0.5f * n2 * inv * inv);
+        const float qnw = pw * inv;
+        const V3f qnu = inv * pu;
+        const V3f gu_{gq[5], gq[6], gq[7]};
+        const float dg = qnw * gq[4] + dot3(qnu, gu_);
+        const float gpw = inv * (gq[4] - dg * qnw);
+        const V3f gpu = inv * (gu_ - dg * qnu);
+        const float gqw = gpw + hh * dot3(w, gpu);
+        const V3f gqu = gpu - (hh * gpw) * w + hh * cross3(gpu, w);
+        V3f gw = (-hh * gpw) * u + hh * (qw * gpu + cross3(u, gpu));
+        if (!(bd.flags & kFlagFreeRot)) gw = v3(bd.mrot[0] * gw.x, bd.mrot[1] * gw.y, bd.mrot[2] * gw.z);
+        gq[4] = gqw;
+        gq[5] = gqu.x;
+        gq[6] = gqu.y;
+        gq[7] = gqu.z;
+        gq[12] += gw.x;
+        gq[13] += gw.y;
+        gq[14] += gw.z;
       }
     }
     __syncthreads();
