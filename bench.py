@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--envs", type=int, default=None, help="envs per GPU")
     p.add_argument("--no-graph", action="store_true", help="launch each step from Python instead of a CUDA graph")
     p.add_argument("--no-env", action="store_true", help="skip the brax_env_step (NEXT-1) measurement")
+    p.add_argument("--no-vjp", action="store_true", help="skip the brax_step_vjp (NEXT-4) measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=200)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -389,6 +390,32 @@ def run_b200(args):
                     "ms_per_step": float(env_ms[0]) / steps_env, "steps": steps_env, "obs_dim": od,
                     "api": "brax_env_step: physics + reward/done/auto-reset/observation epilogue, one launch"}
 
+    # NEXT-4: reverse mode of the same step (brax_step_vjp: g_in = Jᵀ·g_out and g_action,
+    # one launch) on one batch of the workload; device-timed like the step
+    vjp_line = None
+    if not args.no_vjp:
+        gen = torch.Generator(device="cpu").manual_seed(7)
+        g_out = {k: torch.randn(v.shape, generator=gen).to(dev) for k, v in sets[0].items()}
+        a0 = acts[0] if A else None
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                system.step_vjp(sets[0], a0, g_out, stream=stream)
+            stream.synchronize()
+            Kv = 20
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            v0.record(stream)
+            for _ in range(Kv):
+                system.step_vjp(sets[0], a0, g_out, stream=stream)
+            v1.record(stream)
+            v1.synchronize()
+        v_ms = torch.tensor([v0.elapsed_time(v1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(v_ms, op=dist.ReduceOp.MAX)
+        vjp_line = {"value": n * world * Kv / (float(v_ms[0]) / 1e3), "unit": "env-steps/s",
+                    "ms_per_step": float(v_ms[0]) / Kv, "steps": Kv,
+                    "over_step": (float(v_ms[0]) / Kv) / (ms_max / K),
+                    "api": "brax_step_vjp: Jᵀ·g of one step (QP and action cotangents), one launch"}
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -448,7 +475,7 @@ def run_b200(args):
                    "launch": "CUDA graph of brax_step launches" if graph is not None else "eager launches",
                    "kernel_config": system.launch_config(n)},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K, "clocks": clocks,
-        "env_epilogue": env_line,
+        "env_epilogue": env_line, "vjp": vjp_line,
         "blowups": total_blowups, "substeps_per_s": value * system.substeps,
     }
     print(json.dumps(line), flush=True)

@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv > gpurun_out/smi_${TAG}.csv 2>&1
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?" >> gpurun_out/bench_${TAG}.err
 timeout 600 python bench.py --impl reference --steps 200 --warmup 3 > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err
-CMD="python bench.py --steps 50 --warmup 3 --no-cpu-baseline --e2e-steps 2 --no-env"
+CMD="python bench.py --steps 50 --warmup 3 --no-cpu-baseline --e2e-steps 2 --no-env --no-vjp"
 $CMD > gpurun_out/bench_small_${TAG}.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch_${TAG}.log 2>&1
 # full capture of the launch configuration the bench's autotuner chose
