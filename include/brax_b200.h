@@ -210,9 +210,12 @@ brax_status brax_step_jvp(const brax_system *sys, brax_qp in, const float *actio
                           const float *daction, brax_qp out, brax_qp dout, int64_t n_envs, void *stream);
 
 /* Reverse mode (cotangent) of one step: g_in = (∂Q_out/∂Q_in)ᵀ·g_out and
- * g_action = (∂Q_out/∂a)ᵀ·g_out per env — the exact transpose of brax_step_jvp's
+ * g_action = (∂Q_out/∂a)ᵀ·g_out per env — the transpose of brax_step_jvp's
  * derivative (same conventions, R35), in one kernel launch (backwards
- * substep sweep).  g_out members may be NULL (zero); g_action may be
+ * substep sweep).  Joints, plane contacts and the quaternion update
+ * use hand-derived adjoints (equal to the transposed value+tangent derivative up to
+ * fp32 rounding); with the environment variable BRAX_VJP_LOCAL_AD set they use local
+ * value+tangent evaluations instead (cross-check).  g_out members may be NULL (zero); g_action may be
  * NULL (not written) and is [n][act_dim].  in is not modified.  With the
  * environment variable BRAX_VJP_COLUMNS set, the same result is assembled from
  * 13B + A JVP launches instead (cross-check; stream-ordered scratch). */
