@@ -136,7 +136,9 @@ brax_status brax_system_phase_cycles(brax_system *sys, uint64_t out[4]);
  * experiments: BRAX_PLAN="G,V", BRAX_MAXREG=R.
  * brax_system_launch_config writes, for a launch of n_envs envs, out[6] =
  * {G lane groups per warp, V envs per lane, E envs per block, warps per block,
- * register budget, 1 if measured by the autotuner else 0}; it does not tune. */
+ * register budget, flags: bit 0 measured by the autotuner, bit 1 the fixed-shape
+ * body-gather variant}; it does not tune.  BRAX_FIXED_GATHER=0/1
+ * selects the gather variant together with BRAX_PLAN. */
 brax_status brax_system_set_autotune(brax_system *sys, int enable);
 brax_status brax_system_launch_config(const brax_system *sys, int64_t n_envs, int32_t out[6]);
 

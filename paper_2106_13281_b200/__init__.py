@@ -336,10 +336,13 @@ class System:
         _check(lib.brax_system_set_autotune(self._sys, int(enable)))
 
     def launch_config(self, n_envs: int):
-        """dict(G, V, E, warps, regs, tuned) of the next step launch of n_envs envs (see brax_system_launch_config)."""
+        """dict(G, V, E, warps, regs, tuned, fixed_gather) of the next step launch of n_envs envs
+        (see brax_system_launch_config)."""
         out = (C.c_int32 * 6)()
         _check(lib.brax_system_launch_config(self._sys, int(n_envs), out))
-        return dict(zip(("G", "V", "E", "warps", "regs", "tuned"), (int(x) for x in out)))
+        d = dict(zip(("G", "V", "E", "warps", "regs"), (int(x) for x in out[:5])))
+        d["tuned"], d["fixed_gather"] = int(out[5]) & 1, (int(out[5]) >> 1) & 1
+        return d
 
     def phase_cycles(self):
         """(prologue, joints+contacts, integrators, epilogue) SM cycles summed over blocks since the last call."""

@@ -52,7 +52,10 @@ struct KArgs {
 // S = float: one env per lane; F2: two envs per lane.  R: register budget per
 // thread (instantiated for several budgets; launch_step picks the largest that
 // keeps two blocks resident per SM).
-template <class S, int R, bool kEnv>
+// kFixed: body gathers with compile-time list lengths for the common incidence shapes
+// (a separate instantiation the autotuner may pick: the extra code costs instruction-
+// cache space that some systems do not win back; same bits either way).
+template <class S, int R, bool kEnv, bool kFixed = false>
 __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka) {
   extern __shared__ __align__(16) uint32_t smem[];
   const DHeader& H = ka.hd;
@@ -311,10 +314,21 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         if (b < 0) continue;
         Acc<S> acc{typename Acc<S>::NoInit{}};
         const int j0 = jinc_begin[b], j1 = jinc_begin[b + 1], c0 = cinc_begin[b], c1 = cinc_begin[b + 1];
-        if (j1 > j0) acc.template gather<false>(jinc + j0, j1 - j0, sJe, LG * JS);
-        else acc.zero_joints();
-        if (c1 > c0) acc.template gather<true>(cinc + c0, c1 - c0, sCe, LG * CS);
-        else acc.zero_slots();
+        const int nj = j1 - j0, nc = c1 - c0;  // warp-uniform: bodies sharing a step have one shape
+        auto general = [&]() {
+          if (nj > 0) acc.template gather<false>(jinc + j0, nj, sJe, LG * JS);
+          else acc.zero_joints();
+          if (nc > 0) acc.template gather<true>(cinc + c0, nc, sCe, LG * CS);
+          else acc.zero_slots();
+        };
+        if constexpr (kFixed) {
+#define BRAX_GF(NJ, NC) \
+  if (nj == NJ && nc == NC) acc.template gather_fixed<NJ, NC>(jinc + j0, cinc + c0, sJe, LG * JS, sCe, LG * CS); else
+          BRAX_GF(1, 2) BRAX_GF(2, 0) BRAX_GF(2, 2) BRAX_GF(3, 2) BRAX_GF(4, 1) general();
+#undef BRAX_GF
+        } else {
+          general();
+        }
 #ifdef BRAX_DIAG
         if (dg) {  // stamp once the gathered sums exist (the store waits for them)
           dts = clock64();
@@ -470,13 +484,13 @@ int choose_regs(const System& sys, const DPlan& P, int64_t grid) {
 }
 
 namespace {
-template <class S, int R, bool kEnv = false>
+template <class S, int R, bool kEnv = false, bool kFixed = false>
 cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(brax_step_kernel<S, R, kEnv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(brax_step_kernel<S, R, kEnv, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kMaxDynSmem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
@@ -491,10 +505,10 @@ cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, 
   attr[0].val.programmaticStreamSerializationAllowed = std::getenv("BRAX_NO_PDL") ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, brax_step_kernel<S, R, kEnv>, ka);
+  return cudaLaunchKernelEx(&cfg, brax_step_kernel<S, R, kEnv, kFixed>, ka);
 }
 
-cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream) {
+cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs, bool fixed, cudaStream_t stream) {
   KArgs ka{a, sys.d_blob, sys.hd, plan};
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
@@ -516,6 +530,11 @@ cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs
     return launch_variant<F1, 64, true>(ka, grid, block, smem, stream);
   }
   if (P.V == 2) {
+    if (fixed) {
+      if (regs >= 128) return launch_variant<F2, 128, false, true>(ka, grid, block, smem, stream);
+      if (regs >= 96) return launch_variant<F2, 96, false, true>(ka, grid, block, smem, stream);
+      return launch_variant<F2, 80, false, true>(ka, grid, block, smem, stream);
+    }
     if (regs >= 128) return launch_variant<F2, 128>(ka, grid, block, smem, stream);
     if (regs >= 96) return launch_variant<F2, 96>(ka, grid, block, smem, stream);
     return launch_variant<F2, 80>(ka, grid, block, smem, stream);
@@ -545,6 +564,7 @@ int64_t grid_of(const System& sys, int p, int64_t n) { return (n + sys.hd.plan[p
 LaunchConfig heuristic_config(const System& sys, int64_t n) {
   LaunchConfig c;
   c.plan = choose_plan(sys, n);
+  if (const char* e = std::getenv("BRAX_FIXED_GATHER")) c.fixed = std::atoi(e) != 0;  // experiments / tests
   const char* e = std::getenv("BRAX_MAXREG");
   c.regs = variant_regs(sys.hd.plan[c.plan].V,
                         e ? std::atoi(e) : choose_regs(sys, sys.hd.plan[c.plan], grid_of(sys, c.plan, n)));
@@ -584,22 +604,25 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   for (int p = 0; p < kNumPlans; ++p) {
     if (!plan_fits(sys, p)) continue;
     const int regs = variant_regs(sys.hd.plan[p].V, choose_regs(sys, sys.hd.plan[p], grid_of(sys, p, n)));
-    if (launch_with(sys, t, p, regs, stream) != cudaSuccess) {  // warm-up (and feasibility)
-      cudaGetLastError();
-      continue;
-    }
-    cudaEventRecord(e0, stream);
-    for (int r = 0; r < 3; ++r) launch_with(sys, t, p, regs, stream);
-    cudaEventRecord(e1, stream);
-    float ms = 0.f;
-    if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    if (ms < best_ms) {
-      best_ms = ms;
-      best.plan = p;
-      best.regs = regs;
+    for (int fx = 0; fx < (sys.hd.plan[p].V == 2 ? 2 : 1); ++fx) {
+      if (launch_with(sys, t, p, regs, fx, stream) != cudaSuccess) {  // warm-up (and feasibility)
+        cudaGetLastError();
+        continue;
+      }
+      cudaEventRecord(e0, stream);
+      for (int r = 0; r < 3; ++r) launch_with(sys, t, p, regs, fx, stream);
+      cudaEventRecord(e1, stream);
+      float ms = 0.f;
+      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (ms < best_ms) {
+        best_ms = ms;
+        best.plan = p;
+        best.regs = regs;
+        best.fixed = fx != 0;
+      }
     }
   }
   cudaEventDestroy(e0);
@@ -661,7 +684,7 @@ cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t strea
     }
     cudaGetLastError();
   }
-  return launch_with(sys, a, c.plan, c.regs, stream);
+  return launch_with(sys, a, c.plan, c.regs, c.fixed && !a.env, stream);
 }
 
 }  // namespace brax

@@ -850,6 +850,58 @@ template <class S> struct Acc {
       if (k + 1 < n) add<kSlot>(a1, b1, w1, (e1 & 8) ? -1.f : 1.f);
     }
   }
+  // gather with the list lengths known at compile time (NJ joints, NC slots): every
+  // entry, then every record is loaded before the sums (two shared-memory round trips
+  // for the whole body); same operations and order as gather(), so the same bits
+  template <int NJ, int NC>
+  __device__ __forceinline__ void gather_fixed(const int32_t* jl, const int32_t* cl, const float* jrec0, int jstride,
+                                               const float* crec0, int cstride) {
+    int ej[NJ > 0 ? NJ : 1], ec[NC > 0 ? NC : 1];
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) ej[k] = jl[k];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) ec[k] = cl[k];
+    V3T<S> fa[NJ > 0 ? NJ : 1], ta[NJ > 0 ? NJ : 1], pa[NC > 0 ? NC : 1], ra[NC > 0 ? NC : 1];
+    S wa[NC > 0 ? NC : 1];
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+      const float* rec = jrec0 + (ej[k] >> 4) * jstride;
+      fa[k] = Lanes<S>::ld3(rec);
+      ta[k] = Lanes<S>::ld3(rec + (ej[k] & 15) * (M / 4));
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const float* rec = crec0 + (ec[k] >> 4) * cstride;
+      pa[k] = Lanes<S>::ld3w(rec, wa[k]);
+      ra[k] = Lanes<S>::ld3(rec + (ec[k] & 15) * (M / 4));
+    }
+    if (NJ > 0) {
+      F = scale((ej[0] & 8) ? -1.f : 1.f, fa[0]);
+      T = ta[0];
+    } else {
+      zero_joints();
+    }
+#pragma unroll
+    for (int k = 1; k < NJ; ++k) {
+      F = axpy((ej[k] & 8) ? -1.f : 1.f, fa[k], F);
+      T = T + ta[k];
+    }
+    if (NC > 0) {
+      const float sg = (ec[0] & 8) ? -1.f : 1.f;
+      dV = scale(sg, pa[0]);
+      dW = scale(sg, ra[0]);
+      cnt = wa[0];
+    } else {
+      zero_slots();
+    }
+#pragma unroll
+    for (int k = 1; k < NC; ++k) {
+      const float sg = (ec[k] & 8) ? -1.f : 1.f;
+      dV = axpy(sg, pa[k], dV);
+      dW = axpy(sg, ra[k], dW);
+      cnt = cnt + wa[k];
+    }
+  }
   struct NoInit {};
   __device__ __forceinline__ explicit Acc(NoInit) {}
   __device__ __forceinline__ void zero_joints() {

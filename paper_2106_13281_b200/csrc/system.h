@@ -17,6 +17,7 @@ struct LaunchConfig {
   int plan = 0;     // index into DHeader::plan
   int regs = 0;     // register budget variant
   bool tuned = false;
+  bool fixed = false;  // fixed-shape body gathers (kFixed instantiation, V = 2 plans)
 };
 
 struct System {
