@@ -287,8 +287,15 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         if (item < 0) continue;
         if (item < J) {
           const DJoint& jt = joints[item];
-          joint<S>(jt, Row<S>{sQ + (jt.parent * LG + el) * QS}, Row<S>{sQ + (jt.child * LG + el) * QS}, sA + el * SL,
-                   RW, sJ + (item * LG + el) * JS);
+          const Row<S> rp{sQ + (jt.parent * LG + el) * QS}, rc{sQ + (jt.child * LG + el) * QS};
+          float* rec = sJ + (item * LG + el) * JS;
+          if constexpr (kFixed) {  // specialised variant: hinges with a torque actuator at compile time
+            const int4 h0 = *reinterpret_cast<const int4*>(&jt);
+            if (h0.z == 1 && h0.w == 0) joint<S, 1, 0>(jt, rp, rc, sA + el * SL, RW, rec);
+            else joint<S>(jt, rp, rc, sA + el * SL, RW, rec);
+          } else {
+            joint<S>(jt, rp, rc, sA + el * SL, RW, rec);
+          }
         } else {
           int c = item - J;
           const DSlot& sl = slots[c];
@@ -571,8 +578,9 @@ LaunchConfig heuristic_config(const System& sys, int64_t n) {
   return c;
 }
 
-// Times one step of every plan that fits (at its register budget) on a scratch
-// copy of the caller's state and actions; the caller's buffers are not written.
+// Times one step of every plan that fits (at its register budget), reading the
+// caller's state and actions and writing scratch buffers; the caller's buffers are
+// not written.
 LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   LaunchConfig best = heuristic_config(sys, a.n_envs);
   const int64_t n = a.n_envs, B = sys.hd.B;
@@ -586,13 +594,14 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   }
   float* f[4] = {buf, nullptr, nullptr, nullptr};
   for (int k = 1; k < 4; ++k) f[k] = f[k - 1] + fbytes[k - 1] / 4;
-  const float* src[4] = {a.pos_in, a.rot_in, a.vel_in, a.ang_in};
-  for (int k = 0; k < 4; ++k) cudaMemcpyAsync(f[k], src[k], fbytes[k], cudaMemcpyDeviceToDevice, stream);
+  // every trial steps the caller's (read-only) input into the scratch buffers: all
+  // plans are timed on the same state (in-place trials would let the state drift
+  // between plans, e.g. towards more contacts, and bias the later ones)
   StepArgs t = a;
-  t.pos_in = t.pos_out = f[0];
-  t.rot_in = t.rot_out = f[1];
-  t.vel_in = t.vel_out = f[2];
-  t.ang_in = t.ang_out = f[3];
+  t.pos_out = f[0];
+  t.rot_out = f[1];
+  t.vel_out = f[2];
+  t.ang_out = f[3];
   t.n_steps = 1;
   t.status = nullptr;
   t.contact_active = nullptr;
@@ -609,14 +618,20 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
         cudaGetLastError();
         continue;
       }
-      cudaEventRecord(e0, stream);
-      for (int r = 0; r < 3; ++r) launch_with(sys, t, p, regs, fx, stream);
-      cudaEventRecord(e1, stream);
-      float ms = 0.f;
-      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess) {
-        cudaGetLastError();
-        continue;
+      float ms = 1e30f;  // the faster of two rounds of three launches (timing noise)
+      bool ok = true;
+      for (int round = 0; round < 2 && ok; ++round) {
+        cudaEventRecord(e0, stream);
+        for (int r = 0; r < 3; ++r) launch_with(sys, t, p, regs, fx, stream);
+        cudaEventRecord(e1, stream);
+        float m = 0.f;
+        if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&m, e0, e1) != cudaSuccess) {
+          cudaGetLastError();
+          ok = false;
+        }
+        ms = m < ms ? m : ms;
       }
+      if (!ok) continue;
       if (ms < best_ms) {
         best_ms = ms;
         best.plan = p;

@@ -492,12 +492,14 @@ template <class S> __device__ __forceinline__ void kinematic(const DBody& bd, Ro
 // action accessor act(k) for action component k; returns F on the child, T on the
 // child and T on the parent (already negated, as stored).
 template <class S> struct JointOut { V3T<S> f, tc, tp; };
-template <class S, class RowT, class ActF>
+// kDof > 0 / kAct > -2: the joint's dof / actuator kind known at compile time (the
+// specialised kernel variant's common class: hinge with a torque actuator), else read.
+template <class S, class RowT, class ActF, int kDof = 0, int kAct = -2>
 __device__ __forceinline__ JointOut<S> joint_f(const DJoint& Jm, const RowT& P, const RowT& C, ActF act) {
   // the parameter record, read with LDS.128 (struct fields at fixed float4 slots)
   const float4* J4 = reinterpret_cast<const float4*>(&Jm);
   const int4 h0 = *reinterpret_cast<const int4*>(&Jm), h1 = reinterpret_cast<const int4*>(&Jm)[1];
-  const int dof = h0.z, act_kind = h0.w, act_offset = h1.x, flags = h1.y;
+  const int dof = kDof > 0 ? kDof : h0.z, act_kind = kAct > -2 ? kAct : h0.w, act_offset = h1.x, flags = h1.y;
   const float4 op_k = J4[2], oc_cl = J4[3], jp = J4[4], jc = J4[5], lo_kl = J4[6], hi_ka = J4[7], ca_s = J4[8];
   const float lo[3] = {lo_kl.x, lo_kl.y, lo_kl.z}, hi[3] = {hi_ka.x, hi_ka.y, hi_ka.z};
   Q4T<S> qp = P.rot(), qc = C.rot();
@@ -561,9 +563,10 @@ __device__ __forceinline__ JointOut<S> joint_f(const DJoint& Jm, const RowT& P, 
 }
 // act: this lane's column of the block's actions sA[k][slot] (row stride E).
 // out: this (joint, lane) record: F on child | T child | T parent.
-template <class S>
+template <class S, int kDof = 0, int kAct = -2>
 __device__ __forceinline__ void joint(const DJoint& Jm, Row<S> P, Row<S> C, const float* act, int E, float* out) {
-  const JointOut<S> o = joint_f<S>(Jm, P, C, [&](int k) { return Lanes<S>::ld(act + k * E); });
+  auto actf = [&](int k) { return Lanes<S>::ld(act + k * E); };
+  const JointOut<S> o = joint_f<S, Row<S>, decltype(actf), kDof, kAct>(Jm, P, C, actf);
   constexpr int M = Lanes<S>::M;
   Lanes<S>::st3(out, o.f);
   Lanes<S>::st3(out + M, o.tc);
