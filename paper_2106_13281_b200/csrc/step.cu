@@ -301,8 +301,20 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
           const DSlot& sl = slots[c];
           float* cp = sCnt + c * RW + el * SL;
           S cnt = Lanes<S>::ld(cp);
-          contact<S>(sl, Row<S>{sQ + (sl.a * LG + el) * QS}, Row<S>{sQ + (sl.b * LG + el) * QS}, 1.f + H.e,
-                     H.beta_over_h, H.mu, sC + (c * LG + el) * CS, cnt);
+          const Row<S> ra{sQ + (sl.a * LG + el) * QS}, rb{sQ + (sl.b * LG + el) * QS};
+          float* rec = sC + (c * LG + el) * CS;
+          if constexpr (kFixed) {  // specialised variant: capsule ends and spheres on the ground at compile time
+            const int4 h0 = *reinterpret_cast<const int4*>(&sl), h1 = reinterpret_cast<const int4*>(&sl)[1];
+            const bool ground = h1.x == 0 && h1.y == 1 && (h1.z & kCapsuleOnGroundFlags) == kCapsuleOnGroundFlags;
+            if (ground && h0.x == 1)
+              contact<S, 1>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
+            else if (ground && h0.x == 0)
+              contact<S, 2>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
+            else
+              contact<S>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
+          } else {
+            contact<S>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
+          }
           Lanes<S>::st(cp, cnt);
         }
       }
