@@ -289,9 +289,11 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
           const DJoint& jt = joints[item];
           const Row<S> rp{sQ + (jt.parent * LG + el) * QS}, rc{sQ + (jt.child * LG + el) * QS};
           float* rec = sJ + (item * LG + el) * JS;
-          if constexpr (kFixed) {  // specialised variant: hinges with a torque actuator at compile time
+          if constexpr (kFixed) {  // specialised variant: torque-actuated joints with dof at compile time
             const int4 h0 = *reinterpret_cast<const int4*>(&jt);
-            if (h0.z == 1 && h0.w == 0) joint<S, 1, 0>(jt, rp, rc, sA + el * SL, RW, rec);
+            if (h0.w == 0 && h0.z == 1) joint<S, 1, 0>(jt, rp, rc, sA + el * SL, RW, rec);
+            else if (h0.w == 0 && h0.z == 2) joint<S, 2, 0>(jt, rp, rc, sA + el * SL, RW, rec);
+            else if (h0.w == 0 && h0.z == 3) joint<S, 3, 0>(jt, rp, rc, sA + el * SL, RW, rec);
             else joint<S>(jt, rp, rc, sA + el * SL, RW, rec);
           } else {
             joint<S>(jt, rp, rc, sA + el * SL, RW, rec);
@@ -310,6 +312,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
               contact<S, 1>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
             else if (ground && h0.x == 0)
               contact<S, 2>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
+            else if (ground && h0.x == 2)
+              contact<S, 3>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
             else
               contact<S>(sl, ra, rb, 1.f + H.e, H.beta_over_h, H.mu, rec, cnt);
           } else {

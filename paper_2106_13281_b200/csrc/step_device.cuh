@@ -654,10 +654,10 @@ __device__ __forceinline__ void seg_seg(V3T<S> p1, V3T<S> q1, V3T<S> p2, V3T<S> 
 // ---- S5: contact slot, velocity-level impulse + Baumgarte (R13-R19)
 // out: this (slot, lane) record: P, active | r_A×P | r_B×P; cnt: substeps active.
 template <class S> struct ContactOut { V3T<S> P; S active; V3T<S> ta, tb; };
-// Slot classes known at compile time (the specialised kernel variant): kCls = 1 (2) is
-// a capsule end (sphere) of an isotropic dynamic body, collider not offset, on a static
-// plane collider at its body's origin, unrotated (the feet and torsos of the locomotion
-// scenes); kCls = 0: everything read from the record.
+// Slot classes known at compile time (the specialised kernel variant): kCls = 1 / 2 / 3
+// is a capsule end / sphere / box corner of an isotropic dynamic body, collider not
+// offset, on a static plane collider at its body's origin, unrotated (the feet and
+// torsos of the locomotion scenes); kCls = 0: everything read from the record.
 constexpr int kCapsuleOnGroundFlags = kSZeroPa | kSZeroPb | kSIdentB | kSIsoA;
 template <class S, class RowT, int kCls = 0>
 __device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT& A, const RowT& B, float opl_e,
@@ -665,7 +665,8 @@ __device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT&
   // the parameter record, read with LDS.128 at its fixed float4 slots
   const float4* S4 = reinterpret_cast<const float4*>(&SLm);
   const int4 h0 = *reinterpret_cast<const int4*>(&SLm), h1 = reinterpret_cast<const int4*>(&SLm)[1];
-  const int type = kCls == 1 ? 1 : kCls == 2 ? 0 : h0.x, a_static = kCls ? 0 : h1.x, b_static = kCls ? 1 : h1.y;
+  const int type = kCls == 1 ? 1 : kCls == 2 ? 0 : kCls == 3 ? 2 : h0.x, a_static = kCls ? 0 : h1.x,
+            b_static = kCls ? 1 : h1.y;
   const int fl = kCls ? ((h1.z & kSIdentA) | kCapsuleOnGroundFlags) : h1.z;
   const float4 ca = S4[2], cb = S4[4], ells = S4[6];  // ca_pos|ra, cb_pos|rb, ell_a ellb 1/m_a 1/m_b
   const float ra = ca.w, rb = cb.w;
