@@ -545,6 +545,10 @@ cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs
   const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);
   if (a.env) {  // env-epilogue instantiations (fewer register variants)
     if (P.V == 2) {
+      if (fixed) {
+        if (regs >= 128) return launch_variant<F2, 128, true, true>(ka, grid, block, smem, stream);
+        return launch_variant<F2, 96, true, true>(ka, grid, block, smem, stream);
+      }
       if (regs >= 128) return launch_variant<F2, 128, true>(ka, grid, block, smem, stream);
       return launch_variant<F2, 96, true>(ka, grid, block, smem, stream);
     }
@@ -715,7 +719,7 @@ cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t strea
     }
     cudaGetLastError();
   }
-  return launch_with(sys, a, c.plan, c.regs, c.fixed && !a.env, stream);
+  return launch_with(sys, a, c.plan, c.regs, c.fixed, stream);
 }
 
 }  // namespace brax

@@ -133,8 +133,10 @@ def test_env_rollout_equals_single_steps_and_plans_agree():
     assert torch.equal(a["steps"], b["steps"]) and torch.equal(a["episode"], b["episode"])
     assert big["done"].sum() > 0
     try:
-        for plan in ("2,1", "4,1", "1,2", "2,2", "4,2"):
+        for plan, fixed in (("2,1", "0"), ("4,1", "0"), ("1,2", "0"), ("2,2", "0"), ("4,2", "0"), ("1,2", "1"),
+                            ("2,2", "1"), ("4,2", "1")):
             os.environ["BRAX_PLAN"] = plan
+            os.environ["BRAX_FIXED_GATHER"] = fixed
             c = fresh()
             other = s.env_step(c, acts, seed=3)
             for key in ("obs", "reward", "done"):
@@ -143,6 +145,7 @@ def test_env_rollout_equals_single_steps_and_plans_agree():
                 assert torch.equal(c["qp"][k], a["qp"][k]), (plan, k)
     finally:
         os.environ.pop("BRAX_PLAN", None)
+        os.environ.pop("BRAX_FIXED_GATHER", None)
 
 
 def test_env_errors():
