@@ -359,8 +359,18 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
           dtg = clock64();
         }
 #endif
-        integrate<S>(bodies[b], Row<S>{sQ + (b * LG + el) * QS}, acc, H.h, H.g, kin,
-                     save_co && last ? sCo + b * 6 * RW + el * SL : nullptr, RW);
+        float* co = save_co && last ? sCo + b * 6 * RW + el * SL : nullptr;
+        const Row<S> rb{sQ + (b * LG + el) * QS};
+        if constexpr (kFixed) {  // specialised variant: isotropic bodies without frozen axes at compile time
+          const int fl = bodies[b].flags;
+          constexpr int kFreeFlags = kFlagIso | kFlagFreePos | kFlagFreeRot;
+          if ((fl & kFreeFlags) == kFreeFlags && !bodies[b].rot_frozen)
+            integrate<S, true>(bodies[b], rb, acc, H.h, H.g, kin, co, RW);
+          else
+            integrate<S>(bodies[b], rb, acc, H.h, H.g, kin, co, RW);
+        } else {
+          integrate<S>(bodies[b], rb, acc, H.h, H.g, kin, co, RW);
+        }
       }
 #ifdef BRAX_DIAG
       if (dg) {

@@ -930,9 +930,13 @@ template <class S> struct Acc {
 // body: same arithmetic as kinematic(), with v and ω still in registers.
 // co (env epilogue with contact observations, last substep of a step): this body's
 // and lane's [6][E] slot for the collision integrator's velocity change; else NULL.
-template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Row<S> r, const Acc<S>& acc, float h,
-                                                             const float* g, bool kin, float* co, int E) {
-  const bool iso = bd.flags & kFlagIso, fp = bd.flags & kFlagFreePos, fr = bd.flags & kFlagFreeRot;
+// kFree: an isotropic body with no frozen axis, known at compile time (the specialised
+// kernel variant's common body class), else the flags are read.
+template <class S, bool kFree = false>
+__device__ __forceinline__ void integrate(const DBody& bd, Row<S> r, const Acc<S>& acc, float h, const float* g,
+                                          bool kin, float* co, int E) {
+  const bool iso = kFree || (bd.flags & kFlagIso), fp = kFree || (bd.flags & kFlagFreePos),
+             fr = kFree || (bd.flags & kFlagFreeRot);
   Q4T<S> q = r.rot();
   V3T<S> v = axpy(h, axpy(bd.inv_mass, acc.F, bc3<S>(g)), r.vel());
   V3T<S> w = axpy(h, iw(q, bd.inv_inertia, iso, acc.T), r.ang());
@@ -961,7 +965,7 @@ template <class S> __device__ __forceinline__ void integrate(const DBody& bd, Ro
   }
   if (kin) {  // next substep's kinematic integrator (v, ω already masked)
     r.set_pos(axpy(h, v, r.pos()));
-    if (!bd.rot_frozen) r.set_rot(kin_rot(q, w, h));
+    if (kFree || !bd.rot_frozen) r.set_rot(kin_rot(q, w, h));
   }
 }
 
