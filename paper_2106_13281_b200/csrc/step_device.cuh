@@ -759,7 +759,7 @@ __device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT&
   S jt = vmin(vdiv(st, kt), S(mu * jn));
   P = jn * n - jt * th;
   ta = cross(rA, P);
-  tb = cross(rB, P);
+  if (kCls == 0) tb = cross(rB, P);  // the specialised classes' B side is static: r_B×P is never gathered
   active = sel(act, bc<S>(1.f), bc<S>(0.f));
   }
   return ContactOut<S>{P, active, ta, tb};
@@ -771,7 +771,7 @@ __device__ __forceinline__ void contact(const DSlot& SLm, Row<S> A, Row<S> B, fl
   constexpr int M = Lanes<S>::M;
   Lanes<S>::st3(out, o.P, o.active);
   Lanes<S>::st3(out + M, o.ta);
-  Lanes<S>::st3(out + 2 * M, o.tb);
+  if (kCls == 0) Lanes<S>::st3(out + 2 * M, o.tb);  // a static B side's record field is never read
   cnt = cnt + o.active;
 }
 
