@@ -390,7 +390,7 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     T kn = eff(n);
     T jn = xmax(T(0.0), (-(T(1.0) + T(S.e)) * un + (T(S.beta) / h) * d) / kn);
     if (!(jn > T(0.0))) continue;                                // R15
-    if (val(jn * kn) < opt.amb_jn) out->ambiguous = true;        // R23 weak impulse
+    if (val(jn) * val(kn) < opt.amb_jn) out->ambiguous = true;   // R23 weak impulse (diagnostic: not counted)
     V3<T> ut = u - un * n;
     T st_ = xsqrt(dot(ut, ut));
     V3<T> P = jn * n;
