@@ -122,7 +122,10 @@ def r24_qualifies(o, qp, acts, T):
 @pytest.mark.parametrize("name,n,zero_action", [("ball", 1, True), ("pendulum", 1024, False),
                                                 ("chain2", 1024, False), ("ant", 512, True)])
 def test_100_step_parity(name, n, zero_action):
-    """Free-running GPU vs oracle trajectories, 100 steps, ≤ 1e-3 (R24-qualified configs)."""
+    """Free-running GPU vs oracle trajectories, 100 steps, ≤ 1e-3 (R24-qualified configs).
+    Envs are excluded only by the standard R23 band (|d| < 1e-5, j_n·k(n) < 1e-5 in some
+    substep), evaluated along the oracle's own trajectory; at least 95 % must remain
+    (ant: 16 of 512 excluded, measured on B200, tools/parity100.py)."""
     o, s = scene(name)
     T = 100
     qp = synth.to_f32(o.reset(n, 11, 0.1, 0.1))
@@ -130,8 +133,7 @@ def test_100_step_parity(name, n, zero_action):
     if zero_action:
         acts[:] = 0
     assert r24_qualifies(o, qp, acts, T)
-    o_wide = oracle.Oracle(o.sys, amb_d=1e-4, amb_jn=1e-4)
-    ref, info = o_wide.rollout({k: v.astype(np.float64) for k, v in qp.items()}, acts, threads=8)
+    ref, info = o.rollout({k: v.astype(np.float64) for k, v in qp.items()}, acts, threads=8)
     qd = dev(qp)
     ad = torch.from_numpy(acts).cuda() if o.act_dim else None
     for t in range(T):
@@ -139,9 +141,8 @@ def test_100_step_parity(name, n, zero_action):
     torch.cuda.synchronize()
     got = host(qd)
     keep = ~info["ambiguous"] if info["ambiguous"] is not None else np.ones(n, bool)
-    # contact onsets within the widened R23 band over 100 steps (bouncing feet) are
-    # excluded and counted; the rest must match to 1e-3
-    assert keep.mean() > 0.5, f"excluded {(~keep).sum()} of {n}"
+    print(f"{name}: excluded {(~keep).sum()} of {n} envs (R23 band)")
+    assert keep.mean() >= 0.95, f"excluded {(~keep).sum()} of {n}"
     err, errs = max_err(got, ref, keep)
     assert err <= TOL_100, errs
 
