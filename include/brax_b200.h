@@ -27,6 +27,8 @@
  *    "enqueued".  A failed launch returns BRAX_E_CUDA.
  *  - Thread safety: a brax_system is immutable after creation; concurrent
  *    brax_step calls on distinct streams are safe.
+ *  - Device: entry points that launch work make the system's device current for
+ *    the call and restore the caller's current device before returning.
  */
 #ifndef BRAX_B200_H_
 #define BRAX_B200_H_
@@ -82,6 +84,68 @@ typedef struct brax_config brax_config;
 brax_status brax_config_parse(const char *text, size_t len, brax_config **out);
 void brax_config_destroy(brax_config *cfg);
 
+/* Programmatic form ("users can define systems in text, or they can
+ * define systems programmatically"; the App. A Python listing).
+ * Host structs, read only during the call (the caller keeps ownership; names are
+ * copied).  Quaternions are (w, x, y, z) and must be unit (|q| = 1 ± 1e-6); joint
+ * limits are in radians in [−π, π] (R9); frozen flags are 0 or 1 per axis (App. A
+ * `frozen`).  Bodies, joints and actuators are referenced by index;
+ * colliders are attached to bodies by index and take the text format's global order
+ * (body order, then descriptor order within a body).  pairs == NULL selects the
+ * all-pairs rule (R19: collider pairs on different, non-jointed, not-both-static
+ * bodies), else the listed body pairs in order (the text `collide_include`).
+ * The resulting config equals the text parse of the same scene (same integer
+ * tables, same default_qp).  Errors: as brax_config_parse minus BRAX_E_PARSE; the
+ * detail names the offending descriptor ("joints[2].stiffness: must be > 0"). */
+typedef enum { BRAX_SHAPE_SPHERE = 0, BRAX_SHAPE_CAPSULE = 1, BRAX_SHAPE_BOX = 2, BRAX_SHAPE_PLANE = 3 } brax_shape;
+typedef enum { BRAX_ACTUATOR_TORQUE = 0, BRAX_ACTUATOR_ANGLE = 1 } brax_actuator_kind;
+typedef struct {
+  const char *name;         /* may be NULL (then "body<i>"); names must be unique */
+  double mass;              /* > 0 */
+  double inertia[3];        /* body-frame diagonal, > 0 (App. A inertia{x y z}) */
+  double frozen_pos[3], frozen_rot[3]; /* 1 = axis frozen */
+  double init_pos[3], init_rot[4];     /* pose of a root body in default_qp (text: defaults.qps) */
+} brax_body_desc;
+typedef struct {
+  const char *name;
+  int32_t parent, child;    /* body indices */
+  double parent_offset[3], child_offset[3];
+  double rotation[4], reference_rotation[4]; /* joint frame J_p; reference frame (R7) */
+  int32_t dof;              /* 0..3 free axes (the text form's number of angle_limit entries) */
+  double limit_lo[3], limit_hi[3];           /* radians, first `dof` used */
+  double stiffness;         /* > 0 */
+  double spring_damping, angular_damping;    /* >= 0 */
+  double limit_stiffness, angular_stiffness; /* >= 0; negative = stiffness (R8) */
+} brax_joint_desc;
+typedef struct {
+  const char *name;
+  int32_t joint;            /* joint index; at most one actuator per joint, dof >= 1 */
+  int32_t kind;             /* brax_actuator_kind */
+  double strength;
+} brax_actuator_desc;
+typedef struct {
+  int32_t body;             /* body index */
+  int32_t shape;            /* brax_shape */
+  double pos[3], rot[4];    /* pose in the body frame */
+  double radius, length;    /* sphere / capsule (length includes the caps, R17) */
+  double halfsize[3];       /* box */
+  int32_t capsule_end;      /* 0 both ends, +1 / −1 one end (R17) */
+} brax_collider_desc;
+typedef struct { int32_t first, second; } brax_body_pair;
+typedef struct {
+  double dt;                /* > 0 */
+  int32_t substeps;         /* >= 1 */
+  double gravity[3];
+  double friction, elasticity, baumgarte_erp; /* μ >= 0, e in [0, 1], β in (0, 1] (R13) */
+  int32_t n_bodies, n_joints, n_actuators, n_colliders, n_pairs;
+  const brax_body_desc *bodies;
+  const brax_joint_desc *joints;
+  const brax_actuator_desc *actuators;
+  const brax_collider_desc *colliders;
+  const brax_body_pair *pairs;               /* NULL = all-pairs rule */
+} brax_config_desc;
+brax_status brax_config_from_desc(const brax_config_desc *desc, brax_config **out);
+
 /* Host-only introspection of a parsed config (no GPU needed). */
 brax_status brax_config_counts(const brax_config *cfg, int32_t *n_bodies, int32_t *n_joints, int32_t *act_dim,
                                int32_t *n_slots);          /* any output may be NULL */
@@ -128,12 +192,15 @@ brax_status brax_system_phase_cycles(brax_system *sys, uint64_t out[4]);
 
 /* Launch configuration of the step kernel.  Every configuration
  * computes bit-identical results (explicit rounding of every operation), so the
- * choice only affects speed.  With autotuning on (the default), the first launch
- * of a given n_envs (>= 256) outside CUDA-graph capture times one step of every
- * configuration on a scratch copy of the caller's state (the caller's buffers are
- * not written; the call synchronises its stream once) and remembers the fastest
- * for that n_envs; otherwise a size heuristic chooses.  Environment overrides for
- * experiments: BRAX_PLAN="G,V", BRAX_MAXREG=R.
+ * choice only affects speed.  brax_step itself never tunes, allocates or
+ * synchronises: it uses the configuration brax_system_tune measured for its n_envs,
+ * else a size heuristic.  brax_system_tune(sys, in, action, n_envs, stream) times one
+ * step of every configuration on the caller's state `in` (read only; outputs go to a
+ * stream-ordered scratch allocation that is freed before return), synchronises
+ * `stream`, and remembers the fastest for n_envs (thread-safe; call it once per batch
+ * size, outside graph capture).  brax_system_set_autotune(sys, 0) makes
+ * brax_system_tune a no-op.  Environment overrides for experiments:
+ * BRAX_PLAN="G,V", BRAX_MAXREG=R.
  * brax_system_launch_config writes, for a launch of n_envs envs, out[6] =
  * {G lane groups per warp, V envs per lane, E envs per block, warps per block,
  * register budget, flags: bit 0 measured by the autotuner, bit 1 the fixed-shape
@@ -156,6 +223,11 @@ typedef struct {
   float *pos, *rot, *vel, *ang;
 } brax_qp;
 
+/* Launch-configuration tuning for n_envs (see "Launch configuration" above): reads `in`
+ * and `action` (as brax_step would), allocates stream-ordered scratch, synchronises
+ * `stream`.  Not capturable in a CUDA graph. */
+brax_status brax_system_tune(brax_system *sys, brax_qp in, const float *action, int64_t n_envs, void *stream);
+
 /* Broadcast default_qp to n_envs envs, then for every non-static body add
  * v += M_pos ⊙ vel_noise·u, ω += M_rot ⊙ ang_noise·u with u ∈ [−1, 1) from
  * Philox4x32-10(key = seed, counter = (env, body, field, 0)).
@@ -173,6 +245,10 @@ brax_status brax_step(const brax_system *sys, brax_qp in, const float *action, b
 typedef struct {
   uint32_t *status;        /* [n] bit0 non-finite value, bit1 |value| > 1e6; or NULL */
   uint8_t *contact_active; /* [n][C] number of substeps each slot was active; or NULL */
+  float *contact_dp;       /* [n][B][6] Σ over the step's substeps of the collision integrator's
+                              velocity change (Δv, Δω) per body (the input of Table 1's
+                              contact observations); for brax_rollout, of its last
+                              step; 16-byte aligned; or NULL */
 } brax_step_extras;
 
 /* brax_step plus optional per-env outputs (NULL extras or NULL members = skip). */

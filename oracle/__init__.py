@@ -90,13 +90,16 @@ def _load():
             lib = C.CDLL(build())
             dp = C.POINTER(C.c_double)
             lib.oracle_step.argtypes = [C.POINTER(_OSys), C.POINTER(_OOpts), C.c_int64, C.c_int64, dp, dp, dp, dp,
-                                        dp, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), dp]
+                                        dp, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), dp,
+                                        dp]
             lib.oracle_step.restype = C.c_int
             lib.oracle_step_f32.argtypes = lib.oracle_step.argtypes
             lib.oracle_step_f32.restype = C.c_int
             lib.oracle_count_ops.argtypes = [C.POINTER(_OSys), C.POINTER(_OOpts), C.c_int64, C.c_int64, dp, dp, dp,
                                              dp, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
             lib.oracle_count_ops.restype = C.c_int
+            lib.oracle_count_ops_lean.argtypes = lib.oracle_count_ops.argtypes
+            lib.oracle_count_ops_lean.restype = C.c_int
             lib.oracle_slot_geometry.argtypes = [C.POINTER(_OSys), C.c_int32, dp, dp, dp, dp, dp]
             lib.oracle_slot_geometry.restype = C.c_int
             _lib = lib
@@ -188,14 +191,16 @@ class Oracle:
         d = self.default_qp()
         return {k: np.broadcast_to(v, (n,) + v.shape).copy() for k, v in d.items()}
 
-    def step(self, qp, action=None, *, threads: int = 1, fp32: bool = False, contact_dv: bool = False):
+    def step(self, qp, action=None, *, threads: int = 1, fp32: bool = False, contact_dv: bool = False,
+             contact_dp: bool = False):
         """One Brax step (substeps × Alg. 1) on a batch; returns (qp_out, extras).
 
         qp: dict of arrays pos [n,B,3], rot [n,B,4], vel [n,B,3], ang [n,B,3]
         (any float dtype; promoted to fp64).  action: [n, act_dim] or None.
         extras: contact_active [n,C] u8, status [n] u32, ambiguous [n] bool, and with
         contact_dv=True "contact_dv" [n,B,6]: the last substep's collision-integrator
-        velocity change (Δv, Δω) per body.
+        velocity change (Δv, Δω) per body; with contact_dp=True "contact_dp" [n,B,6]: that
+        change summed over the step's substeps (brax_step_extras.contact_dp).
         fp32=True runs the same code in fp32 arithmetic: a diagnostic of the fp32
         rounding floor of the method, never a parity reference."""
         lib = _load()
@@ -214,6 +219,7 @@ class Oracle:
         dp = C.POINTER(C.c_double)
         ca_ptr = ca.ctypes.data_as(C.POINTER(C.c_uint8)) if self.n_slots else None
         cdv = np.zeros((n, B, 6)) if contact_dv else None
+        cdp = np.zeros((n, B, 6)) if contact_dp else None
 
         def run(e0, e1):
             fn = lib.oracle_step_f32 if fp32 else lib.oracle_step
@@ -223,7 +229,8 @@ class Oracle:
                                  act.ctypes.data_as(dp), ca_ptr,
                                  status.ctypes.data_as(C.POINTER(C.c_uint32)),
                                  amb.ctypes.data_as(C.POINTER(C.c_uint8)),
-                                 cdv.ctypes.data_as(dp) if cdv is not None else None)
+                                 cdv.ctypes.data_as(dp) if cdv is not None else None,
+                                 cdp.ctypes.data_as(dp) if cdp is not None else None)
             assert rc == 0
 
         if threads <= 1 or n < 2 * threads:
@@ -239,6 +246,8 @@ class Oracle:
         ex = {"contact_active": ca, "status": status, "ambiguous": amb.astype(bool)}
         if cdv is not None:
             ex["contact_dv"] = cdv
+        if cdp is not None:
+            ex["contact_dp"] = cdp
         return out, ex
 
     def rollout(self, qp, actions, *, threads: int = 1):
@@ -253,8 +262,11 @@ class Oracle:
             status = ex["status"] if status is None else (status | ex["status"])
         return qp, {"ambiguous": amb, "status": status}
 
-    def count_ops(self, qp, action=None):
-        """Algorithmic (flops, mufu) summed over the batch for one step."""
+    def count_ops(self, qp, action=None, *, lean: bool = False):
+        """Algorithmic (flops, mufu) summed over the batch for one step.
+        lean=True: the second convention — operations made exactly neutral by the scene
+        (unit masks, isotropic inertia, zero damping, zero collider offsets / identity
+        collider rotations) are not counted."""
         lib = _load()
         out = {k: np.ascontiguousarray(qp[k], dtype=np.float64).copy() for k in ("pos", "rot", "vel", "ang")}
         n = out["pos"].shape[0]
@@ -263,7 +275,8 @@ class Oracle:
         fl = C.c_uint64()
         mu = C.c_uint64()
         dp = C.POINTER(C.c_double)
-        rc = lib.oracle_count_ops(C.byref(self._sys), C.byref(self._opts), 0, n,
+        fn = lib.oracle_count_ops_lean if lean else lib.oracle_count_ops
+        rc = fn(C.byref(self._sys), C.byref(self._opts), 0, n,
                                   out["pos"].ctypes.data_as(dp), out["rot"].ctypes.data_as(dp),
                                   out["vel"].ctypes.data_as(dp), out["ang"].ctypes.data_as(dp),
                                   act.ctypes.data_as(dp), C.byref(fl), C.byref(mu))

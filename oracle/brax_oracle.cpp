@@ -34,16 +34,33 @@ namespace {
 // op-counting scalar
 // ----------------------------------------------------------------------------
 thread_local uint64_t g_flops = 0, g_mufu = 0;
+// "lean" counting (second convention, reported beside the first): operations whose
+// operand is an exactly neutral value fixed by the scene — a unit mask (no frozen
+// axis), an isotropic inertia (I_w⁻¹ = 1/I, no rotation), a zero damping coefficient,
+// a zero collider offset, an identity collider rotation — are not counted.  The
+// values computed are identical; only the tally differs.
+thread_local bool g_lean = false;
+thread_local int g_mute = 0;  // > 0: inside a neutral operation in lean mode
 
 struct Cnt {
   double v;
   Cnt() : v(0) {}
   Cnt(double x) : v(x) {}  // NOLINT: implicit from constants
 };
-inline Cnt operator+(Cnt a, Cnt b) { g_flops += 1; return Cnt(a.v + b.v); }
-inline Cnt operator-(Cnt a, Cnt b) { g_flops += 1; return Cnt(a.v - b.v); }
-inline Cnt operator*(Cnt a, Cnt b) { g_flops += 1; return Cnt(a.v * b.v); }
-inline Cnt operator/(Cnt a, Cnt b) { g_flops += 4; g_mufu += 1; return Cnt(a.v / b.v); }
+inline void tally(uint64_t f, uint64_t m) {
+  if (g_mute == 0) { g_flops += f; g_mufu += m; }
+}
+inline Cnt operator+(Cnt a, Cnt b) { tally(1, 0); return Cnt(a.v + b.v); }
+inline Cnt operator-(Cnt a, Cnt b) { tally(1, 0); return Cnt(a.v - b.v); }
+inline Cnt operator*(Cnt a, Cnt b) { tally(1, 0); return Cnt(a.v * b.v); }
+inline Cnt operator/(Cnt a, Cnt b) { tally(4, 1); return Cnt(a.v / b.v); }
+// Scope of an operation that is neutral for this scene: uncounted in lean mode (no
+// effect on fp64 / fp32 runs, or on the default counting convention).
+struct Neutral {
+  bool on;
+  explicit Neutral(bool neutral) : on(neutral && g_lean) { if (on) ++g_mute; }
+  ~Neutral() { if (on) --g_mute; }
+};
 inline Cnt operator-(Cnt a) { return Cnt(-a.v); }
 inline bool operator<(Cnt a, Cnt b) { return a.v < b.v; }
 inline bool operator>(Cnt a, Cnt b) { return a.v > b.v; }
@@ -56,15 +73,15 @@ inline Cnt& operator-=(Cnt& a, Cnt b) { a = a - b; return a; }
 inline double val(double x) { return x; }
 inline double val(Cnt x) { return x.v; }
 inline double xsqrt(double x) { return std::sqrt(x); }
-inline Cnt xsqrt(Cnt x) { g_flops += 4; g_mufu += 1; return Cnt(std::sqrt(x.v)); }
+inline Cnt xsqrt(Cnt x) { tally(4, 1); return Cnt(std::sqrt(x.v)); }
 inline double xatan2(double y, double x) { return std::atan2(y, x); }
-inline Cnt xatan2(Cnt y, Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::atan2(y.v, x.v)); }
+inline Cnt xatan2(Cnt y, Cnt x) { tally(20, 1); return Cnt(std::atan2(y.v, x.v)); }
 inline double xasin(double x) { return std::asin(x); }
 inline double xsin(double x) { return std::sin(x); }
 inline double xcos(double x) { return std::cos(x); }
-inline Cnt xsin(Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::sin(x.v)); }
-inline Cnt xcos(Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::cos(x.v)); }
-inline Cnt xasin(Cnt x) { g_flops += 20; g_mufu += 1; return Cnt(std::asin(x.v)); }
+inline Cnt xsin(Cnt x) { tally(20, 1); return Cnt(std::sin(x.v)); }
+inline Cnt xcos(Cnt x) { tally(20, 1); return Cnt(std::cos(x.v)); }
+inline Cnt xasin(Cnt x) { tally(20, 1); return Cnt(std::asin(x.v)); }
 // fp32 instantiation (diagnostic only: measures the fp32 rounding floor of the
 // same algorithm; never used as a parity reference)
 inline double val(float x) { return x; }
@@ -110,6 +127,31 @@ template <class T> inline V3<T> inv_rotate(Q4<T> q, V3<T> v) { return rotate(qco
 // I_w⁻¹(q)·v = rotate(q, inv_rotate(q, v) ⊘ I_b)   (R4: world inverse inertia)
 template <class T> inline V3<T> inv_inertia_world(Q4<T> q, V3<T> inertia, V3<T> v) {
   return rotate(q, divide(inv_rotate(q, v), inertia));
+}
+// lean count of an isotropic I_w⁻¹·v: three products v·(1/I) (1/I a scene constant)
+template <class T> inline void lean_iso_count(V3<T> inertia) {
+  if (g_lean && val(inertia.x) == val(inertia.y) && val(inertia.y) == val(inertia.z)) tally(3, 0);
+}
+template <class T> inline bool iso(V3<T> inertia) {
+  return val(inertia.x) == val(inertia.y) && val(inertia.y) == val(inertia.z);
+}
+inline bool ones3(const double* m) { return m[0] == 1.0 && m[1] == 1.0 && m[2] == 1.0; }
+inline bool zero3(const double* m) { return m[0] == 0.0 && m[1] == 0.0 && m[2] == 0.0; }
+inline bool ident4(const double* q) { return q[0] == 1.0 && q[1] == 0.0 && q[2] == 0.0 && q[3] == 0.0; }
+// mask ⊙ v, neutral (lean count) when no axis is frozen
+template <class T> inline V3<T> mhad(const double* m, V3<T> v) {
+  Neutral n(ones3(m));
+  return hadamard(V3<T>{T(m[0]), T(m[1]), T(m[2])}, v);
+}
+// I_w⁻¹·v counted leanly: an isotropic body's rotate / divide / rotate is three products
+template <class T> inline V3<T> iiw(Q4<T> q, V3<T> inertia, V3<T> v) {
+  V3<T> r;
+  {
+    Neutral n(iso(inertia));
+    r = inv_inertia_world(q, inertia, v);
+  }
+  lean_iso_count(inertia);
+  return r;
 }
 
 // ----------------------------------------------------------------------------
@@ -199,10 +241,12 @@ void narrowphase(const OSys& S, const OSlot& sl, const BodyState<T>* st, double 
   const OCollider& CB = S.colliders[sl.col_b];
   const BodyState<T>& A = st[sl.a];
   const BodyState<T>& Bs = st[sl.b];
-  V3<T> cA = A.x + rotate(A.q, V<T>(CA.pos));
-  V3<T> cB = Bs.x + rotate(Bs.q, V<T>(CB.pos));
-  Q4<T> qA = qmul(A.q, Q<T>(CA.rot));
-  Q4<T> qB = qmul(Bs.q, Q<T>(CB.rot));
+  V3<T> cA, cB;
+  Q4<T> qA, qB;
+  { Neutral n(zero3(CA.pos)); cA = A.x + rotate(A.q, V<T>(CA.pos)); }
+  { Neutral n(zero3(CB.pos)); cB = Bs.x + rotate(Bs.q, V<T>(CB.pos)); }
+  { Neutral n(ident4(CA.rot)); qA = qmul(A.q, Q<T>(CA.rot)); }
+  { Neutral n(ident4(CB.rot)); qB = qmul(Bs.q, Q<T>(CB.rot)); }
   const V3<T> zhat = v3(T(0.0), T(0.0), T(1.0));
   V3<T> n, pt;
   T d;
@@ -262,6 +306,7 @@ struct EnvOut {
   uint8_t* active;
   bool ambiguous;
   double* contact_dv;  // [B][6] or NULL: the collision integrator's Δv, Δω of this substep (NEXT-1 obs)
+  double* contact_dp;  // [B][6] or NULL: the same summed over the step's substeps (brax_step_extras.contact_dp)
 };
 
 // One substep of Alg. 1 on one env.  `st` holds all B bodies.
@@ -275,9 +320,9 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     const OBody& bd = S.bodies[b];
     if (bd.is_static) continue;  // R21: fully frozen body is bitwise unchanged
     BodyState<T>& s = st[b];
-    s.x = s.x + h * hadamard(V<T>(bd.mpos), s.v);
+    s.x = s.x + h * mhad(bd.mpos, s.v);
     if (!bd.rot_frozen) {
-      V3<T> wm = hadamard(V<T>(bd.mrot), s.w);
+      V3<T> wm = mhad(bd.mrot, s.w);
       Q4<T> dq = qmul(Q4<T>{T(0.0), wm.x, wm.y, wm.z}, s.q);
       T hh = T(0.5) * h;
       Q4<T> q{s.q.w + hh * dq.w, s.q.x + hh * dq.x, s.q.y + hh * dq.y, s.q.z + hh * dq.z};
@@ -298,8 +343,15 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     V3<T> rp = rotate(P.q, V<T>(J.o_p));
     V3<T> rc = rotate(C.q, V<T>(J.o_c));
     V3<T> dx = (P.x - C.x) + (rp - rc);                                  // evaluated in this order
-    V3<T> dv = (P.v + cross(P.w, rp)) - (C.v + cross(C.w, rc));
-    V3<T> f = T(J.k) * dx + T(J.c_l) * dv;                              // force on child
+    const bool no_cl = J.c_l == 0.0, no_ca = J.c_a == 0.0;             // lean count: neutral damping terms
+    V3<T> dv, cdv, f;
+    {
+      Neutral n(no_cl);
+      dv = (P.v + cross(P.w, rp)) - (C.v + cross(C.w, rc));
+      cdv = T(J.c_l) * dv;
+    }
+    const V3<T> kdx = T(J.k) * dx;
+    { Neutral n(no_cl); f = kdx + cdv; }                               // F = k·Δx + c_l·Δv, force on child
     Q4<T> fp = qmul(P.q, Q<T>(J.jp));
     Q4<T> fc = qmul(C.q, Q<T>(J.jc));
     Q4<T> qr = qmul(qconj(fp), fc);
@@ -348,11 +400,12 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     V3<T> b2 = v3(T(0.0), -(s0 * ic), c0 * ic);
     V3<T> tj = tau[0] * b0 + tau[1] * b1 + tau[2] * b2;
     V3<T> tw = rotate(fp, tj);
-    V3<T> td = T(J.c_a) * (P.w - C.w);
+    V3<T> td, twd_c, twd_p;
+    { Neutral n(no_ca); td = T(J.c_a) * (P.w - C.w); twd_c = tw + td; twd_p = tw + td; }
     F[J.child] = F[J.child] + f;
-    Tq[J.child] = Tq[J.child] + ((tw + td) + cross(rc, f));
+    Tq[J.child] = Tq[J.child] + (twd_c + cross(rc, f));
     F[J.parent] = F[J.parent] - f;
-    Tq[J.parent] = Tq[J.parent] - ((tw + td) + cross(rp, f));
+    Tq[J.parent] = Tq[J.parent] - (twd_p + cross(rp, f));
   }
 
   // ---- 4. contacts, velocity level + Baumgarte (R13-R19)
@@ -379,11 +432,11 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
       T k(0.0);
       if (!bA.is_static) {
         V3<T> rn = cross(rA, dir);
-        k = k + T(1.0) / T(bA.mass) + dot(rn, inv_inertia_world(A.q, V<T>(bA.inertia), rn));
+        k = k + T(1.0) / T(bA.mass) + dot(rn, iiw(A.q, V<T>(bA.inertia), rn));
       }
       if (!bB.is_static) {
         V3<T> rn = cross(rB, dir);
-        k = k + T(1.0) / T(bB.mass) + dot(rn, inv_inertia_world(Bs.q, V<T>(bB.inertia), rn));
+        k = k + T(1.0) / T(bB.mass) + dot(rn, iiw(Bs.q, V<T>(bB.inertia), rn));
       }
       return k;
     };
@@ -401,12 +454,12 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     }
     if (!bA.is_static) {
       dV[sl.a] = dV[sl.a] + (T(1.0) / T(bA.mass)) * P;
-      dW[sl.a] = dW[sl.a] + inv_inertia_world(A.q, V<T>(bA.inertia), cross(rA, P));
+      dW[sl.a] = dW[sl.a] + iiw(A.q, V<T>(bA.inertia), cross(rA, P));
       cnt[sl.a] += 1;
     }
     if (!bB.is_static) {
       dV[sl.b] = dV[sl.b] - (T(1.0) / T(bB.mass)) * P;
-      dW[sl.b] = dW[sl.b] - inv_inertia_world(Bs.q, V<T>(bB.inertia), cross(rB, P));
+      dW[sl.b] = dW[sl.b] - iiw(Bs.q, V<T>(bB.inertia), cross(rB, P));
       cnt[sl.b] += 1;
     }
     if (out->active) out->active[i] += 1;
@@ -418,8 +471,8 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     const OBody& bd = S.bodies[b];
     if (bd.is_static) continue;
     BodyState<T>& s = st[b];
-    s.v = hadamard(V<T>(bd.mpos), s.v + h * ((T(1.0) / T(bd.mass)) * F[b] + g));
-    s.w = hadamard(V<T>(bd.mrot), s.w + h * inv_inertia_world(s.q, V<T>(bd.inertia), Tq[b]));
+    s.v = mhad(bd.mpos, s.v + h * ((T(1.0) / T(bd.mass)) * F[b] + g));
+    s.w = mhad(bd.mrot, s.w + h * iiw(s.q, V<T>(bd.inertia), Tq[b]));
   }
   // ---- 6. collision integrator (R14 mean over active contacts) -
   for (int b = 0; b < B; ++b) {
@@ -430,13 +483,15 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
     BodyState<T>& s = st[b];
     const V3<T> v0 = s.v, w0 = s.w;
     T scale = opt.combine_sum ? T(1.0) : T(1.0) / T(double(cnt[b]));
-    s.v = hadamard(V<T>(bd.mpos), s.v + scale * dV[b]);
-    s.w = hadamard(V<T>(bd.mrot), s.w + scale * dW[b]);
-    if (out->contact_dv) {  // velocity change of the collision integrator: after − before
+    s.v = mhad(bd.mpos, s.v + scale * dV[b]);
+    s.w = mhad(bd.mrot, s.w + scale * dW[b]);
+    if (out->contact_dv || out->contact_dp) {  // velocity change of the collision integrator: after − before
       const V3<T> dv = s.v - v0, dw = s.w - w0;
-      double* o = out->contact_dv + 6 * b;
-      o[0] = val(dv.x); o[1] = val(dv.y); o[2] = val(dv.z);
-      o[3] = val(dw.x); o[4] = val(dw.y); o[5] = val(dw.z);
+      const double d6[6] = {val(dv.x), val(dv.y), val(dv.z), val(dw.x), val(dw.y), val(dw.z)};
+      if (out->contact_dv)
+        for (int k = 0; k < 6; ++k) out->contact_dv[6 * b + k] = d6[k];
+      if (out->contact_dp)
+        for (int k = 0; k < 6; ++k) out->contact_dp[6 * b + k] += d6[k];
     }
   }
 }
@@ -444,7 +499,7 @@ void substep(const OSys& S, const OOpts& opt, BodyState<T>* st, const double* ac
 template <class T>
 void step_range(const OSys& S, const OOpts& opt, int64_t e0, int64_t e1, double* pos, double* rot,
                 double* vel, double* ang, const double* action, uint8_t* contact_active,
-                uint32_t* status, uint8_t* ambiguous, double* contact_dv) {
+                uint32_t* status, uint8_t* ambiguous, double* contact_dv, double* contact_dp) {
   const int B = S.nb;
   std::vector<BodyState<T>> st(B);
   for (int64_t e = e0; e < e1; ++e) {
@@ -459,8 +514,9 @@ void step_range(const OSys& S, const OOpts& opt, int64_t e0, int64_t e1, double*
       st[b].w = V<T>(w + 3 * b);
     }
     EnvOut<T> out{contact_active ? contact_active + e * S.ns : nullptr, false,
-                  contact_dv ? contact_dv + e * B * 6 : nullptr};
+                  contact_dv ? contact_dv + e * B * 6 : nullptr, contact_dp ? contact_dp + e * B * 6 : nullptr};
     if (out.active) std::memset(out.active, 0, S.ns);
+    if (out.contact_dp) std::memset(out.contact_dp, 0, sizeof(double) * 6 * B);
     const double* a = action ? action + e * S.act_dim : nullptr;
     for (int s = 0; s < S.substeps; ++s) substep<T>(S, opt, st.data(), a, &out);
     uint32_t stat = 0;
@@ -491,22 +547,23 @@ extern "C" {
 // contact_active: [n][ns] u8 number of substeps each slot was active (or NULL).
 // status: [n] bit0 non-finite, bit1 |x| > 1e6 (or NULL).  ambiguous: [n] R23 flag (or NULL).
 // contact_dv: [n][B][6] the last substep's collision-integrator Δv, Δω per body (or NULL).
+// contact_dp: [n][B][6] the same summed over the step's substeps (or NULL).
 int oracle_step(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, double* pos, double* rot,
                 double* vel, double* ang, const double* action, uint8_t* contact_active,
-                uint32_t* status, uint8_t* ambiguous, double* contact_dv) {
+                uint32_t* status, uint8_t* ambiguous, double* contact_dv, double* contact_dp) {
   if (!S || !opt || e1 < e0) return 1;
   step_range<double>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous,
-                     contact_dv);
+                     contact_dv, contact_dp);
   return 0;
 }
 
 // Diagnostic: the same step in fp32 arithmetic (inputs/outputs fp64 arrays).
 int oracle_step_f32(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, double* pos, double* rot,
                     double* vel, double* ang, const double* action, uint8_t* contact_active,
-                    uint32_t* status, uint8_t* ambiguous, double* contact_dv) {
+                    uint32_t* status, uint8_t* ambiguous, double* contact_dv, double* contact_dp) {
   if (!S || !opt || e1 < e0) return 1;
   step_range<float>(*S, *opt, e0, e1, pos, rot, vel, ang, action, contact_active, status, ambiguous,
-                    contact_dv);
+                    contact_dv, contact_dp);
   return 0;
 }
 
@@ -518,7 +575,8 @@ int oracle_count_ops(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, do
   if (!S || !opt || e1 < e0) return 1;
   g_flops = 0;
   g_mufu = 0;
-  step_range<Cnt>(*S, *opt, e0, e1, pos, rot, vel, ang, action, nullptr, nullptr, nullptr, nullptr);
+  g_mute = 0;
+  step_range<Cnt>(*S, *opt, e0, e1, pos, rot, vel, ang, action, nullptr, nullptr, nullptr, nullptr, nullptr);
   *flops = g_flops;
   *mufu = g_mufu;
   return 0;
@@ -543,6 +601,15 @@ int oracle_slot_geometry(const OSys* S, int32_t slot, const double* pos, const d
   n[0] = nn.x; n[1] = nn.y; n[2] = nn.z;
   pt[0] = pp.x; pt[1] = pp.y; pt[2] = pp.z;
   return par ? 1 : 0;
+}
+
+// The same count in the "lean" convention (see g_lean): scene-neutral operations uncounted.
+int oracle_count_ops_lean(const OSys* S, const OOpts* opt, int64_t e0, int64_t e1, double* pos, double* rot,
+                          double* vel, double* ang, const double* action, uint64_t* flops, uint64_t* mufu) {
+  g_lean = true;
+  const int rc = oracle_count_ops(S, opt, e0, e1, pos, rot, vel, ang, action, flops, mufu);
+  g_lean = false;
+  return rc;
 }
 
 int oracle_abi_version(void) { return 1; }

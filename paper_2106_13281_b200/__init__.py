@@ -26,7 +26,8 @@ __all__ = [
     "brax_step_ex", "brax_rollout", "brax_qp", "brax_step_extras", "brax_system_info", "LIB_PATH", "lib",
     "brax_env_io", "brax_system_task_info", "brax_env_step", "brax_env_reset", "brax_env_observe",
     "brax_random_actions", "brax_rollout_random", "brax_env_step_random", "brax_step_jvp",
-    "brax_step_vjp",
+    "brax_step_vjp", "brax_config_from_desc", "brax_system_tune", "brax_config_desc", "brax_body_desc",
+    "brax_joint_desc", "brax_actuator_desc", "brax_collider_desc", "brax_body_pair",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbrax_b200.so")
@@ -53,7 +54,47 @@ class brax_qp(C.Structure):
 
 
 class brax_step_extras(C.Structure):
-    _fields_ = [("status", C.c_void_p), ("contact_active", C.c_void_p)]
+    _fields_ = [("status", C.c_void_p), ("contact_active", C.c_void_p), ("contact_dp", C.c_void_p)]
+
+
+# programmatic config descriptors (brax_config_from_desc)
+class brax_body_desc(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("mass", C.c_double), ("inertia", C.c_double * 3),
+                ("frozen_pos", C.c_double * 3), ("frozen_rot", C.c_double * 3), ("init_pos", C.c_double * 3),
+                ("init_rot", C.c_double * 4)]
+
+
+class brax_joint_desc(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("parent", C.c_int32), ("child", C.c_int32),
+                ("parent_offset", C.c_double * 3), ("child_offset", C.c_double * 3), ("rotation", C.c_double * 4),
+                ("reference_rotation", C.c_double * 4), ("dof", C.c_int32), ("limit_lo", C.c_double * 3),
+                ("limit_hi", C.c_double * 3), ("stiffness", C.c_double), ("spring_damping", C.c_double),
+                ("angular_damping", C.c_double), ("limit_stiffness", C.c_double),
+                ("angular_stiffness", C.c_double)]
+
+
+class brax_actuator_desc(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("joint", C.c_int32), ("kind", C.c_int32), ("strength", C.c_double)]
+
+
+class brax_collider_desc(C.Structure):
+    _fields_ = [("body", C.c_int32), ("shape", C.c_int32), ("pos", C.c_double * 3), ("rot", C.c_double * 4),
+                ("radius", C.c_double), ("length", C.c_double), ("halfsize", C.c_double * 3),
+                ("capsule_end", C.c_int32)]
+
+
+class brax_body_pair(C.Structure):
+    _fields_ = [("first", C.c_int32), ("second", C.c_int32)]
+
+
+class brax_config_desc(C.Structure):
+    _fields_ = [("dt", C.c_double), ("substeps", C.c_int32), ("gravity", C.c_double * 3),
+                ("friction", C.c_double), ("elasticity", C.c_double), ("baumgarte_erp", C.c_double),
+                ("n_bodies", C.c_int32), ("n_joints", C.c_int32), ("n_actuators", C.c_int32),
+                ("n_colliders", C.c_int32), ("n_pairs", C.c_int32),
+                ("bodies", C.POINTER(brax_body_desc)), ("joints", C.POINTER(brax_joint_desc)),
+                ("actuators", C.POINTER(brax_actuator_desc)), ("colliders", C.POINTER(brax_collider_desc)),
+                ("pairs", C.POINTER(brax_body_pair))]
 
 
 class brax_env_io(C.Structure):
@@ -77,6 +118,8 @@ _i32p = C.POINTER(C.c_int32)
 _SIGS = {
     "brax_config_parse": ([C.c_char_p, C.c_size_t, C.POINTER(_P)], C.c_int),
     "brax_config_destroy": ([_P], None),
+    "brax_config_from_desc": ([C.POINTER(brax_config_desc), C.POINTER(_P)], C.c_int),
+    "brax_system_tune": ([_P, brax_qp, _P, C.c_int64, _P], C.c_int),
     "brax_config_counts": ([_P, _i32p, _i32p, _i32p, _i32p], C.c_int),
     "brax_config_slot_table": ([_P, _i32p], C.c_int),
     "brax_config_default_qp": ([_P, _P, _P], C.c_int),
@@ -129,6 +172,18 @@ def brax_config_parse(text: str) -> int:
 
 def brax_config_destroy(cfg: int) -> None:
     lib.brax_config_destroy(cfg)
+
+
+def brax_config_from_desc(desc: "brax_config_desc") -> int:
+    """desc: a filled brax_config_desc (its arrays must stay alive during the call)."""
+    out = _P()
+    _check(lib.brax_config_from_desc(C.byref(desc), C.byref(out)))
+    return out.value
+
+
+def brax_system_tune(sys: int, qp_in, action, n_envs: int, stream=None) -> None:
+    _check(lib.brax_system_tune(sys, _qp(qp_in), None if action is None else action.data_ptr(), n_envs,
+                                _stream(stream)))
 
 
 def brax_config_counts(cfg: int):
@@ -209,23 +264,24 @@ def brax_step(sys: int, qp_in, action, qp_out, n_envs: int, stream=None) -> None
                          _stream(stream)))
 
 
-def _extras(status, contact_active):
-    if status is None and contact_active is None:
+def _extras(status, contact_active, contact_dp=None):
+    if status is None and contact_active is None and contact_dp is None:
         return None
     return brax_step_extras(None if status is None else status.data_ptr(),
-                            None if contact_active is None else contact_active.data_ptr())
+                            None if contact_active is None else contact_active.data_ptr(),
+                            None if contact_dp is None else contact_dp.data_ptr())
 
 
 def brax_step_ex(sys: int, qp_in, action, qp_out, n_envs: int, status=None, contact_active=None,
-                 stream=None) -> None:
-    x = _extras(status, contact_active)
+                 stream=None, contact_dp=None) -> None:
+    x = _extras(status, contact_active, contact_dp)
     _check(lib.brax_step_ex(sys, _qp(qp_in), None if action is None else action.data_ptr(), _qp(qp_out), n_envs,
                             None if x is None else C.byref(x), _stream(stream)))
 
 
 def brax_rollout(sys: int, qp_in, actions, n_steps: int, qp_out, n_envs: int, status=None, contact_active=None,
-                 stream=None) -> None:
-    x = _extras(status, contact_active)
+                 stream=None, contact_dp=None) -> None:
+    x = _extras(status, contact_active, contact_dp)
     _check(lib.brax_rollout(sys, _qp(qp_in), None if actions is None else actions.data_ptr(), n_steps,
                             _qp(qp_out), n_envs, None if x is None else C.byref(x), _stream(stream)))
 
@@ -299,8 +355,10 @@ def brax_env_observe(sys: int, qp, n_envs: int, obs, stream=None) -> None:
 class System:
     """A config parsed and turned into a device-resident system (owns both handles)."""
 
-    def __init__(self, text: str, device: int = 0):
-        self._cfg = brax_config_parse(text)
+    def __init__(self, text: str = None, device: int = 0, *, desc: "brax_config_desc" = None):
+        if (text is None) == (desc is None):
+            raise ValueError("give exactly one of text or desc")
+        self._cfg = brax_config_parse(text) if text is not None else brax_config_from_desc(desc)
         try:
             self._sys = brax_system_create(self._cfg, device)
         except Exception:
@@ -367,14 +425,18 @@ class System:
         brax_reset(self._sys, qp, qp["pos"].shape[0], seed, vel_noise, ang_noise, stream)
         return qp
 
-    def step(self, qp_in, action, qp_out=None, *, status=None, contact_active=None, stream=None):
+    def step(self, qp_in, action, qp_out=None, *, status=None, contact_active=None, contact_dp=None, stream=None):
         qp_out = qp_in if qp_out is None else qp_out
         n = qp_in["pos"].shape[0]
-        if status is None and contact_active is None:
+        if status is None and contact_active is None and contact_dp is None:
             brax_step(self._sys, qp_in, action, qp_out, n, stream)
         else:
-            brax_step_ex(self._sys, qp_in, action, qp_out, n, status, contact_active, stream)
+            brax_step_ex(self._sys, qp_in, action, qp_out, n, status, contact_active, stream, contact_dp)
         return qp_out
+
+    def tune(self, qp_in, action, *, stream=None):
+        """brax_system_tune for qp_in's batch size (synchronises; not graph-capturable)."""
+        brax_system_tune(self._sys, qp_in, action, qp_in["pos"].shape[0], stream)
 
     # ---- NEXT-1 env epilogue (needs a `task` block) ----
     def task_info(self):
@@ -492,9 +554,9 @@ class System:
         return obs
 
     def rollout(self, qp_in, actions, qp_out=None, *, n_steps=None, status=None, contact_active=None,
-                stream=None):
+                contact_dp=None, stream=None):
         qp_out = qp_in if qp_out is None else qp_out
         n = qp_in["pos"].shape[0]
         T = n_steps if n_steps is not None else actions.shape[0]
-        brax_rollout(self._sys, qp_in, actions, T, qp_out, n, status, contact_active, stream)
+        brax_rollout(self._sys, qp_in, actions, T, qp_out, n, status, contact_active, stream, contact_dp)
         return qp_out

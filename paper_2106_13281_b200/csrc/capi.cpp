@@ -42,6 +42,21 @@ brax_status check_qp(const brax_qp& q, const char* which) {
   return BRAX_OK;
 }
 
+// Makes `device` current for the lifetime of the guard and restores the caller's
+// current device afterwards (header convention "Device").
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != device) err = cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 brax_status cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return BRAX_OK;
   return fail(e == cudaErrorMemoryAllocation ? BRAX_E_OUT_OF_MEMORY : BRAX_E_CUDA,
@@ -87,9 +102,12 @@ brax_status step_common(const brax_system* sys, brax_qp in, const float* actions
         if (a0 < b1 && b0 < a1) return fail(BRAX_E_INVALID_ARGUMENT, "out arrays overlap");
       }
   }
+  if (x && x->contact_dp && !aligned16(x->contact_dp)) return fail(BRAX_E_MISALIGNED, "contact_dp must be 16-byte aligned");
+  if (x && x->contact_dp && env) return fail(BRAX_E_INVALID_ARGUMENT, "contact_dp is not an env-step output");
   brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, out.pos, out.rot, out.vel, out.ang, actions,
                    x ? x->status : nullptr, x ? x->contact_active : nullptr, n_envs, n_steps, 0, 0, nullptr};
   if (a.contact_active && s.hd.C == 0) a.contact_active = nullptr;
+  a.contact_dp = x ? x->contact_dp : nullptr;
   if (ra && s.hd.A > 0) {
     a.act_random = 1;
     a.act_seed = ra->seed;
@@ -114,12 +132,8 @@ brax_status step_common(const brax_system* sys, brax_qp in, const float* actions
       a.env_offset = io->env_offset;
     }
   }
-  int cur = -1;
-  cudaGetDevice(&cur);
-  if (cur != s.device) {
-    cudaError_t e = cudaSetDevice(s.device);
-    if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
-  }
+  DeviceGuard dg(s.device);
+  if (dg.err != cudaSuccess) return cuda_status(dg.err, "cudaSetDevice");
   return cuda_status(brax::launch_step(s, a, static_cast<cudaStream_t>(stream)), "brax_step launch");
 }
 }  // namespace
@@ -154,6 +168,15 @@ brax_status brax_config_parse(const char* text, size_t len, brax_config** out) {
 }
 
 void brax_config_destroy(brax_config* cfg) { delete cfg; }
+
+brax_status brax_config_from_desc(const brax_config_desc* desc, brax_config** out) {
+  if (!desc || !out) return fail(BRAX_E_INVALID_ARGUMENT, "desc and out must be non-NULL");
+  return guarded([&] {
+    brax_config* c = new brax_config{brax::config_from_desc(*desc)};
+    *out = c;
+    return BRAX_OK;
+  });
+}
 
 brax_status brax_config_slot_table(const brax_config* cfg, int32_t* out) {
   if (!cfg || !out) return fail(BRAX_E_INVALID_ARGUMENT, "cfg and out must be non-NULL");
@@ -236,7 +259,7 @@ brax_status brax_system_set_tracing(brax_system* sys, int enable) {
 
 brax_status brax_system_phase_cycles(brax_system* sys, uint64_t out[4]) {
   if (!sys || !out) return fail(BRAX_E_INVALID_ARGUMENT, "NULL argument");
-  cudaSetDevice(sys->impl->device);
+  DeviceGuard dg(sys->impl->device);
   unsigned long long h[4];
   cudaError_t e = cudaMemcpy(h, sys->impl->d_phase_cycles, sizeof h, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemset(sys->impl->d_phase_cycles, 0, sizeof h);
@@ -249,6 +272,22 @@ brax_status brax_system_set_autotune(brax_system* sys, int enable) {
   if (!sys) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
   sys->impl->autotune = enable != 0;
   return BRAX_OK;
+}
+
+brax_status brax_system_tune(brax_system* sys, brax_qp in, const float* action, int64_t n_envs, void* stream) {
+  if (!sys || !sys->impl) return fail(BRAX_E_INVALID_ARGUMENT, "sys is NULL");
+  if (n_envs < 0) return fail(BRAX_E_INVALID_ARGUMENT, "n_envs must be >= 0");
+  if (n_envs == 0 || !sys->impl->autotune) return BRAX_OK;
+  brax_status st = check_qp(in, "in");
+  if (st != BRAX_OK) return st;
+  const brax::System& s = *sys->impl;
+  if (s.hd.A > 0 && !action) return fail(BRAX_E_INVALID_ARGUMENT, "action is NULL but act_dim > 0");
+  if (action && !aligned16(action)) return fail(BRAX_E_MISALIGNED, "action must be 16-byte aligned");
+  DeviceGuard dg(s.device);
+  if (dg.err != cudaSuccess) return cuda_status(dg.err, "cudaSetDevice");
+  brax::StepArgs a{in.pos, in.rot, in.vel, in.ang, nullptr, nullptr, nullptr, nullptr, action,
+                   nullptr, nullptr, n_envs, 1, 0, 0, nullptr};
+  return cuda_status(brax::tune_system(s, a, static_cast<cudaStream_t>(stream)), "brax_system_tune");
 }
 
 brax_status brax_system_launch_config(const brax_system* sys, int64_t n_envs, int32_t out[6]) {
@@ -288,7 +327,7 @@ brax_status brax_reset(const brax_system* sys, brax_qp out, int64_t n_envs, uint
   if (n_envs == 0) return BRAX_OK;
   brax_status st = check_qp(out, "out");
   if (st != BRAX_OK) return st;
-  cudaSetDevice(sys->impl->device);
+  DeviceGuard dg(sys->impl->device);
   return cuda_status(brax::launch_reset(*sys->impl, out.pos, out.rot, out.vel, out.ang, n_envs, seed, vel_noise,
                                         ang_noise, static_cast<cudaStream_t>(stream)),
                      "brax_reset launch");
@@ -343,7 +382,7 @@ brax_status brax_step_jvp(const brax_system* sys, brax_qp in, const float* actio
   a.drot_out = dout.rot;
   a.dvel_out = dout.vel;
   a.dang_out = dout.ang;
-  cudaSetDevice(s.device);
+  DeviceGuard dg(s.device);
   cudaError_t e = brax::launch_step_jvp(s, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorInvalidValue) return fail(BRAX_E_VALIDATION, "brax_step_jvp: system too large for the JVP kernel");
   return cuda_status(e, "brax_step_jvp launch");
@@ -363,7 +402,7 @@ brax_status brax_step_vjp(const brax_system* sys, brax_qp in, const float* actio
                    nullptr, nullptr, n_envs, 1, 0, 0, nullptr};
   const float* go[4] = {g_out.pos, g_out.rot, g_out.vel, g_out.ang};
   float* gi[4] = {g_in.pos, g_in.rot, g_in.vel, g_in.ang};
-  cudaSetDevice(s.device);
+  DeviceGuard dg(s.device);
   cudaError_t e = std::getenv("BRAX_VJP_COLUMNS")
                       ? brax::launch_step_vjp(s, a, go, gi, g_action, static_cast<cudaStream_t>(stream))
                       : brax::launch_step_vjp_fused(s, a, go, gi, g_action, static_cast<cudaStream_t>(stream));
@@ -402,7 +441,7 @@ brax_status brax_env_reset(const brax_system* sys, brax_qp out, int64_t n_envs, 
   if (n_envs == 0) return BRAX_OK;
   brax_status st = check_qp(out, "out");
   if (st != BRAX_OK) return st;
-  cudaSetDevice(s.device);
+  DeviceGuard dg(s.device);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = brax::launch_reset(s, out.pos, out.rot, out.vel, out.ang, n_envs, io->seed,
                                      float(s.cfg.task.noise_vel), float(s.cfg.task.noise_ang), cs, io->env_offset);

@@ -4,6 +4,7 @@
 //   file := field* ;  field := NAME ':' scalar | NAME ':'? '{' field* '}'
 // '#' comments, ',' and ';' separators are ignored.  Semantic rules (defaults,
 // pair enumeration R19, forest check) follow SPEC.md:290-298 and SURVEY §8(c).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <map>
@@ -228,6 +229,108 @@ void euler_field(const std::vector<Node>* node, const std::string& path, double 
 
 std::string idx(const char* what, size_t i) { return std::string(what) + "[" + std::to_string(i) + "]"; }
 
+struct ActuatorSpec { std::string name; int joint = 0; double strength = 0; ActuatorKind kind = kTorque; std::string path; };
+struct IncludeSpec { int first, second; std::string path; };
+
+// Checks and derived tables shared by the text parser and the programmatic
+// descriptors (brax_config_from_desc): the joint forest, actuators folded into
+// their joints (action offsets in actuator order, dof-major), and the contact
+// pair list + slot table (naive pairwise collision; rule R19).
+void finalize_config(Config& c, const std::vector<ActuatorSpec>& acts, const std::vector<IncludeSpec>* include) {
+  // forest: every body is the child of at most one joint, no cycles
+  std::vector<int> parent_of(c.bodies.size(), -1);
+  for (size_t ji = 0; ji < c.joints.size(); ++ji) {
+    int ch = c.joints[ji].child;
+    if (parent_of[ch] >= 0) invalid(idx("joints", ji) + ".child", "body is already the child of another joint");
+    parent_of[ch] = c.joints[ji].parent;
+  }
+  for (size_t b = 0; b < c.bodies.size(); ++b) {
+    size_t steps = 0;
+    for (int x = int(b); parent_of[x] >= 0; x = parent_of[x])
+      if (++steps > c.bodies.size()) invalid(idx("bodies", b), "cyclic joint graph", BRAX_E_CYCLIC_JOINT_GRAPH);
+  }
+
+  std::set<int> actuated;
+  for (const ActuatorSpec& s : acts) {
+    if (s.joint < 0 || s.joint >= int(c.joints.size())) invalid(s.path + ".joint", "unknown joint");
+    if (actuated.count(s.joint)) invalid(s.path + ".joint", "joint already has an actuator");
+    if (c.joints[s.joint].dof == 0) invalid(s.path + ".joint", "actuated joint must have dof >= 1");
+    actuated.insert(s.joint);
+    Actuator a;
+    a.name = s.name;
+    a.joint = s.joint;
+    a.strength = s.strength;
+    a.kind = s.kind;
+    a.act_offset = c.act_dim;
+    c.act_dim += c.joints[a.joint].dof;
+    Joint& j = c.joints[a.joint];
+    j.act_kind = a.kind;
+    j.act_strength = a.strength;
+    j.act_offset = a.act_offset;
+    c.actuators.push_back(a);
+  }
+
+  // ---- pairs (naive pairwise collision, PAPER.md:284; enumeration rule R19) ----
+  struct Cand { int i, j; std::string path; };
+  std::vector<Cand> cand;
+  if (include) {
+    for (const IncludeSpec& in : *include) {
+      const int ba = in.first, bb = in.second;
+      if (ba < 0 || bb < 0 || ba >= int(c.bodies.size()) || bb >= int(c.bodies.size()))
+        invalid(in.path, "unknown body");
+      if (ba == bb) invalid(in.path, "a body cannot collide with itself");
+      if (c.bodies[ba].is_static() && c.bodies[bb].is_static()) invalid(in.path, "static-static pair");
+      for (size_t i = 0; i < c.colliders.size(); ++i)
+        if (c.colliders[i].body == ba)
+          for (size_t j = 0; j < c.colliders.size(); ++j)
+            if (c.colliders[j].body == bb) cand.push_back({int(i), int(j), in.path});
+    }
+  } else {
+    std::set<std::pair<int, int>> jointed;
+    for (const Joint& j : c.joints) {
+      jointed.insert({j.parent, j.child});
+      jointed.insert({j.child, j.parent});
+    }
+    for (size_t i = 0; i < c.colliders.size(); ++i)
+      for (size_t j = i + 1; j < c.colliders.size(); ++j) {
+        int bi = c.colliders[i].body, bj = c.colliders[j].body;
+        if (bi == bj || jointed.count({bi, bj})) continue;
+        if (c.bodies[bi].is_static() && c.bodies[bj].is_static()) continue;
+        cand.push_back({int(i), int(j), "colliders[" + std::to_string(i) + "]x[" + std::to_string(j) + "]"});
+      }
+  }
+  static const char* kind_name[] = {"sphere", "capsule", "box", "plane"};
+  for (const Cand& cd : cand) {
+    int a = cd.i, b = cd.j;
+    int ka = c.colliders[a].kind, kb = c.colliders[b].kind;  // enum order = orientation rank
+    if (ka > kb || (ka == kb && a > b)) { std::swap(a, b); std::swap(ka, kb); }
+    int type = -1;
+    if (kb == kPlane) type = (ka == kSphere) ? BRAX_SLOT_SPHERE_PLANE : (ka == kCapsule) ? BRAX_SLOT_CAPSULE_PLANE
+                                            : (ka == kBox) ? BRAX_SLOT_BOX_PLANE : -1;
+    else if (ka == kSphere && kb == kSphere) type = BRAX_SLOT_SPHERE_SPHERE;
+    else if (ka == kSphere && kb == kCapsule) type = BRAX_SLOT_SPHERE_CAPSULE;
+    else if (ka == kCapsule && kb == kCapsule) type = BRAX_SLOT_CAPSULE_CAPSULE;
+    if (type < 0)
+      invalid(cd.path, std::string("unsupported collider pair ") + kind_name[ka] + "-" + kind_name[kb],
+              BRAX_E_UNSUPPORTED_PAIR);
+    c.pairs.push_back({a, b, type});
+  }
+  for (size_t pi = 0; pi < c.pairs.size(); ++pi) {
+    const Pair& pr = c.pairs[pi];
+    const Collider& A = c.colliders[pr.col_a];
+    int first = 0, count = 1;
+    if (pr.type == BRAX_SLOT_CAPSULE_PLANE) {
+      if (A.end == 0) count = 2;
+      else first = (A.end == 1) ? 0 : 1;
+    } else if (pr.type == BRAX_SLOT_BOX_PLANE) {
+      count = 8;
+    }
+    for (int k = 0; k < count; ++k)
+      c.slots.push_back({int(pi), pr.type, A.body, c.colliders[pr.col_b].body, pr.col_a, pr.col_b, first + k});
+  }
+  if (c.slots.size() > 255) invalid("config", "more than 255 contact slots");
+}
+
 }  // namespace
 
 void euler_deg_to_quat(const double deg[3], double q[4]) {
@@ -402,107 +505,34 @@ Config parse_config(const std::string& text) {
     c.joints.push_back(j);
   }
 
-  // forest: every body is the child of at most one joint, no cycles
-  std::vector<int> parent_of(c.bodies.size(), -1);
-  for (size_t ji = 0; ji < c.joints.size(); ++ji) {
-    int ch = c.joints[ji].child;
-    if (parent_of[ch] >= 0) invalid(idx("joints", ji) + ".child", "body is already the child of another joint");
-    parent_of[ch] = c.joints[ji].parent;
-  }
-  for (size_t b = 0; b < c.bodies.size(); ++b) {
-    size_t steps = 0;
-    for (int x = int(b); parent_of[x] >= 0; x = parent_of[x])
-      if (++steps > c.bodies.size()) invalid(idx("bodies", b), "cyclic joint graph", BRAX_E_CYCLIC_JOINT_GRAPH);
-  }
-
+  // actuators and collide_include pairs (resolved by name), then the shared checks
+  std::vector<ActuatorSpec> acts;
   auto anodes = top.all("actuators");
-  std::set<int> actuated;
   for (size_t ai = 0; ai < anodes.size(); ++ai) {
     std::string path = idx("actuators", ai);
     Fields af(anodes[ai]->children, path, {"name", "joint", "strength", "torque", "angle"});
-    Actuator a;
+    ActuatorSpec a;
     a.name = af.str("name");
     std::string jn = af.str("joint");
     if (!joint_ix.count(jn)) invalid(path + ".joint", "unknown joint '" + jn + "'");
     if (af.has("torque") + af.has("angle") != 1) invalid(path, "exactly one of torque/angle required");
     a.joint = joint_ix[jn];
-    if (actuated.count(a.joint)) invalid(path + ".joint", "joint already has an actuator");
-    if (c.joints[a.joint].dof == 0) invalid(path + ".joint", "actuated joint must have dof >= 1");
-    actuated.insert(a.joint);
     a.strength = af.num("strength", 0);
     a.kind = af.has("torque") ? kTorque : kAngle;
-    a.act_offset = c.act_dim;
-    c.act_dim += c.joints[a.joint].dof;
-    Joint& j = c.joints[a.joint];
-    j.act_kind = a.kind;
-    j.act_strength = a.strength;
-    j.act_offset = a.act_offset;
-    c.actuators.push_back(a);
+    a.path = path;
+    acts.push_back(a);
   }
-
-  // ---- pairs (naive pairwise collision, PAPER.md:284; enumeration rule R19) ----
-  struct Cand { int i, j; std::string path; };
-  std::vector<Cand> cand;
+  std::vector<IncludeSpec> inc;
   auto inodes = top.all("collide_include");
-  if (!inodes.empty()) {
-    for (size_t ii = 0; ii < inodes.size(); ++ii) {
-      std::string path = idx("collide_include", ii);
-      Fields f(inodes[ii]->children, path, {"first", "second"});
-      std::string a = f.str("first"), b = f.str("second");
-      if (!body_ix.count(a)) invalid(path + ".first", "unknown body '" + a + "'");
-      if (!body_ix.count(b)) invalid(path + ".second", "unknown body '" + b + "'");
-      int ba = body_ix[a], bb = body_ix[b];
-      if (ba == bb) invalid(path, "a body cannot collide with itself");
-      if (c.bodies[ba].is_static() && c.bodies[bb].is_static()) invalid(path, "static-static pair");
-      for (size_t i = 0; i < c.colliders.size(); ++i)
-        if (c.colliders[i].body == ba)
-          for (size_t j = 0; j < c.colliders.size(); ++j)
-            if (c.colliders[j].body == bb) cand.push_back({int(i), int(j), path});
-    }
-  } else {
-    std::set<std::pair<int, int>> jointed;
-    for (const Joint& j : c.joints) {
-      jointed.insert({j.parent, j.child});
-      jointed.insert({j.child, j.parent});
-    }
-    for (size_t i = 0; i < c.colliders.size(); ++i)
-      for (size_t j = i + 1; j < c.colliders.size(); ++j) {
-        int bi = c.colliders[i].body, bj = c.colliders[j].body;
-        if (bi == bj || jointed.count({bi, bj})) continue;
-        if (c.bodies[bi].is_static() && c.bodies[bj].is_static()) continue;
-        cand.push_back({int(i), int(j), "colliders[" + std::to_string(i) + "]x[" + std::to_string(j) + "]"});
-      }
+  for (size_t ii = 0; ii < inodes.size(); ++ii) {
+    std::string path = idx("collide_include", ii);
+    Fields f(inodes[ii]->children, path, {"first", "second"});
+    std::string a = f.str("first"), b = f.str("second");
+    if (!body_ix.count(a)) invalid(path + ".first", "unknown body '" + a + "'");
+    if (!body_ix.count(b)) invalid(path + ".second", "unknown body '" + b + "'");
+    inc.push_back({body_ix[a], body_ix[b], path});
   }
-  static const char* kind_name[] = {"sphere", "capsule", "box", "plane"};
-  for (const Cand& cd : cand) {
-    int a = cd.i, b = cd.j;
-    int ka = c.colliders[a].kind, kb = c.colliders[b].kind;  // enum order = orientation rank
-    if (ka > kb || (ka == kb && a > b)) { std::swap(a, b); std::swap(ka, kb); }
-    int type = -1;
-    if (kb == kPlane) type = (ka == kSphere) ? BRAX_SLOT_SPHERE_PLANE : (ka == kCapsule) ? BRAX_SLOT_CAPSULE_PLANE
-                                            : (ka == kBox) ? BRAX_SLOT_BOX_PLANE : -1;
-    else if (ka == kSphere && kb == kSphere) type = BRAX_SLOT_SPHERE_SPHERE;
-    else if (ka == kSphere && kb == kCapsule) type = BRAX_SLOT_SPHERE_CAPSULE;
-    else if (ka == kCapsule && kb == kCapsule) type = BRAX_SLOT_CAPSULE_CAPSULE;
-    if (type < 0)
-      invalid(cd.path, std::string("unsupported collider pair ") + kind_name[ka] + "-" + kind_name[kb],
-              BRAX_E_UNSUPPORTED_PAIR);
-    c.pairs.push_back({a, b, type});
-  }
-  for (size_t pi = 0; pi < c.pairs.size(); ++pi) {
-    const Pair& pr = c.pairs[pi];
-    const Collider& A = c.colliders[pr.col_a];
-    int first = 0, count = 1;
-    if (pr.type == BRAX_SLOT_CAPSULE_PLANE) {
-      if (A.end == 0) count = 2;
-      else first = (A.end == 1) ? 0 : 1;
-    } else if (pr.type == BRAX_SLOT_BOX_PLANE) {
-      count = 8;
-    }
-    for (int k = 0; k < count; ++k)
-      c.slots.push_back({int(pi), pr.type, A.body, c.colliders[pr.col_b].body, pr.col_a, pr.col_b, first + k});
-  }
-  if (c.slots.size() > 255) invalid("config", "more than 255 contact slots");
+  finalize_config(c, acts, inodes.empty() ? nullptr : &inc);
   if (const std::vector<Node>* tn = top.msg("task")) {
     const std::string path = "config.task";
     Fields tf(*tn, path, {"torso", "forward", "survive_reward", "ctrl_cost", "healthy_z", "episode_length",
@@ -546,6 +576,167 @@ Config parse_config(const std::string& text) {
     }
     if (t.noise_vel < 0 || t.noise_ang < 0) invalid(path + ".reset_noise", "must be >= 0");
   }
+  return c;
+}
+
+// Programmatic construction ("define systems programmatically"; the
+// App. A listing at): the same Config the text parser yields, from
+// plain C descriptors.  Quaternions (w, x, y, z) instead of Euler degrees, limits in
+// radians; the numeric checks are the text parser's, the structural ones shared.
+Config config_from_desc(const brax_config_desc& d) {
+  auto finite = [](const double* v, int n) {
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(v[i])) return false;
+    return true;
+  };
+  auto unit_quat = [&](const double* q, const std::string& path, double out[4]) {
+    if (!finite(q, 4)) invalid(path, "must be finite");
+    const double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (!(std::fabs(n - 1.0) <= 1e-6)) invalid(path, "must be a unit quaternion (w, x, y, z)");
+    for (int k = 0; k < 4; ++k) out[k] = q[k];
+  };
+  Config c;
+  c.dt = d.dt;
+  if (!(c.dt > 0)) invalid("config.dt", "must be > 0");
+  if (d.substeps < 1) invalid("config.substeps", "must be a positive integer");
+  c.substeps = d.substeps;
+  if (!finite(d.gravity, 3)) invalid("config.gravity", "must be finite");
+  for (int k = 0; k < 3; ++k) c.gravity[k] = d.gravity[k];
+  c.friction = d.friction;
+  c.elasticity = d.elasticity;
+  c.baumgarte = d.baumgarte_erp;
+  if (!(c.friction >= 0)) invalid("config.friction", "must be >= 0");
+  if (!(c.elasticity >= 0 && c.elasticity <= 1)) invalid("config.elasticity", "must be in [0, 1]");
+  if (!(c.baumgarte > 0 && c.baumgarte <= 1)) invalid("config.baumgarte_erp", "must be in (0, 1]");
+  if (d.n_bodies <= 0 || !d.bodies) invalid("config.bodies", "no bodies");
+  if (d.n_joints < 0 || d.n_actuators < 0 || d.n_colliders < 0 || d.n_pairs < 0)
+    invalid("config", "negative count");
+  if ((d.n_joints && !d.joints) || (d.n_actuators && !d.actuators) || (d.n_colliders && !d.colliders))
+    invalid("config", "NULL array with a nonzero count");
+  std::set<std::string> names;
+  for (int bi = 0; bi < d.n_bodies; ++bi) {
+    const brax_body_desc& bd = d.bodies[bi];
+    const std::string path = idx("bodies", size_t(bi));
+    Body b;
+    b.name = bd.name ? bd.name : ("body" + std::to_string(bi));
+    if (bd.name && !names.insert(b.name).second) invalid(path + ".name", "duplicate body name '" + b.name + "'");
+    b.mass = bd.mass;
+    if (!(b.mass > 0)) invalid(path + ".mass", "must be > 0");
+    for (int k = 0; k < 3; ++k) {
+      b.inertia[k] = bd.inertia[k];
+      if (!(b.inertia[k] > 0)) invalid(path + ".inertia", "must be > 0");
+      if ((bd.frozen_pos[k] != 0 && bd.frozen_pos[k] != 1) || (bd.frozen_rot[k] != 0 && bd.frozen_rot[k] != 1))
+        invalid(path + ".frozen", "axis flags must be 0 or 1");
+      b.frozen_pos[k] = bd.frozen_pos[k];
+      b.frozen_rot[k] = bd.frozen_rot[k];
+    }
+    if (!finite(bd.init_pos, 3)) invalid(path + ".init_pos", "must be finite");
+    for (int k = 0; k < 3; ++k) b.init_pos[k] = bd.init_pos[k];
+    unit_quat(bd.init_rot, path + ".init_rot", b.init_rot);
+    c.bodies.push_back(b);
+  }
+  // colliders: global order = body order, then the descriptor order within a body
+  // (the text format's order, so both forms enumerate the same slots)
+  std::vector<int> corder(size_t(d.n_colliders));
+  for (int i = 0; i < d.n_colliders; ++i) corder[size_t(i)] = i;
+  for (int i = 0; i < d.n_colliders; ++i)
+    if (d.colliders[i].body < 0 || d.colliders[i].body >= d.n_bodies)
+      invalid(idx("colliders", size_t(i)) + ".body", "out of range");
+  std::stable_sort(corder.begin(), corder.end(),
+                   [&](int x, int y) { return d.colliders[x].body < d.colliders[y].body; });
+  for (int i : corder) {
+    const brax_collider_desc& cd = d.colliders[i];
+    const std::string path = idx("colliders", size_t(i));
+    Collider col;
+    col.body = cd.body;
+    if (!finite(cd.pos, 3)) invalid(path + ".pos", "must be finite");
+    for (int k = 0; k < 3; ++k) col.pos[k] = cd.pos[k];
+    unit_quat(cd.rot, path + ".rot", col.rot);
+    switch (cd.shape) {
+      case BRAX_SHAPE_SPHERE:
+        col.kind = kSphere;
+        col.radius = cd.radius;
+        if (!(col.radius > 0)) invalid(path + ".radius", "must be > 0");
+        break;
+      case BRAX_SHAPE_CAPSULE:
+        col.kind = kCapsule;
+        col.radius = cd.radius;
+        col.length = cd.length;
+        if (!(col.radius > 0)) invalid(path + ".radius", "must be > 0");
+        if (!(col.length >= 2 * col.radius)) invalid(path + ".length", "must be >= 2*radius");
+        if (cd.capsule_end != 0 && cd.capsule_end != 1 && cd.capsule_end != -1)
+          invalid(path + ".capsule_end", "must be -1, 0 or 1");
+        col.end = cd.capsule_end;
+        break;
+      case BRAX_SHAPE_BOX:
+        col.kind = kBox;
+        for (int k = 0; k < 3; ++k) {
+          col.halfsize[k] = cd.halfsize[k];
+          if (!(col.halfsize[k] > 0)) invalid(path + ".halfsize", "must be > 0");
+        }
+        break;
+      case BRAX_SHAPE_PLANE:
+        col.kind = kPlane;
+        break;
+      default:
+        invalid(path + ".shape", "unknown shape");
+    }
+    c.colliders.push_back(col);
+  }
+  std::set<std::string> jnames;
+  for (int ji = 0; ji < d.n_joints; ++ji) {
+    const brax_joint_desc& jd = d.joints[ji];
+    const std::string path = idx("joints", size_t(ji));
+    Joint j;
+    j.name = jd.name ? jd.name : ("joint" + std::to_string(ji));
+    if (jd.name && !jnames.insert(j.name).second) invalid(path + ".name", "duplicate joint name '" + j.name + "'");
+    if (jd.parent < 0 || jd.parent >= d.n_bodies) invalid(path + ".parent", "out of range");
+    if (jd.child < 0 || jd.child >= d.n_bodies) invalid(path + ".child", "out of range");
+    if (jd.parent == jd.child) invalid(path + ".child", "parent and child must differ");
+    j.parent = jd.parent;
+    j.child = jd.child;
+    j.stiffness = jd.stiffness;
+    if (!(j.stiffness > 0)) invalid(path + ".stiffness", "must be > 0");
+    j.spring_damping = jd.spring_damping;
+    j.angular_damping = jd.angular_damping;
+    j.limit_stiffness = jd.limit_stiffness < 0 ? j.stiffness : jd.limit_stiffness;  // R8 (negative = default)
+    j.angular_stiffness = jd.angular_stiffness < 0 ? j.stiffness : jd.angular_stiffness;
+    if (!(j.spring_damping >= 0)) invalid(path + ".spring_damping", "must be >= 0");
+    if (!(j.angular_damping >= 0)) invalid(path + ".angular_damping", "must be >= 0");
+    if (!finite(jd.parent_offset, 3) || !finite(jd.child_offset, 3)) invalid(path, "offsets must be finite");
+    for (int k = 0; k < 3; ++k) {
+      j.parent_offset[k] = jd.parent_offset[k];
+      j.child_offset[k] = jd.child_offset[k];
+    }
+    unit_quat(jd.rotation, path + ".rotation", j.rotation);
+    unit_quat(jd.reference_rotation, path + ".reference_rotation", j.reference_rotation);
+    if (jd.dof < 0 || jd.dof > 3) invalid(path + ".dof", "must be 0..3");
+    j.dof = jd.dof;
+    for (int k = 0; k < j.dof; ++k) {
+      if (!(jd.limit_lo[k] <= jd.limit_hi[k])) invalid(path + ".limit", "min > max");
+      if (jd.limit_lo[k] < -M_PI - 1e-12 || jd.limit_hi[k] > M_PI + 1e-12)
+        invalid(path + ".limit", "limits must lie in [-pi, pi] (R9)");
+      j.lo[k] = jd.limit_lo[k];
+      j.hi[k] = jd.limit_hi[k];
+    }
+    c.joints.push_back(j);
+  }
+  std::vector<ActuatorSpec> acts;
+  for (int ai = 0; ai < d.n_actuators; ++ai) {
+    const brax_actuator_desc& ad = d.actuators[ai];
+    ActuatorSpec a;
+    a.path = idx("actuators", size_t(ai));
+    a.name = ad.name ? ad.name : ("actuator" + std::to_string(ai));
+    a.joint = ad.joint;
+    if (ad.kind != BRAX_ACTUATOR_TORQUE && ad.kind != BRAX_ACTUATOR_ANGLE) invalid(a.path + ".kind", "unknown kind");
+    a.kind = ad.kind == BRAX_ACTUATOR_TORQUE ? kTorque : kAngle;
+    a.strength = ad.strength;
+    acts.push_back(a);
+  }
+  std::vector<IncludeSpec> inc;
+  if (d.pairs)
+    for (int pi = 0; pi < d.n_pairs; ++pi) inc.push_back({d.pairs[pi].first, d.pairs[pi].second, idx("pairs", size_t(pi))});
+  finalize_config(c, acts, d.pairs ? &inc : nullptr);
   return c;
 }
 

@@ -112,6 +112,8 @@ struct Config {
 
 // Parse + validate; throws brax::Error.
 Config parse_config(const std::string& text);
+// Programmatic form (brax_config_from_desc); throws brax::Error.
+Config config_from_desc(const brax_config_desc& desc);
 
 // Euler angles in degrees, intrinsic X-Y-Z: qx(a) ⊗ qy(b) ⊗ qz(c).
 void euler_deg_to_quat(const double deg[3], double q[4]);

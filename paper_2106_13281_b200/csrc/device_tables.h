@@ -105,6 +105,7 @@ BRAX_HD inline int32_t inc_pack(int index, bool second_side) { return (index << 
 // Shared-memory layout of the step kernel (words; every region 16-byte aligned).
 //   [2 mbarriers][tables][QP records B·L·rec_q][U][sA A·E][action staging E·A][counts C·E][status E]
 //   [env epilogue, systems with a task: x0 3E | steps E | episode E | reset flag E | contact Δv 6·B·E]
+//   (the contact Δv region also serves brax_step_extras.contact_dp of the physics-only kernel)
 // with L = E/V lanes (records) per body or item.  U holds the joint and slot
 // records during the substeps, the contiguous TMA staging chunks (pos|rot|vel|ang,
 // E·B·13 words) while loading / storing, and the observation rows (E·obs_dim) in
@@ -117,7 +118,8 @@ BRAX_HD inline int32_t round4(int32_t w) { return (w + 3) & ~3; }
 // value + tangent of the JVP step); RW: words per row of a per-env array (actions,
 // contact counts, contact Δv): LG·(paired ? 2 : 1).
 BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A, int32_t E, int32_t LG,
-                                      int32_t paired, int32_t blob_words, int32_t obs_dim, int32_t contact_obs) {
+                                      int32_t paired, int32_t blob_words, int32_t obs_dim, int32_t contact_obs,
+                                      int32_t contact_dp = 0) {
   SmemLayout L;
   const int32_t V = paired ? 2 : 1, RW = LG * V;
   L.blob = 4;
@@ -136,7 +138,7 @@ BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A
   L.ep = L.steps + env * round4(E);
   L.rst = L.ep + env * round4(E);
   L.co = L.rst + env * round4(E);
-  L.total_words = L.co + env * (contact_obs ? round4(6 * B * RW) : 0);
+  L.total_words = L.co + ((env && contact_obs) || contact_dp ? round4(6 * B * RW) : 0);
   return L;
 }
 
@@ -183,6 +185,7 @@ struct StepArgs {
   // NEXT-4 JVP (lane type D1): tangents of the inputs (NULL = zero) and of the outputs
   const float *dpos_in, *drot_in, *dvel_in, *dang_in, *dactions;
   float *dpos_out, *drot_out, *dvel_out, *dang_out;
+  float* contact_dp;           // [n][B][6] Σ_substeps collision-integrator (Δv, Δω), or NULL (physics kernel only)
 };
 constexpr uint32_t kActTag = 0x41435431u;  // "ACT1": separates the action stream from the reset stream
 
@@ -195,7 +198,7 @@ struct DPlan {
   int32_t G, V, E, W;  // lane groups per warp, envs per lane, envs per block E = 32·V/G, warps
   int32_t off_item_begin, off_items;          // per warp: item steps [begin, end); items[step*G + g]
   int32_t off_body_begin, off_bodies_of_warp;  // per warp: body steps; bodies[step*G + g]
-  int32_t smem_bytes, smem_bytes_jvp, smem_bytes_env, pad2;  // physics | JVP (V = 1 plans) | env epilogue
+  int32_t smem_bytes, smem_bytes_jvp, smem_bytes_env, smem_bytes_cdp;  // physics | JVP (V = 1) | env | + contact_dp
 };
 
 struct DHeader {            // passed by value as a kernel argument

@@ -68,7 +68,9 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   const DTask& T = H.task;
   const int LG = 32 / G;  // lanes per group = records per item
   const int RW = LG * SL;
-  const SmemLayout L = smem_layout(B, J, C, A, E, LG, SL == 2, H.blob_words, kEnv ? T.obs_dim : 0, T.contact_obs);
+  const bool cdp = !kEnv && a.contact_dp != nullptr;  // brax_step_extras.contact_dp (physics kernel)
+  const SmemLayout L =
+      smem_layout(B, J, C, A, E, LG, SL == 2, H.blob_words, kEnv ? T.obs_dim : 0, kEnv ? T.contact_obs : 0, cdp);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [0] tables + QP, [1] actions
   uint32_t* sBlob = smem + L.blob;
   float* sQ = reinterpret_cast<float*>(smem + L.q);
@@ -164,6 +166,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     if (save_co)
       for (int i = tid; i < 6 * B * RW; i += blockDim.x) sCo[i] = 0.f;
   }
+  if (cdp)  // static bodies keep 0; dynamic bodies store at substep 0 of every step
+    for (int i = tid; i < 6 * B * RW; i += blockDim.x) sCo[i] = 0.f;
   __syncthreads();
   lap(0);
 
@@ -359,17 +363,18 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
           dtg = clock64();
         }
 #endif
-        float* co = save_co && last ? sCo + b * 6 * RW + el * SL : nullptr;
+        float* co = (save_co && last) || cdp ? sCo + b * 6 * RW + el * SL : nullptr;
+        const bool co_acc = cdp && s > 0;
         const Row<S> rb{sQ + (b * LG + el) * QS};
         if constexpr (kFixed) {  // specialised variant: isotropic bodies without frozen axes at compile time
           const int fl = bodies[b].flags;
           constexpr int kFreeFlags = kFlagIso | kFlagFreePos | kFlagFreeRot;
           if ((fl & kFreeFlags) == kFreeFlags && !bodies[b].rot_frozen)
-            integrate<S, true>(bodies[b], rb, acc, H.h, H.g, kin, co, RW);
+            integrate<S, true>(bodies[b], rb, acc, H.h, H.g, kin, co, RW, co_acc);
           else
-            integrate<S>(bodies[b], rb, acc, H.h, H.g, kin, co, RW);
+            integrate<S>(bodies[b], rb, acc, H.h, H.g, kin, co, RW, co_acc);
         } else {
-          integrate<S>(bodies[b], rb, acc, H.h, H.g, kin, co, RW);
+          integrate<S>(bodies[b], rb, acc, H.h, H.g, kin, co, RW, co_acc);
         }
       }
 #ifdef BRAX_DIAG
@@ -438,8 +443,13 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   }
   lap(2);
   __syncthreads();
-  // S9: status bits, contact counts, and the single write-back of the QP (TMA bulk for full blocks)
+  // S9: status bits, contact counts, contact Δv sums, and the single write-back of the QP (TMA bulk for full blocks)
   block_extras<V>(a, sQ, sCnt, sStat, B, C, E, LG, e0, nvalid);
+  if (cdp)
+    for (int i = tid; i < nvalid * B * 6; i += blockDim.x) {
+      const int env = i / (B * 6), r = i - env * (B * 6);
+      a.contact_dp[(e0 + env) * B * 6 + r] = sCo[r * RW + eslot<V>(env, LG)];
+    }
   if (bulk) {
     records_to_stg<V>(sQ, stg, B, E);
     fence_proxy_async();
@@ -552,7 +562,7 @@ cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs
   if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
   const DPlan& P = sys.hd.plan[plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
-  const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);
+  const size_t smem = size_t(a.env ? P.smem_bytes_env : a.contact_dp ? P.smem_bytes_cdp : P.smem_bytes);
   if (a.env) {  // env-epilogue instantiations (fewer register variants)
     if (P.V == 2) {
       if (fixed) {
@@ -613,6 +623,7 @@ LaunchConfig heuristic_config(const System& sys, int64_t n) {
 // not written.
 LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   LaunchConfig best = heuristic_config(sys, a.n_envs);
+  if (!sys.autotune || std::getenv("BRAX_PLAN") || std::getenv("BRAX_MAXREG")) return best;
   const int64_t n = a.n_envs, B = sys.hd.B;
   const size_t fbytes[4] = {size_t(n * B * 3 * 4), size_t(n * B * 4 * 4), size_t(n * B * 3 * 4),
                             size_t(n * B * 3 * 4)};
@@ -635,6 +646,7 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   t.n_steps = 1;
   t.status = nullptr;
   t.contact_active = nullptr;
+  t.contact_dp = nullptr;
   t.env = 0;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -707,27 +719,31 @@ LaunchConfig launch_config(const System& sys, int64_t n_envs) {
   return heuristic_config(sys, n_envs);
 }
 
+// Explicit tuning (brax_system_tune): measures every plan on the caller's state and
+// remembers the fastest for a.n_envs.  Allocates stream-ordered scratch and
+// synchronises the stream; brax_step itself never does either.
+cudaError_t tune_system(const System& sys, const StepArgs& a, cudaStream_t stream) {
+  if (a.n_envs <= 0) return cudaSuccess;
+  LaunchConfig c = tune(sys, a, stream);
+  cudaError_t e = cudaGetLastError();
+  std::lock_guard<std::mutex> g(sys.tune_mu);
+  sys.tuned[a.n_envs] = c;
+  return e;
+}
+
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream) {
   if (a.n_envs <= 0 || (a.n_steps <= 0 && !a.env)) return cudaSuccess;
   LaunchConfig c = launch_config(sys, a.n_envs);
-  if (a.env && sys.hd.plan[c.plan].smem_bytes_env > kMaxDynSmem) {  // epilogue regions: smaller blocks
+  // the env epilogue / contact_dp regions may not fit the tuned plan: the largest block that does
+  auto bytes = [&](int p) { return a.env ? sys.hd.plan[p].smem_bytes_env
+                                         : a.contact_dp ? sys.hd.plan[p].smem_bytes_cdp : sys.hd.plan[p].smem_bytes; };
+  if (bytes(c.plan) > kMaxDynSmem) {
     int q = -1;
     for (int p = kNumPlans - 1; p >= 0; --p)
-      if (sys.hd.plan[p].smem_bytes_env <= kMaxDynSmem && (q < 0 || sys.hd.plan[p].E > sys.hd.plan[q].E)) q = p;
+      if (bytes(p) <= kMaxDynSmem && (q < 0 || sys.hd.plan[p].E > sys.hd.plan[q].E)) q = p;
     if (q < 0) return cudaErrorInvalidValue;
     c.plan = q;
     c.regs = variant_regs(sys.hd.plan[q].V, choose_regs(sys, sys.hd.plan[q], grid_of(sys, q, a.n_envs)));
-  }
-  // first launch of this batch size outside graph capture: measure every plan once
-  if (!c.tuned && sys.autotune && a.n_envs >= 256 && a.n_steps > 0 && !std::getenv("BRAX_PLAN") &&
-      !std::getenv("BRAX_MAXREG")) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
-      c = tune(sys, a, stream);
-      std::lock_guard<std::mutex> g(sys.tune_mu);
-      sys.tuned[a.n_envs] = c;
-    }
-    cudaGetLastError();
   }
   return launch_with(sys, a, c.plan, c.regs, c.fixed, stream);
 }

@@ -934,7 +934,7 @@ template <class S> struct Acc {
 // kernel variant's common body class), else the flags are read.
 template <class S, bool kFree = false>
 __device__ __forceinline__ void integrate(const DBody& bd, Row<S> r, const Acc<S>& acc, float h, const float* g,
-                                          bool kin, float* co, int E) {
+                                          bool kin, float* co, int E, bool co_acc = false) {
   const bool iso = kFree || (bd.flags & kFlagIso), fp = kFree || (bd.flags & kFlagFreePos),
              fr = kFree || (bd.flags & kFlagFreeRot);
   Q4T<S> q = r.rot();
@@ -954,14 +954,11 @@ __device__ __forceinline__ void integrate(const DBody& bd, Row<S> r, const Acc<S
   }
   r.set_vel(v);
   r.set_ang(w);
-  if (co) {  // collision integrator's velocity change: after − before (R32)
+  if (co) {  // collision integrator's velocity change: after − before (R32); co_acc: summed over substeps
     const V3T<S> dv = v - v_pre, dw = w - w_pre;
-    Lanes<S>::st(co, dv.x);
-    Lanes<S>::st(co + E, dv.y);
-    Lanes<S>::st(co + 2 * E, dv.z);
-    Lanes<S>::st(co + 3 * E, dw.x);
-    Lanes<S>::st(co + 4 * E, dw.y);
-    Lanes<S>::st(co + 5 * E, dw.z);
+    const S d[6] = {dv.x, dv.y, dv.z, dw.x, dw.y, dw.z};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) Lanes<S>::st(co + k * E, co_acc ? Lanes<S>::ld(co + k * E) + d[k] : d[k]);
   }
   if (kin) {  // next substep's kinematic integrator (v, ω already masked)
     r.set_pos(axpy(h, v, r.pos()));

@@ -425,6 +425,7 @@ System* build_host(const Config& cfg) {
     P.smem_bytes = smem_layout(B, J, C, hd.A, P.E, LG, P.V == 2, hd.blob_words, 0, 0).total_words * 4;
     P.smem_bytes_env = smem_layout(B, J, C, hd.A, P.E, LG, P.V == 2, hd.blob_words, hd.task.obs_dim,
                                    hd.task.contact_obs).total_words * 4;
+    P.smem_bytes_cdp = smem_layout(B, J, C, hd.A, P.E, LG, P.V == 2, hd.blob_words, 0, 0, 1).total_words * 4;
     P.smem_bytes_jvp = P.V == 1 ? smem_layout(B, J, C, hd.A, P.E, LG, 1, hd.blob_words, 0, 0).total_words * 4 : 0;
   }
   // smallest block (G = 4: 8 envs) must fit; larger blocks are used where they fit

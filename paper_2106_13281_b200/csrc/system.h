@@ -36,7 +36,7 @@ struct System {
   bool trace = false;                  // per-phase cycle tracing (brax_system_set_tracing)
   unsigned long long* d_phase_cycles = nullptr;  // device [4]
   size_t smem_bytes = 0;
-  // launch configuration per batch size, measured on the first uncaptured launch
+  // launch configuration per batch size, measured by brax_system_tune
   // (every plan gives the same bits, so the choice only affects speed)
   bool autotune = true;
   mutable std::mutex tune_mu;
@@ -60,6 +60,8 @@ LaunchConfig launch_config(const System& sys, int64_t n_envs);
 
 // Kernel launchers (step.cu, reset.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream);
+// brax_system_tune: time every launch plan on a's input (scratch outputs), remember the fastest.
+cudaError_t tune_system(const System& sys, const StepArgs& a, cudaStream_t stream);
 // Forward-mode derivative (JVP) of the step: StepArgs' d*_in tangents -> d*_out (NEXT-4).
 cudaError_t launch_step_jvp(const System& sys, const StepArgs& a, cudaStream_t stream);
 // Reverse-mode cotangent of one step in one launch (vjp.cu): g_in = Jᵀ·g_out.

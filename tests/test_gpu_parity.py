@@ -293,10 +293,11 @@ def test_every_launch_plan_matches_oracle(name):
         os.environ.pop("BRAX_FIXED_GATHER", None)
 
 
-def test_autotune_picks_a_plan_without_touching_inputs():
-    """The first launch of a batch size times every plan on a scratch copy (the
-    caller's input is not written), remembers the fastest, and the result equals
-    the heuristic plan's bit for bit."""
+def test_tune_picks_a_plan_without_touching_inputs():
+    """brax_system_tune times every plan on scratch outputs (the caller's input is not
+    written), remembers the fastest, and the tuned launch equals the heuristic plan's
+    bit for bit.  brax_step alone never tunes (header: it allocates nothing and never
+    synchronises)."""
     o, s0 = scene("ant")
     s = bx.System(oracle.load_scene("ant"))
     n = 1000
@@ -305,19 +306,94 @@ def test_autotune_picks_a_plan_without_touching_inputs():
     assert s.launch_config(n)["tuned"] == 0
     qd = dev(qp)
     before = host(qd)
+    ad = torch.from_numpy(act).cuda()
     out = s.alloc_qp(n)
-    s.step(qd, torch.from_numpy(act).cuda(), out)
+    s.step(qd, ad, out)                        # untuned: heuristic plan, no tuning side effect
     torch.cuda.synchronize()
+    assert s.launch_config(n)["tuned"] == 0
+    heur = host(out)
+    s.tune(qd, ad)
     for k in FIELDS:
         assert np.array_equal(host(qd)[k], before[k])
     cfg = s.launch_config(n)
     assert cfg["tuned"] == 1 and cfg["E"] == 32 * cfg["V"] // cfg["G"], cfg
-    s0.set_autotune(False)
-    ref, _, _ = gpu_step(s0, qp, act)
-    s0.set_autotune(True)
+    s.step(qd, ad, out)
+    torch.cuda.synchronize()
     got = host(out)
     for k in FIELDS:
-        assert np.array_equal(got[k], ref[k]), k
+        assert np.array_equal(got[k], heur[k]), k
+    # a tuned plan whose shared memory cannot hold the env epilogue falls back (no failure)
+    s.tune(qd, ad)
+    del s0
+
+
+@pytest.mark.parametrize("name", ["ball", "ant", "humanoid", "grasp", "coverage"])
+def test_contact_dp_matches_oracle(name):
+    """brax_step_extras.contact_dp = Σ over the step's substeps of the collision
+    integrator's (Δv, Δω) per body (Table 1's contact observations,
+    PAPER.md:115) vs the oracle's; asking for it leaves the QP bits unchanged."""
+    o, s = scene(name)
+    n = 1 if name == "ball" else 333
+    if name == "ball":
+        dstar = 9.8 * 0.01 ** 2 / 0.2
+        qp = synth.to_f32({"pos": np.array([[[0, 0, 0], [0, 0, 0.5 - 1.5 * dstar]]]),
+                           "rot": np.array([[[1.0, 0, 0, 0]] * 2]), "vel": np.array([[[0, 0, 0], [2.0, 0, -0.3]]]),
+                           "ang": np.zeros((1, 2, 3))})
+    else:
+        qp = trajectory_states(o, n, seed=81, T0=3)
+    act = synth.actions(82, 1, n, o.act_dim)[0]
+    ref, ex = o.step(qp, act, threads=8, contact_dp=True)
+    keep = ~ex["ambiguous"]
+    qd = dev(qp)
+    out, plain = s.alloc_qp(n), s.alloc_qp(n)
+    cdp = torch.full((n, s.n_bodies, 6), float("nan"), device="cuda")
+    ad = torch.from_numpy(act).cuda() if o.act_dim else None
+    s.step(qd, ad, out, contact_dp=cdp)
+    s.step(qd, ad, plain)
+    torch.cuda.synchronize()
+    for k in FIELDS:
+        assert torch.equal(out[k], plain[k]), k
+    got = cdp.cpu().numpy().astype(np.float64)
+    err = np.max(np.abs(got[keep] - ex["contact_dp"][keep]) / np.maximum(1.0, np.abs(ex["contact_dp"][keep])))
+    assert err <= TOL_STEP, err
+    assert np.any(ex["contact_dp"] != 0)
+
+
+def test_contact_dp_of_a_rollout_is_its_last_step():
+    o, s = scene("ant")
+    n, T = 257, 3
+    qp = trajectory_states(o, n, seed=83, T0=2)
+    acts = torch.from_numpy(synth.actions(84, T, n, o.act_dim)).cuda()
+    a = dev(qp)
+    cdp_r = torch.empty((n, s.n_bodies, 6), device="cuda")
+    s.rollout(a, acts, contact_dp=cdp_r)
+    b = dev(qp)
+    cdp_s = torch.empty((n, s.n_bodies, 6), device="cuda")
+    for t in range(T):
+        s.step(b, acts[t], b, contact_dp=cdp_s)
+    torch.cuda.synchronize()
+    assert torch.equal(cdp_r, cdp_s)
+    for k in FIELDS:
+        assert torch.equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("name", ["ant", "grasp", "coverage"])
+def test_programmatic_system_steps_like_the_text_system(name):
+    """A system built with brax_config_from_desc steps bit-identically to
+    the one parsed from the same scene's text."""
+    from test_config_desc import desc_from_system
+    o, s = scene(name)
+    text = oracle.load_scene(name)
+    d, keep = desc_from_system(o.sys, text)
+    sd = bx.System(desc=d)
+    n = 200
+    qp = trajectory_states(o, n, seed=85, T0=2)
+    act = synth.actions(86, 1, n, o.act_dim)[0]
+    a, _, _ = gpu_step(s, qp, act)
+    b, _, _ = gpu_step(sd, qp, act)
+    for k in FIELDS:
+        assert np.array_equal(a[k], b[k]), k
+    del keep
 
 
 def test_rollout_random_actions_match_the_oracle_generator():

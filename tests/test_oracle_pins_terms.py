@@ -331,3 +331,36 @@ joints { name: "J" parent: "P" child: "C" stiffness: 1000 limit_stiffness: 300 a
         r = q["rot"][0, 1]
         assert abs(2 * math.atan2(r[1], r[0]) - th) < 1e-12
         assert abs(q["ang"][0, 1, 0] - w) < 1e-12
+
+
+# ---------------------------------------------------------------- contact Δv sums (brax_step_extras.contact_dp)
+def test_contact_dp_resting_ball_is_g_dt():
+    """A ball resting at its equilibrium depth d* = g h²/β with S substeps: in every substep
+    the collision integrator adds exactly the velocity gravity removed, g·h upwards (the
+    Baumgarte impulse βd*/h = g·h, u_n = 0), so Σ over the step's substeps of the collision
+    integrator's Δv is (0, 0, S·g·h) = (0, 0, g·dt) and Δω = 0; the last substep's alone is g·h."""
+    g, dt, S, beta, r = 9.8, 0.02, 4, 0.2, 0.5
+    h = dt / S
+    txt = f"""dt: {dt} substeps: {S} gravity {{ z: -{g} }} baumgarte_erp: {beta}
+bodies {{ name: "G" frozen {{ all: true }} colliders {{ plane {{}} }} }}
+bodies {{ name: "Ball" mass: 1 inertia {{ x: 0.1 y: 0.1 z: 0.1 }} colliders {{ sphere {{ radius: {r} }} }} }}"""
+    o = oracle.Oracle(txt)
+    q = qp1(o, pos=[[0, 0, 0], [0, 0, r - g * h * h / beta]])
+    q, ex = o.step(q, contact_dv=True, contact_dp=True)
+    assert np.allclose(ex["contact_dp"][0, 1], [0, 0, g * dt, 0, 0, 0], atol=1e-12)
+    assert np.allclose(ex["contact_dv"][0, 1], [0, 0, g * h, 0, 0, 0], atol=1e-12)
+    assert np.all(ex["contact_dp"][0, 0] == 0)       # static ground
+    assert ex["contact_active"][0, 0] == S
+
+
+def test_op_count_lean_convention_ball():
+    """The lean convention (scene-neutral operations uncounted) for the free-flying ball:
+    kinematic without the two unit-mask products (76 − 6), sphere–plane narrowphase without
+    the zero collider offsets (2 × 33) and identity collider rotations (2 × 28) = 45, the
+    potential integrator without its masks and with I_w⁻¹ of the isotropic ball as three
+    products (16 + 9) = 140 flops; MUFU: kinematic 5 + 1/m = 6."""
+    o = oracle.Oracle(oracle.load_scene("ball"))
+    fl, mu = o.count_ops(o.batch_default_qp(1), lean=True)
+    assert (KIN - 6) + (SPHERE_PLANE - 2 * 33 - 2 * 28) + (POT - 6 - 72 + 3) == 140
+    assert (fl, mu) == (140, 6)
+    assert o.count_ops(o.batch_default_qp(1)) == (343, 9)     # the default convention is unchanged

@@ -27,13 +27,16 @@ def count(name, n=64, burn=30, measure=20, seed=0):
     o = oracle.Oracle(oracle.load_scene(name))
     qp = o.reset(n, seed, 0.1, 0.1)
     acts = synth.actions(seed + 1, burn + measure, n, o.act_dim)
-    fl = mu = 0
+    fl = mu = fl_lean = mu_lean = 0
     active = 0.0
     for t in range(burn + measure):
         if t >= burn:
             f, m = o.count_ops(qp, acts[t])
             fl += f
             mu += m
+            f, m = o.count_ops(qp, acts[t], lean=True)
+            fl_lean += f
+            mu_lean += m
         qp, ex = o.step(qp, acts[t], threads=8)
         if t >= burn and o.n_slots:
             active += ex["contact_active"].sum() / (o.sys.substeps * n)
@@ -42,6 +45,8 @@ def count(name, n=64, burn=30, measure=20, seed=0):
     return {
         "flops_per_env_step": fl / steps,
         "mufu_per_env_step": mu / steps,
+        "flops_per_env_step_lean": fl_lean / steps,
+        "mufu_per_env_step_lean": mu_lean / steps,
         "bytes_per_env_step": 4 * (26 * B + A),
         "active_contacts_per_substep": active / measure,
         "n_bodies": B, "act_dim": A, "n_slots": o.n_slots, "substeps": o.sys.substeps,
@@ -51,7 +56,10 @@ def count(name, n=64, burn=30, measure=20, seed=0):
 
 if __name__ == "__main__":
     out = {"convention": "add/sub/mul 1 flop, div/sqrt 4 flops + 1 MUFU, atan2/asin 20 flops + 1 MUFU "
-                         "(SURVEY.md §8(d)); bytes = full QP read + write + action read = 4*(26*B + A)",
+                         "(SURVEY.md §8(d)); bytes = full QP read + write + action read = 4*(26*B + A); "
+                         "*_lean: the same with the operations an exactly neutral scene value makes (unit "
+                         "masks, isotropic inertia, zero damping, zero collider offset, identity collider "
+                         "rotation) not counted",
            "scenes": {}}
     for s in SCENES:
         out["scenes"][s] = count(s)

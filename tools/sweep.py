@@ -7,6 +7,7 @@ batch (L2-resident for small N: a kernel-characterisation sweep, not the bench).
 import argparse
 import json
 import os
+import re
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -48,6 +49,8 @@ for scene in a.scenes.split(","):
             s.reset(qp, 0, 0.1, 0.1)
             T = a.steps
             acts = torch.from_numpy(synth.actions(1, T, n, s.act_dim)).cuda() if s.act_dim else None
+            if G == "0":
+                s.tune(qp, acts[0] if acts is not None else None)
             def run():  # noqa: E306
                 if a.rollout:
                     for t0 in range(0, T, a.rollout):
@@ -70,7 +73,11 @@ for scene in a.scenes.split(","):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
             rate = n * T / (ms / 1e3)
-            tf = rate * counts[scene]["flops_per_env_step"] / 1e12
+            # the count is per env-step at the scene's own substeps; per-substep work is the same,
+            # so an overridden substep count scales it
+            S0 = int(re.search(r"^substeps: *(\d+)", open(os.path.join(ROOT, "scenes", f"{scene}.bxc")).read(),
+                               flags=re.M).group(1))
+            tf = rate * counts[scene]["flops_per_env_step"] * s.substeps / S0 / 1e12
             print(json.dumps({"scene": scene, "substeps": s.substeps, "envs": n, "G": G, "cfg": s.launch_config(n), "rollout": a.rollout,
                               "us_per_step": 1e3 * ms / T, "env_steps_per_s": rate, "tflops": tf,
                               "frac_fp32_1965": tf / 74.45}), flush=True)
