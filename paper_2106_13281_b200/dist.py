@@ -1,12 +1,19 @@
-"""Multi-GPU plumbing: env sharding and the statistics all-reduce.
+"""Multi-GPU plumbing: rank launch, env sharding and the statistics all-reduce
+(SURVEY §8(e)).
 
 The step has no exchange at all: rank g of G owns its own batch of envs (weak
 scaling, envs_per_rank fixed), and the only collective is one all-reduce of a
 few scalars after a rollout — the analogue of the paper's normalisation
-statistics "synced between all cores".  Backend-agnostic
-(NCCL on GPUs, gloo in the CPU tests).
+statistics "synced between all cores".  Backend-agnostic:
+NCCL on GPUs, gloo in the CPU tests, which run these same functions.
 """
 from __future__ import annotations
+
+import os
+import socket
+import subprocess
+import sys
+from dataclasses import dataclass
 
 
 def env_shard(rank: int, world: int, envs_per_rank: int):
@@ -24,6 +31,70 @@ def strong_shard(rank: int, world: int, n_total: int):
     return start, start + base + (1 if rank < extra else 0)
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_or_check(gpus: int, script: str, argv: list[str]) -> int | None:
+    """One process per GPU.  Under a launcher (WORLD_SIZE set) check that it started
+    exactly `gpus` ranks and return None (the caller continues as that rank).  Without
+    one and gpus > 1, start `gpus` ranks of `script argv` with torch.distributed.run on
+    127.0.0.1 and return their exit code (the caller exits with it)."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus:
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
+        return None
+    if gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", script, *argv]
+    return subprocess.call(cmd)
+
+
+@dataclass
+class Ranks:
+    rank: int
+    world: int
+    local: int
+    backend: str | None      # None for a single process without a process group
+    nranks: int              # the communicator's size as the process group reports it
+
+
+def init_ranks(backend: str) -> Ranks:
+    """Read RANK / WORLD_SIZE / LOCAL_RANK (torchrun), bind the local GPU for "nccl", and
+    create the process group for world > 1.  Logs the communicator size to stderr."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+    if world == 1:
+        return Ranks(rank, 1, local, None, 1)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    n = dist.get_world_size()
+    if n != world:
+        raise SystemExit(f"process group has {n} ranks, WORLD_SIZE={world}")
+    print(f"[rank {rank}/{world}] {backend} communicator: nranks={n}", file=sys.stderr, flush=True)
+    return Ranks(rank, world, local, backend, n)
+
+
+def barrier(r: Ranks) -> None:
+    if r.world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
 def allreduce_stats(env_steps: float, blowups: float, elapsed_ms: float, return_sum: float = 0.0, device=None):
     """SUM of [env_steps, blowups, return_sum] and MAX of [elapsed_ms] over ranks (≤ 32 B each way).
 
@@ -36,3 +107,14 @@ def allreduce_stats(env_steps: float, blowups: float, elapsed_ms: float, return_
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
     return float(s[0]), float(s[1]), float(s[2]), float(m[0])
+
+
+def allreduce_max(x: float, device=None) -> float:
+    """MAX over ranks of one timing (ms); identity for a single process."""
+    return allreduce_stats(0.0, 0.0, x, device=device)[3]
+
+
+def finalize(r: Ranks) -> None:
+    if r.world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()

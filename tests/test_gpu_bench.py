@@ -33,7 +33,13 @@ def test_bench_json_line():
     e2e = d["e2e"]
     assert 0 < e2e["value"] < d["value"] and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 40
-    assert d["clocks"]["samples"] >= 1 and d["clocks"]["sm_max_mhz"] > 0
+    assert "exactly 40 brax_step launches" in d["config"]["launch"]
+    assert d["clocks"]["samples"] >= 10 and d["clocks"]["sm_max_mhz"] > 0
+    assert 0.0 < roof["frac_lean"] < roof["frac"]
+    assert d["config"]["comm"]["nranks"] == 1
+    for sc in ("humanoid", "halfcheetah", "grasp", "fetch"):
+        line = d["scenes"][sc]
+        assert line["value"] > 0 and 0.0 < line["frac"] < 1.0 and line["blowups"] == 0, (sc, line)
     assert d["blowups"] == 0
     if d.get("vjp"):
         assert d["vjp"]["value"] > 0 and d["vjp"]["over_step"] > 1.0

@@ -76,3 +76,35 @@ def test_gloo_world2_sharded_equals_unsharded(tmp_path):
         assert float(d["blowups"]) == 0
         for k in ("pos", "rot", "vel", "ang"):
             assert np.array_equal(d[k], qp[k][int(d["lo"]):int(d["hi"])])
+
+
+def _bench(args, env=None):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True, text=True,
+                          cwd=root, env=e, timeout=300)
+
+
+def test_bench_gpus2_starts_two_ranks_and_reduces_stats():
+    """`python bench.py --gpus 2` (no launcher) starts 2 ranks itself (torch.distributed.run on
+    127.0.0.1); they agree on WORLD_SIZE, build a 2-rank communicator and all-reduce the run
+    statistics through the functions the B200 arm calls (dist.init_ranks, dist.barrier,
+    dist.allreduce_stats) — here on gloo with synthetic per-rank numbers (--dist-selftest):
+    SUM of env-steps 100 + 200, SUM of blow-ups 0 + 1, MAX of the times (10, 11 ms)."""
+    import json
+    r = _bench(["--gpus", "2", "--dist-selftest"])
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["nranks"] == 2 and d["backend"] == "gloo"
+    assert d["env_steps"] == 300.0 and d["blowups"] == 1.0 and d["ms_max"] == 11.0
+    assert r.stderr.count("gloo communicator: nranks=2") == 2
+
+
+def test_bench_rejects_a_world_size_mismatch():
+    r = _bench(["--gpus", "2", "--dist-selftest"], env={"WORLD_SIZE": "3", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE=3" in (r.stderr + r.stdout)
