@@ -247,24 +247,26 @@ class Workload:
             for i in range(K):
                 self.launch(i)
         self.stream.synchronize()
-        self.graph.replay()  # untimed: upload + first execution
+        with torch.cuda.stream(self.stream):  # CUDAGraph.replay launches on the current stream
+            self.graph.replay()  # untimed: upload + first execution
         self.stream.synchronize()
 
     def timed_replay(self, ranks, bd, soak_s=0.0, sampler=None):
         """Soak (untimed replays, clocks sampled), then ONE timed replay: barrier + sync on
         both sides, CUDA events on the launch stream; returns this rank's ms."""
         torch = self.torch
-        if soak_s > 0:
-            t0 = time.perf_counter()
-            while time.perf_counter() - t0 < soak_s:
-                self.graph.replay()
-                self.stream.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        bd.barrier(ranks)
-        torch.cuda.synchronize()
-        ev0.record(self.stream)
-        self.graph.replay()
-        ev1.record(self.stream)
+        with torch.cuda.stream(self.stream):  # CUDAGraph.replay launches on the current stream
+            if soak_s > 0:
+                t0 = time.perf_counter()
+                while time.perf_counter() - t0 < soak_s:
+                    self.graph.replay()
+                    self.stream.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            bd.barrier(ranks)
+            torch.cuda.synchronize()
+            ev0.record(self.stream)
+            self.graph.replay()
+            ev1.record(self.stream)
         ev1.synchronize()
         torch.cuda.synchronize()
         bd.barrier(ranks)
@@ -458,12 +460,13 @@ def run_b200(args):
         with torch.cuda.graph(egraph, stream=stream):
             for i in range(Kv):
                 env_launch(i)
-        egraph.replay()
-        stream.synchronize()
-        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        x0.record(stream)
-        egraph.replay()
-        x1.record(stream)
+        with torch.cuda.stream(stream):
+            egraph.replay()
+            stream.synchronize()
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            x0.record(stream)
+            egraph.replay()
+            x1.record(stream)
         x1.synchronize()
         env_ms = bd.allreduce_max(x0.elapsed_time(x1), device=dev)
         env_line = {"value": n * world * Kv / (env_ms / 1e3), "unit": "env-steps/s", "ms_per_step": env_ms / Kv,
