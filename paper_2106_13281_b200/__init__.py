@@ -31,6 +31,9 @@ __all__ = [
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbrax_b200.so")
+# experiments only (A/B timing of two builds in one process tree): BRAX_LIB_PATH points at
+# another in-tree build of the same library
+LIB_PATH = os.environ.get("BRAX_LIB_PATH", LIB_PATH)
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2106_13281_b200.build` "
                       "(or __graft_entry__.build()); there is no CPU fallback")

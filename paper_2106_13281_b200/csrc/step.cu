@@ -96,7 +96,9 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   // tracing (brax_system_phase_cycles): thread 0 times prologue / joints+contacts /
   // integrate / epilogue with clock64 (uniform branch; off unless requested)
   // (the sums live in shared memory, not in registers held across the whole kernel)
-  const bool trace = a.phase_cycles != nullptr && tid == 0;
+  // the specialised (kFixed) variants carry no tracing code: a traced launch uses the generic one
+  constexpr bool kTraceable = !kFixed;
+  const bool trace = kTraceable && a.phase_cycles != nullptr && tid == 0;
   __shared__ long long sTr[5];  // per-phase sums, last mark
 #ifdef BRAX_DIAG
   __shared__ float sDiag[kMaxWarps];  // diagnostics (a.diag_block) only
@@ -106,7 +108,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     sTr[4] = clock64();
   }
   auto lap = [&](int k) {  // re-tests the (uniform) argument instead of holding `trace` in a register
-    if (a.phase_cycles != nullptr && threadIdx.x == 0) {
+    if (kTraceable && a.phase_cycles != nullptr && threadIdx.x == 0) {
       const long long t = clock64();
       sTr[k] += t - sTr[4];
       sTr[4] = t;
@@ -559,6 +561,7 @@ cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs
   ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * sys.hd.A) % 4 == 0);
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
   ka.a.phase_cycles = sys.trace ? sys.d_phase_cycles : nullptr;
+  if (sys.trace) fixed = false;  // tracing is compiled into the generic variants only
   if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
   const DPlan& P = sys.hd.plan[plan];
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
