@@ -402,7 +402,7 @@ class System:
         out = (C.c_int32 * 6)()
         _check(lib.brax_system_launch_config(self._sys, int(n_envs), out))
         d = dict(zip(("G", "V", "E", "warps", "regs"), (int(x) for x in out[:5])))
-        d["tuned"], d["fixed_gather"] = int(out[5]) & 1, (int(out[5]) >> 1) & 1
+        d["tuned"], d["fixed_gather"], d["lean"] = int(out[5]) & 1, (int(out[5]) >> 1) & 1, (int(out[5]) >> 2) & 1
         return d
 
     def phase_cycles(self):

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libbrax_b200.so")
-SOURCES = ["config.cpp", "system.cpp", "capi.cpp", "step.cu", "reset.cu", "diff.cu", "vjp.cu"]
+SOURCES = ["config.cpp", "system.cpp", "capi.cpp", "step.cu", "step_lean.cu", "reset.cu", "diff.cu", "vjp.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

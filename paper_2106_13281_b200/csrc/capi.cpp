@@ -301,7 +301,7 @@ brax_status brax_system_launch_config(const brax_system* sys, int64_t n_envs, in
   out[2] = P.E;
   out[3] = P.W;
   out[4] = c.regs;
-  out[5] = (c.tuned ? 1 : 0) | (c.fixed && P.V == 2 ? 2 : 0);
+  out[5] = (c.tuned ? 1 : 0) | (c.fixed && P.V == 2 ? 2 : 0) | (c.lean ? 4 : 0);
   return BRAX_OK;
 }
 

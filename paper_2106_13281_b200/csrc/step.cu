@@ -615,6 +615,7 @@ LaunchConfig heuristic_config(const System& sys, int64_t n) {
   LaunchConfig c;
   c.plan = choose_plan(sys, n);
   if (const char* e = std::getenv("BRAX_FIXED_GATHER")) c.fixed = std::atoi(e) != 0;  // experiments / tests
+  if (const char* e = std::getenv("BRAX_LEAN")) c.lean = std::atoi(e) != 0;
   const char* e = std::getenv("BRAX_MAXREG");
   c.regs = variant_regs(sys.hd.plan[c.plan].V,
                         e ? std::atoi(e) : choose_regs(sys, sys.hd.plan[c.plan], grid_of(sys, c.plan, n)));
@@ -682,6 +683,34 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
         best.plan = p;
         best.regs = regs;
         best.fixed = fx != 0;
+        best.lean = false;
+      }
+    }
+    if (lean_applies(sys, p, t)) {  // the lean kernel of this plan (same bits)
+      const int lregs = regs >= 128 ? 128 : 96;
+      if (launch_lean(sys, t, p, lregs, stream) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      float ms = 1e30f;
+      bool ok = true;
+      for (int round = 0; round < 2 && ok; ++round) {
+        cudaEventRecord(e0, stream);
+        for (int r = 0; r < 3; ++r) launch_lean(sys, t, p, lregs, stream);
+        cudaEventRecord(e1, stream);
+        float m = 0.f;
+        if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&m, e0, e1) != cudaSuccess) {
+          cudaGetLastError();
+          ok = false;
+        }
+        ms = m < ms ? m : ms;
+      }
+      if (ok && ms < best_ms) {
+        best_ms = ms;
+        best.plan = p;
+        best.regs = lregs;
+        best.fixed = true;
+        best.lean = true;
       }
     }
   }
@@ -747,7 +776,9 @@ cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t strea
     if (q < 0) return cudaErrorInvalidValue;
     c.plan = q;
     c.regs = variant_regs(sys.hd.plan[q].V, choose_regs(sys, sys.hd.plan[q], grid_of(sys, q, a.n_envs)));
+    c.lean = false;
   }
+  if (c.lean && lean_applies(sys, c.plan, a)) return launch_lean(sys, a, c.plan, c.regs, stream);
   return launch_with(sys, a, c.plan, c.regs, c.fixed, stream);
 }
 

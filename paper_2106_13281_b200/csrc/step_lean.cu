@@ -1,0 +1,312 @@
+// step_lean.cu — the lean step kernel: the same physics as brax_step_kernel
+// (Alg. 1; device code in step_device.cuh, identical operations in
+// the identical order, so identical bits) with the per-substep scaffolding cut down
+// for the common launch shape (DESIGN.md §5 "Lean kernel").
+//
+// Applies to the two-envs-per-lane plans with G = 2 or 4 lane groups whose work plan
+// gives every warp at most one item step and at most one body step (the planner's
+// G > 1 rule W = max(item steps, body steps) does, up to 16 warps).  Then:
+//   * G, the lanes per group, E and every record stride are compile-time constants;
+//   * each warp's item and body, their code class (the specialised classes of the
+//     kFixed variant, else the generic code) and their shared-memory record addresses
+//     are resolved once, before the substep loop, instead of once per substep;
+//   * no env epilogue, JVP, tracing, random-action or contact-Δv code is compiled in
+//     (those launches use brax_step_kernel).
+// Measured on B200 (tools/experiments/ab.sh): see DESIGN.md §5.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdlib>
+
+#include "step_device.cuh"
+#include "system.h"
+
+namespace brax {
+namespace {
+
+using namespace dev;
+
+struct LeanArgs {
+  StepArgs a;
+  const uint32_t* blob;
+  DHeader hd;
+  int32_t plan;
+  SmemLayout L;
+};
+
+// item classes (warp-uniform: the items sharing a warp step share a class)
+enum : int {
+  kItemNone = 0, kJointHinge = 1, kJoint2 = 2, kJoint3 = 3, kJointGeneric = 4,
+  kCapsuleGround = 5, kSphereGround = 6, kBoxGround = 7, kContactGeneric = 8,
+};
+// body gather shapes with compile-time list lengths (as in the kFixed variant)
+enum : int { kGatherGeneral = 0, kG12 = 1, kG20 = 2, kG22 = 3, kG32 = 4, kG41 = 5 };
+
+template <int G, int R>
+__global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs ka) {
+  using S = F2;
+  constexpr int V = 2, SL = 2, LG = 32 / G, E = 2 * LG, RW = LG * SL;
+  constexpr int LGS = G == 1 ? 5 : G == 2 ? 4 : 3;  // log2(LG)
+  constexpr int QS = kQS2, JS = kJS2, CS = kCS2;
+  extern __shared__ __align__(16) uint32_t smem[];
+  const DHeader& H = ka.hd;
+  const DPlan& P = H.plan[ka.plan];
+  const StepArgs& a = ka.a;
+  const SmemLayout& L = ka.L;
+  const int B = H.B, J = H.J, C = H.C, A = H.A;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [0] tables + QP, [1] actions
+  uint32_t* sBlob = smem + L.blob;
+  float* sQ = reinterpret_cast<float*>(smem + L.q);
+  float* sJ = reinterpret_cast<float*>(smem + L.u);
+  float* sC = sJ + J * LG * JS;
+  float* stg = reinterpret_cast<float*>(smem + L.u);  // aliases sJ/sC outside the substeps
+  float* sA = reinterpret_cast<float*>(smem + L.a);
+  float* sAstg = reinterpret_cast<float*>(smem + L.astg);
+  float* sCnt = reinterpret_cast<float*>(smem + L.cnt);
+  uint32_t* sStat = smem + L.stat;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = lane >> LGS, el = lane & (LG - 1);
+  const int64_t e0 = int64_t(blockIdx.x) * E;
+  const int nvalid = (a.n_envs - e0 < E) ? int(a.n_envs - e0) : E;
+  const bool bulk = a.bulk_ok && nvalid == E;  // block-uniform
+  const bool act_bulk = bulk && a.act_bulk_ok && A > 0;
+  const uint32_t qp_bytes = uint32_t(E * B) * 13u * 4u, act_bytes = uint32_t(E * A) * 4u;
+
+  // S1: tables and (full blocks) the four contiguous QP chunks arrive by TMA bulk copies
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {  // the tables are constant: load them before waiting for the previous grid
+    mbar_expect_tx(&bars[0], uint32_t(H.blob_words) * 4u + (bulk ? qp_bytes : 0u));
+    tma_load(sBlob, ka.blob, uint32_t(H.blob_words) * 4u, &bars[0]);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the QP may be the previous kernel's output
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (tid == 0) {
+    if (bulk) {
+      float* sp = stg;
+      float* sr = sp + E * B * 3;
+      float* sv = sr + E * B * 4;
+      float* sw = sv + E * B * 3;
+      tma_load(sp, a.pos_in + e0 * B * 3, uint32_t(E * B) * 12u, &bars[0]);
+      tma_load(sr, a.rot_in + e0 * B * 4, uint32_t(E * B) * 16u, &bars[0]);
+      tma_load(sv, a.vel_in + e0 * B * 3, uint32_t(E * B) * 12u, &bars[0]);
+      tma_load(sw, a.ang_in + e0 * B * 3, uint32_t(E * B) * 12u, &bars[0]);
+    }
+    if (act_bulk) {
+      mbar_expect_tx(&bars[1], act_bytes);
+      tma_load(sAstg, a.actions + e0 * A, act_bytes, &bars[1]);
+    }
+  }
+  if (!bulk) load_block<V>(a, sQ, B, E, e0, nvalid);  // ragged tail / unaligned: per-row loads
+  mbar_wait(&bars[0], 0);
+  if (bulk) stg_to_records<V>(stg, sQ, B, E);
+  for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
+  __syncthreads();
+
+  // ---- this warp's program, resolved once: at most one item and one body ----
+  const DBody* bodies = reinterpret_cast<const DBody*>(sBlob + H.off_bodies);
+  const int32_t* item_begin = reinterpret_cast<const int32_t*>(sBlob + P.off_item_begin);
+  const int32_t* body_begin = reinterpret_cast<const int32_t*>(sBlob + P.off_body_begin);
+  const int it0 = item_begin[warp];
+  const int item = it0 < item_begin[warp + 1] ? reinterpret_cast<const int32_t*>(sBlob + P.off_items)[it0 * G + grp]
+                                              : -1;
+  const int bw0 = body_begin[warp];
+  const int body = bw0 < body_begin[warp + 1]
+                       ? reinterpret_cast<const int32_t*>(sBlob + P.off_bodies_of_warp)[bw0 * G + grp]
+                       : -1;
+  int icls = kItemNone;
+  const uint32_t* iparams = nullptr;  // the item's parameter record (DJoint / DSlot) in shared memory
+  float *ip = nullptr, *ic = nullptr, *irec = nullptr, *icnt = nullptr;  // record addresses
+  if (item >= 0 && item < J) {
+    const DJoint& jt = reinterpret_cast<const DJoint*>(sBlob + H.off_joints)[item];
+    const int4 h0 = *reinterpret_cast<const int4*>(&jt);
+    icls = h0.w == 0 ? (h0.z == 1 ? kJointHinge : h0.z == 2 ? kJoint2 : h0.z == 3 ? kJoint3 : kJointGeneric)
+                     : kJointGeneric;
+    iparams = reinterpret_cast<const uint32_t*>(&jt);
+    ip = sQ + ((h0.x << LGS) + el) * QS;
+    ic = sQ + ((h0.y << LGS) + el) * QS;
+    irec = sJ + ((item << LGS) + el) * JS;
+  } else if (item >= J) {
+    const int c = item - J;
+    const DSlot& sl = reinterpret_cast<const DSlot*>(sBlob + H.off_slots)[c];
+    const int4 h0 = *reinterpret_cast<const int4*>(&sl), h1 = reinterpret_cast<const int4*>(&sl)[1];
+    const bool ground = h1.x == 0 && h1.y == 1 && (h1.z & kCapsuleOnGroundFlags) == kCapsuleOnGroundFlags;
+    icls = !ground ? kContactGeneric : h0.x == 1 ? kCapsuleGround : h0.x == 0 ? kSphereGround
+                                   : h0.x == 2 ? kBoxGround : kContactGeneric;
+    iparams = reinterpret_cast<const uint32_t*>(&sl);
+    ip = sQ + ((h0.y << LGS) + el) * QS;
+    ic = sQ + ((h0.z << LGS) + el) * QS;
+    irec = sC + ((c << LGS) + el) * CS;
+    icnt = sCnt + c * RW + el * SL;
+  }
+  int gcls = kGatherGeneral, j0 = 0, nj = 0, c0 = 0, nc = 0;
+  bool free_body = false;
+  float* brow = nullptr;
+  if (body >= 0) {
+    const int32_t* jinc_begin = reinterpret_cast<const int32_t*>(sBlob + H.off_jinc_begin);
+    const int32_t* cinc_begin = reinterpret_cast<const int32_t*>(sBlob + H.off_cinc_begin);
+    j0 = jinc_begin[body];
+    nj = jinc_begin[body + 1] - j0;
+    c0 = cinc_begin[body];
+    nc = cinc_begin[body + 1] - c0;
+    gcls = nj == 1 && nc == 2 ? kG12 : nj == 2 && nc == 0 ? kG20 : nj == 2 && nc == 2 ? kG22
+         : nj == 3 && nc == 2 ? kG32 : nj == 4 && nc == 1 ? kG41 : kGatherGeneral;
+    constexpr int kFreeFlags = kFlagIso | kFlagFreePos | kFlagFreeRot;
+    free_body = (bodies[body].flags & kFreeFlags) == kFreeFlags && !bodies[body].rot_frozen;
+    brow = sQ + ((body << LGS) + el) * QS;
+  }
+  const float* sJe = sJ + el * JS;  // this lane's record of joint 0 (joint j: + j·LG·JS)
+  const float* sCe = sC + el * CS;
+
+  // S2 of the first substep; every later S2 is fused into the previous substep's integrate()
+  if (body >= 0) kinematic<S>(bodies[body], Row<S>{brow}, H.h);
+  for (int64_t step = 0; step < a.n_steps; ++step) {
+    if (act_bulk) {  // this step's actions arrived in sAstg [E][A]; transpose to sA [A][E]
+      mbar_wait(&bars[1], uint32_t(step & 1));
+      for (int i = tid; i < E * A; i += blockDim.x) {
+        const int env = i / A, k = i - env * A;
+        sA[k * RW + eslot<V>(env, LG)] = sAstg[i];
+      }
+    } else {
+      load_actions<V>(a, sA, A, E, LG, step, e0, nvalid);
+    }  // sA is read after the next barrier
+    if (icnt) Lanes<S>::st(icnt, bc<S>(0.f));
+    const bool pf_act = act_bulk && tid == 0 && step + 1 < a.n_steps;
+    for (int s = 0; s < H.S; ++s) {
+      __syncthreads();
+      if (s == 0 && pf_act) {  // prefetch next step's actions
+        mbar_expect_tx(&bars[1], act_bytes);
+        tma_load(sAstg, a.actions + ((step + 1) * a.n_envs + e0) * A, act_bytes, &bars[1]);
+      }
+      // phase 1: this warp's joint (with its actuator) or contact slot (S3-S5)
+      if (icls != kItemNone) {
+        const Row<S> rp{ip}, rc{ic};
+        if (icls <= kJointGeneric) {
+          const DJoint& jt = *reinterpret_cast<const DJoint*>(iparams);
+          const float* act = sA + el * SL;
+          if (icls == kJointHinge) joint<S, 1, 0>(jt, rp, rc, act, RW, irec);
+          else if (icls == kJoint2) joint<S, 2, 0>(jt, rp, rc, act, RW, irec);
+          else if (icls == kJoint3) joint<S, 3, 0>(jt, rp, rc, act, RW, irec);
+          else joint<S>(jt, rp, rc, act, RW, irec);
+        } else {
+          const DSlot& sl = *reinterpret_cast<const DSlot*>(iparams);
+          S cnt = Lanes<S>::ld(icnt);
+          if (icls == kCapsuleGround) contact<S, 1>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
+          else if (icls == kSphereGround) contact<S, 2>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
+          else if (icls == kBoxGround) contact<S, 3>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
+          else contact<S>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
+          Lanes<S>::st(icnt, cnt);
+        }
+      }
+      __syncthreads();
+      // phase 2: this warp's body — gather (S6), potential + collision integrators
+      // (S7, S8) fused with the next substep's kinematic integrator (S2)
+      if (body >= 0) {
+        const bool kin = !(s + 1 == H.S && step + 1 == a.n_steps);
+        const int32_t* jl = reinterpret_cast<const int32_t*>(sBlob + H.off_jinc) + j0;
+        const int32_t* cl = reinterpret_cast<const int32_t*>(sBlob + H.off_cinc) + c0;
+        Acc<S> acc{typename Acc<S>::NoInit{}};
+        switch (gcls) {
+          case kG12: acc.template gather_fixed<1, 2>(jl, cl, sJe, LG * JS, sCe, LG * CS); break;
+          case kG20: acc.template gather_fixed<2, 0>(jl, cl, sJe, LG * JS, sCe, LG * CS); break;
+          case kG22: acc.template gather_fixed<2, 2>(jl, cl, sJe, LG * JS, sCe, LG * CS); break;
+          case kG32: acc.template gather_fixed<3, 2>(jl, cl, sJe, LG * JS, sCe, LG * CS); break;
+          case kG41: acc.template gather_fixed<4, 1>(jl, cl, sJe, LG * JS, sCe, LG * CS); break;
+          default:
+            if (nj > 0) acc.template gather<false>(jl, nj, sJe, LG * JS);
+            else acc.zero_joints();
+            if (nc > 0) acc.template gather<true>(cl, nc, sCe, LG * CS);
+            else acc.zero_slots();
+        }
+        if (free_body) integrate<S, true>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, nullptr, RW);
+        else integrate<S>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, nullptr, RW);
+      }
+    }
+  }
+  __syncthreads();
+  // S9: status bits, contact counts, and the single write-back of the QP (TMA bulk for full blocks)
+  block_extras<V>(a, sQ, sCnt, sStat, B, C, E, LG, e0, nvalid);
+  if (bulk) {
+    records_to_stg<V>(sQ, stg, B, E);
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      const float* sp = stg;
+      const float* sr = sp + E * B * 3;
+      const float* sv = sr + E * B * 4;
+      const float* sw = sv + E * B * 3;
+      tma_store(a.pos_out + e0 * B * 3, sp, uint32_t(E * B) * 12u);
+      tma_store(a.rot_out + e0 * B * 4, sr, uint32_t(E * B) * 16u);
+      tma_store(a.vel_out + e0 * B * 3, sv, uint32_t(E * B) * 12u);
+      tma_store(a.ang_out + e0 * B * 3, sw, uint32_t(E * B) * 12u);
+      tma_store_commit_wait();
+    }
+  } else {
+    store_block<V>(a, sQ, B, E, e0, nvalid);
+  }
+  if (a.status) {
+    __syncthreads();
+    for (int i = tid; i < nvalid; i += blockDim.x) a.status[e0 + i] = sStat[i];
+  }
+}
+
+template <int G, int R>
+cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kMaxDynSmem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: prologue overlaps the previous kernel
+  attr[0].val.programmaticStreamSerializationAllowed = std::getenv("BRAX_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, brax_step_lean<G, R>, ka);
+}
+
+}  // namespace
+
+bool lean_applies(const System& sys, int plan, const StepArgs& a) {
+  const DPlan& P = sys.hd.plan[plan];
+  if (P.V != 2 || (P.G != 2 && P.G != 4)) return false;
+  if (a.env || a.act_random || a.contact_dp || sys.trace || a.dpos_out) return false;
+  if (!sys.lean_plan_ok[plan]) return false;
+  return P.smem_bytes <= kMaxDynSmem;
+}
+
+cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream) {
+  const DPlan& P = sys.hd.plan[plan];
+  const DHeader& H = sys.hd;
+  LeanArgs ka{a, sys.d_blob, sys.hd, plan, {}};
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
+                 al16(a.rot_out) && al16(a.vel_out) && al16(a.ang_out);
+  ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * H.A) % 4 == 0);
+  if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
+  ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, 1, H.blob_words, 0, 0, 0);
+  dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
+  const size_t smem = size_t(P.smem_bytes);
+  if (P.G == 2) {
+    if (regs >= 128) return launch_lean_variant<2, 128>(ka, grid, block, smem, stream);
+    return launch_lean_variant<2, 96>(ka, grid, block, smem, stream);
+  }
+  if (regs >= 128) return launch_lean_variant<4, 128>(ka, grid, block, smem, stream);
+  return launch_lean_variant<4, 96>(ka, grid, block, smem, stream);
+}
+
+}  // namespace brax

@@ -383,6 +383,14 @@ System* build_host(const Config& cfg) {
       blob.push_back(uint32_t(acc));
       if (w < W) acc += int(wb[w].size());
     }
+    {
+      size_t max_items = 0, max_bodies = 0;
+      for (int w = 0; w < W; ++w) {
+        max_items = std::max(max_items, per_warp[w].size());
+        max_bodies = std::max(max_bodies, wb[w].size());
+      }
+      s->lean_plan_ok[pi] = max_items <= 1 && max_bodies <= 1;
+    }
     P.off_bodies_of_warp = int32_t(blob.size());
     for (int w = 0; w < W; ++w)
       for (int k : wb[w])

@@ -18,6 +18,7 @@ struct LaunchConfig {
   int regs = 0;     // register budget variant
   bool tuned = false;
   bool fixed = false;  // fixed-shape body gathers (kFixed instantiation, V = 2 plans)
+  bool lean = false;   // the lean kernel (step_lean.cu; V = 2, G = 2 / 4, ≤ 1 item and body step per warp)
 };
 
 struct System {
@@ -36,6 +37,7 @@ struct System {
   bool trace = false;                  // per-phase cycle tracing (brax_system_set_tracing)
   unsigned long long* d_phase_cycles = nullptr;  // device [4]
   size_t smem_bytes = 0;
+  bool lean_plan_ok[kNumPlans] = {};   // plan gives every warp at most one item step and one body step
   // launch configuration per batch size, measured by brax_system_tune
   // (every plan gives the same bits, so the choice only affects speed)
   bool autotune = true;
@@ -60,6 +62,9 @@ LaunchConfig launch_config(const System& sys, int64_t n_envs);
 
 // Kernel launchers (step.cu, reset.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_step(const System& sys, const StepArgs& a, cudaStream_t stream);
+// The lean kernel (step_lean.cu): whether it can run launch `a` with plan `plan`, and its launcher.
+bool lean_applies(const System& sys, int plan, const StepArgs& a);
+cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream);
 // brax_system_tune: time every launch plan on a's input (scratch outputs), remember the fastest.
 cudaError_t tune_system(const System& sys, const StepArgs& a, cudaStream_t stream);
 // Forward-mode derivative (JVP) of the step: StepArgs' d*_in tangents -> d*_out (NEXT-4).

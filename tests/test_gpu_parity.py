@@ -272,12 +272,14 @@ def test_every_launch_plan_matches_oracle(name):
     ref, ex = o.step(qp, act, threads=8)
     keep = ~ex["ambiguous"]
     try:
-        for plan, fixed in (("1,1", "0"), ("2,1", "0"), ("4,1", "0"), ("1,2", "0"), ("2,2", "0"), ("4,2", "0"),
-                            ("1,2", "1"), ("2,2", "1"), ("4,2", "1")):
+        for plan, fixed, lean in (("1,1", "0", "0"), ("2,1", "0", "0"), ("4,1", "0", "0"), ("1,2", "0", "0"),
+                                  ("2,2", "0", "0"), ("4,2", "0", "0"), ("1,2", "1", "0"), ("2,2", "1", "0"),
+                                  ("4,2", "1", "0"), ("2,2", "1", "1"), ("4,2", "1", "1")):
             for regs in ("56", "96", "128"):
                 os.environ["BRAX_PLAN"] = plan
                 os.environ["BRAX_MAXREG"] = regs
                 os.environ["BRAX_FIXED_GATHER"] = fixed
+                os.environ["BRAX_LEAN"] = lean
                 got, status, ca = gpu_step(s, qp, act)
                 if plan == "1,1" and regs == "56":
                     first = got
@@ -291,6 +293,7 @@ def test_every_launch_plan_matches_oracle(name):
         os.environ.pop("BRAX_PLAN", None)
         os.environ.pop("BRAX_MAXREG", None)
         os.environ.pop("BRAX_FIXED_GATHER", None)
+        os.environ.pop("BRAX_LEAN", None)
 
 
 def test_tune_picks_a_plan_without_touching_inputs():
