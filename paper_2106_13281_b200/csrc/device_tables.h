@@ -43,6 +43,7 @@ enum : int32_t {
 };
 enum : int32_t {
   kSZeroPa = 1, kSZeroPb = 2, kSIdentA = 4, kSIdentB = 8, kSIsoA = 16, kSIsoB = 32,
+  kSZeroLa = 64,  // plane contacts: the A-side point in body A's frame (pa_local) is the origin
 };
 
 // Every struct is a whole number of 16-byte vectors so the kernel reads it with
@@ -67,7 +68,7 @@ struct alignas(16) DJoint {  // 36 words
   float hi[3], k_a;         // ... ; alignment stiffness
   float c_a, strength, pad2, pad3;  // angular damping; actuator strength (act_kind ≥ 0)
 };
-struct alignas(16) DSlot {  // 40 words
+struct alignas(16) DSlot {  // 44 words
   int32_t type, a, b, point;
   int32_t a_static, b_static, flags, pad0;
   float ca_pos[3], ra;      // collider A offset in body A; radius A
@@ -78,6 +79,10 @@ struct alignas(16) DSlot {  // 40 words
   float corner[3], pad1;    // box: signed half-extent corner of slot `point`
   float inv_inertia_a[3], pad2;
   float inv_inertia_b[3], pad3;
+  // plane contacts: the A-side point in body A's frame, ca_pos + rotate(ca_rot, v) with v = 0
+  // (sphere), ±ℓ·ẑ (capsule end), the signed half-extent corner (box): its world position is
+  // x_A + rotate(q_A, pa_local) — one rotation instead of the collider frame q_A ⊗ ca_rot
+  float pa_local[3], pad4;
 };
 
 // Shared-memory layouts (words): per (item, lane) records, 16-byte aligned,

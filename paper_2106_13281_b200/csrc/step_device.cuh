@@ -466,8 +466,13 @@ template <class S> struct Row {
 
 // ---- S2: kinematic integrator (R3, R21) -------------------------
 // rotation part: q' = normalize(q + ½h (0, ω)⊗q) (ω already masked)
+// (0, ω)⊗q written out without the products by the zero scalar part (same values)
+template <class S> __device__ __forceinline__ Q4T<S> qmul_pure(V3T<S> a, Q4T<S> b) {
+  return {-(a.x * b.x) - a.y * b.y - a.z * b.z, a.x * b.w + a.y * b.z - a.z * b.y,
+          a.y * b.w - a.x * b.z + a.z * b.x, a.z * b.w + a.x * b.y - a.y * b.x};
+}
 template <class S> __device__ __forceinline__ Q4T<S> kin_rot(Q4T<S> q, V3T<S> w, float h) {
-  Q4T<S> dq = qmul(Q4T<S>{bc<S>(0.f), w.x, w.y, w.z}, q);
+  Q4T<S> dq = qmul_pure(w, q);
   const float hh = 0.5f * h;
   q = Q4T<S>{q.w + hh * dq.w, q.x + hh * dq.x, q.y + hh * dq.y, q.z + hh * dq.z};
   S n2 = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
@@ -512,9 +517,9 @@ __device__ __forceinline__ JointOut<S> joint_f(const DJoint& Jm, const RowT& P, 
     f = axpy(oc_cl.w, cross_add(wp, rp, P.vel()) - cross_add(wc, rc, C.vel()), f);
   Q4T<S> fp = qmul(qp, Q4T<S>{bc<S>(jp.x), bc<S>(jp.y), bc<S>(jp.z), bc<S>(jp.w)});
   Q4T<S> fc = qmul(qc, Q4T<S>{bc<S>(jc.x), bc<S>(jc.y), bc<S>(jc.z), bc<S>(jc.w)});
+  // q_r's canonicalisation to w >= 0 (R25) is not evaluated: every entry of R(q_r) below is a
+  // sum of products of two components, which flipping all four signs leaves bit-identical
   Q4T<S> qr = qmul(qconj(fp), fc);
-  S sg = sel(lt(qr.w, bc<S>(0.f)), bc<S>(-1.f), bc<S>(1.f));  // canonicalise q_r to w >= 0 (R25)
-  qr = Q4T<S>{sg * qr.w, sg * qr.x, sg * qr.y, sg * qr.z};
   S R02 = 2.f * (qr.x * qr.z + qr.w * qr.y);
   S R12 = 2.f * (qr.y * qr.z - qr.w * qr.x);
   S R22 = 1.f - 2.f * (qr.x * qr.x + qr.y * qr.y);
@@ -672,13 +677,8 @@ __device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT&
   const float ra = ca.w, rb = cb.w;
   Q4T<S> qa = A.rot(), qb = B.rot();
   V3T<S> xa = A.pos(), xb = B.pos();
-  V3T<S> cA = (fl & kSZeroPa) ? xa : xa + rotate(qa, V3T<S>{bc<S>(ca.x), bc<S>(ca.y), bc<S>(ca.z)});
   V3T<S> cB = (fl & kSZeroPb) ? xb : xb + rotate(qb, V3T<S>{bc<S>(cb.x), bc<S>(cb.y), bc<S>(cb.z)});
-  Q4T<S> qA = qa, qB = qb;
-  if (!(fl & kSIdentA)) {
-    const float4 r = S4[3];
-    qA = qmul(qa, Q4T<S>{bc<S>(r.x), bc<S>(r.y), bc<S>(r.z), bc<S>(r.w)});
-  }
+  Q4T<S> qB = qb;
   if (!(fl & kSIdentB)) {
     const float4 r = S4[5];
     qB = qmul(qb, Q4T<S>{bc<S>(r.x), bc<S>(r.y), bc<S>(r.z), bc<S>(r.w)});
@@ -688,17 +688,26 @@ __device__ __forceinline__ ContactOut<S> contact_f(const DSlot& SLm, const RowT&
   S d;
   if (type <= 2) {  // sphere / capsule end / box corner vs plane: plane is B
     n = rotate_z(qB);
+    // the A-side point x_A + rotate(q_A, pa_local) (DSlot::pa_local; a sphere at its body's origin: x_A)
+    V3T<S> c = xa;
+    if (kCls == 1 || kCls == 3 || (kCls == 0 && !(fl & kSZeroLa))) {
+      const float4 l = S4[10];
+      c = xa + rotate(qa, V3T<S>{bc<S>(l.x), bc<S>(l.y), bc<S>(l.z)});
+    }
     if (type == 2) {
-      const float4 k = S4[7];
-      V3T<S> c = cA + rotate(qA, V3T<S>{bc<S>(k.x), bc<S>(k.y), bc<S>(k.z)});
       d = -dot(c - cB, n);
       pt = c;
     } else {
-      V3T<S> c = (type == 1) ? axpy(ells.x, rotate_z(qA), cA) : cA;
       d = ra - dot(c - cB, n);
       pt = axpy(-ra, n, c);
     }
   } else {
+    V3T<S> cA = (fl & kSZeroPa) ? xa : xa + rotate(qa, V3T<S>{bc<S>(ca.x), bc<S>(ca.y), bc<S>(ca.z)});
+    Q4T<S> qA = qa;
+    if (!(fl & kSIdentA)) {
+      const float4 r = S4[3];
+      qA = qmul(qa, Q4T<S>{bc<S>(r.x), bc<S>(r.y), bc<S>(r.z), bc<S>(r.w)});
+    }
     V3T<S> pa = cA, pb = cB;
     if (type == 4) {  // sphere (A) – capsule (B)
       V3T<S> axb = rotate_z(qB);

@@ -15,7 +15,7 @@
 
 namespace brax {
 // the kernel reads these records with 16-byte vector loads at fixed slots
-static_assert(sizeof(DBody) == 64 && sizeof(DJoint) == 144 && sizeof(DSlot) == 160, "record sizes");
+static_assert(sizeof(DBody) == 64 && sizeof(DJoint) == 144 && sizeof(DSlot) == 176, "record sizes");
 static_assert(offsetof(DJoint, o_p) == 32 && offsetof(DJoint, o_c) == 48 && offsetof(DJoint, jp) == 64 &&
                   offsetof(DJoint, jc) == 80 && offsetof(DJoint, lo) == 96 && offsetof(DJoint, hi) == 112 &&
                   offsetof(DJoint, c_a) == 128,
@@ -272,6 +272,22 @@ System* build_host(const Config& cfg) {
     d.flags = (zero3(d.ca_pos) ? kSZeroPa : 0) | (zero3(d.cb_pos) ? kSZeroPb : 0) | (ident(d.ca_rot) ? kSIdentA : 0) |
               (ident(d.cb_rot) ? kSIdentB : 0) | ((bodies[sl.a].flags & kFlagIso) ? kSIsoA : 0) |
               ((bodies[sl.b].flags & kFlagIso) ? kSIsoB : 0);
+    if (sl.type <= BRAX_SLOT_BOX_PLANE) {  // pa_local = ca_pos + rotate(ca_rot, v), in double
+      double v[3] = {0, 0, 0};
+      if (sl.type == BRAX_SLOT_CAPSULE_PLANE) v[2] = (sl.point == 1 ? -1.0 : 1.0) * (0.5 * A.length - A.radius);
+      if (sl.type == BRAX_SLOT_BOX_PLANE) {
+        const int sg[3] = {(sl.point & 1) ? 1 : -1, (sl.point & 2) ? 1 : -1, (sl.point & 4) ? 1 : -1};
+        for (int k = 0; k < 3; ++k) v[k] = sg[k] * A.halfsize[k];
+      }
+      const double* q = A.rot;  // rotate(q, v) = v + w·t + u×t, t = 2 u×v
+      const double t[3] = {2 * (q[2] * v[2] - q[3] * v[1]), 2 * (q[3] * v[0] - q[1] * v[2]),
+                           2 * (q[1] * v[1] - q[2] * v[0])};
+      const double r[3] = {v[0] + q[0] * t[0] + (q[2] * t[2] - q[3] * t[1]),
+                           v[1] + q[0] * t[1] + (q[3] * t[0] - q[1] * t[2]),
+                           v[2] + q[0] * t[2] + (q[1] * t[1] - q[2] * t[0])};
+      for (int k = 0; k < 3; ++k) d.pa_local[k] = float(A.pos[k] + r[k]);
+      if (zero3(d.pa_local)) d.flags |= kSZeroLa;
+    }
     push_struct(blob, d);
   }
 

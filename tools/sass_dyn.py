@@ -20,10 +20,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2106_13281_b200", "_lib", "libbrax_b200.so")
 
 
-def sass_of(kernel_substr):
+def sass_of(kernel_substr, unit="step", kname="brax_step_kernel"):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=tmp, capture_output=True)
-    cub = os.path.join(tmp, "step.sm_100a.cubin")
+    cub = os.path.join(tmp, f"{unit}.sm_100a.cubin")
     elf = subprocess.run(["cuobjdump", "-elf", cub], capture_output=True, text=True).stdout
     sym = None
     in_symtab = False
@@ -33,7 +33,7 @@ def sass_of(kernel_substr):
             continue
         if in_symtab and line.startswith(".section"):
             break
-        if in_symtab and "brax_step_kernel" in line and kernel_substr in line and line.split()[-1].startswith("_Z"):
+        if in_symtab and kname in line and kernel_substr in line and line.split()[-1].startswith("_Z"):
             sym = line.split()[0]
             break
     if sym is None:
@@ -45,16 +45,18 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("report")
     p.add_argument("--kernel", default="F2ELi96ELb0ELb1E")
+    p.add_argument("--lean", action="store_true", help="the lean kernel (step_lean.cu); --kernel e.g. ILi4ELi96E")
     p.add_argument("--by", default="callsite", choices=["callsite", "line", "op"])
     p.add_argument("--ops", default="")
     p.add_argument("--top", type=int, default=40)
     a = p.parse_args()
     src = {}
-    for f in ("step.cu", "step_device.cuh"):
+    for f in ("step.cu", "step_device.cuh", "step_lean.cu"):
         src[f] = open(os.path.join(ROOT, "paper_2106_13281_b200", "csrc", f)).read().splitlines()
     info = {}
     frames = []
-    for line in sass_of(a.kernel).splitlines():
+    sass = sass_of(a.kernel, "step_lean", "brax_step_lean") if a.lean else sass_of(a.kernel)
+    for line in sass.splitlines():
         if "//## File" in line:
             frames = re.findall(r'"([^"]+)", line (\d+)', line)
             continue
