@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "step_device.cuh"
@@ -179,6 +180,10 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
     const bool pf_act = act_bulk && tid == 0 && step + 1 < a.n_steps;
     for (int s = 0; s < H.S; ++s) {
       __syncthreads();
+#ifdef BRAX_DIAG  // per-warp clock stamps of substep 3 of step 0 in one block (build with -DBRAX_DIAG)
+      const bool dg = a.diag_block && step == 0 && s == 3 && int(blockIdx.x) == a.diag_block - 1 && lane == 0;
+      long long dt0 = dg ? clock64() : 0, dt1 = 0, dt2 = 0;
+#endif
       if (s == 0 && pf_act) {  // prefetch next step's actions
         mbar_expect_tx(&bars[1], act_bytes);
         tma_load(sAstg, a.actions + ((step + 1) * a.n_envs + e0) * A, act_bytes, &bars[1]);
@@ -203,7 +208,13 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
           Lanes<S>::st(icnt, cnt);
         }
       }
+#ifdef BRAX_DIAG
+      if (dg) dt1 = clock64();
+#endif
       __syncthreads();
+#ifdef BRAX_DIAG
+      if (dg) dt2 = clock64();
+#endif
       // phase 2: this warp's body — gather (S6), potential + collision integrators
       // (S7, S8) fused with the next substep's kinematic integrator (S2)
       if (body >= 0) {
@@ -226,6 +237,14 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
         if (free_body) integrate<S, true>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, nullptr, RW);
         else integrate<S>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, nullptr, RW);
       }
+#ifdef BRAX_DIAG
+      if (dg) {  // lane 0 only: no warp-wide synchronisation in here
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        printf("LEAN sm %u warp %d item-class %d body %d gather %d: p1 %lld wait %lld p2 %lld\n", smid, warp, icls,
+               body, gcls, dt1 - dt0, dt2 - dt1, clock64() - dt2);
+      }
+#endif
     }
   }
   __syncthreads();
@@ -298,6 +317,7 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
                  al16(a.rot_out) && al16(a.vel_out) && al16(a.ang_out);
   ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * H.A) % 4 == 0);
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
+  if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
   ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, 1, H.blob_words, 0, 0, 0);
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(P.smem_bytes);
