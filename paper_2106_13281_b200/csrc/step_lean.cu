@@ -74,6 +74,12 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   const bool act_bulk = bulk && a.act_bulk_ok && A > 0;
   const uint32_t qp_bytes = uint32_t(E * B) * 13u * 4u, act_bytes = uint32_t(E * A) * 4u;
 
+#ifdef BRAX_DIAG  // block timeline (globaltimer, ns): entry, after griddepcontrol.wait, staged, loop end, exit
+  long long tl[5] = {0, 0, 0, 0, 0};
+  const bool dgb = a.diag_block && tid == 0 && (blockIdx.x % 64) == 0;
+  auto gtime = []() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+  if (dgb) tl[0] = gtime();
+#endif
   // S1: tables and (full blocks) the four contiguous QP chunks arrive by TMA bulk copies
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -87,6 +93,9 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the QP may be the previous kernel's output
   asm volatile("griddepcontrol.launch_dependents;");
+#ifdef BRAX_DIAG
+  if (dgb) tl[1] = gtime();
+#endif
   if (tid == 0) {
     if (bulk) {
       float* sp = stg;
@@ -108,6 +117,9 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   if (bulk) stg_to_records<V>(stg, sQ, B, E);
   for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
   __syncthreads();
+#ifdef BRAX_DIAG
+  if (dgb) tl[2] = gtime();
+#endif
 
   // ---- this warp's program, resolved once: at most one item and one body ----
   const DBody* bodies = reinterpret_cast<const DBody*>(sBlob + H.off_bodies);
@@ -248,6 +260,9 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
     }
   }
   __syncthreads();
+#ifdef BRAX_DIAG
+  if (dgb) tl[3] = gtime();
+#endif
   // S9: status bits, contact counts, and the single write-back of the QP (TMA bulk for full blocks)
   block_extras<V>(a, sQ, sCnt, sStat, B, C, E, LG, e0, nvalid);
   if (bulk) {
@@ -264,6 +279,15 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
       tma_store(a.vel_out + e0 * B * 3, sv, uint32_t(E * B) * 12u);
       tma_store(a.ang_out + e0 * B * 3, sw, uint32_t(E * B) * 12u);
       tma_store_commit_wait();
+#ifdef BRAX_DIAG
+      if (dgb) {
+        tl[4] = gtime();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        printf("BLOCK %u sm %u t0 %lld wait %lld stage %lld loop %lld store %lld\n", blockIdx.x, smid, tl[0] % 100000000,
+               tl[1] - tl[0], tl[2] - tl[1], tl[3] - tl[2], tl[4] - tl[3]);
+      }
+#endif
     }
   } else {
     store_block<V>(a, sQ, B, E, e0, nvalid);
@@ -302,7 +326,7 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
 
 bool lean_applies(const System& sys, int plan, const StepArgs& a) {
   const DPlan& P = sys.hd.plan[plan];
-  if (P.V != 2 || (P.G != 2 && P.G != 4)) return false;
+  if (P.V != 2) return false;
   if (a.env || a.act_random || a.contact_dp || sys.trace || a.dpos_out) return false;
   if (!sys.lean_plan_ok[plan]) return false;
   return P.smem_bytes <= kMaxDynSmem;
@@ -321,6 +345,10 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, 1, H.blob_words, 0, 0, 0);
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(P.smem_bytes);
+  if (P.G == 1) {
+    if (regs >= 128) return launch_lean_variant<1, 128>(ka, grid, block, smem, stream);
+    return launch_lean_variant<1, 96>(ka, grid, block, smem, stream);
+  }
   if (P.G == 2) {
     if (regs >= 128) return launch_lean_variant<2, 128>(ka, grid, block, smem, stream);
     return launch_lean_variant<2, 96>(ka, grid, block, smem, stream);
