@@ -28,7 +28,7 @@ constexpr int kEnvsPerBlock = 32;  // lane = env; warp = work item
 // dynamic shared memory a block may request: 227 KB minus the kernel's static
 // shared memory (the tracing sums)
 constexpr int kMaxDynSmem = 227 * 1024 - 128;
-constexpr int kMaxWarps = 24;      // 768 threads per block at most
+constexpr int kMaxWarps = 16;      // 512 threads per block at most
 
 // Flag bits (precomputed on the host; warp-uniform tests in the kernel).  An
 // exact-zero offset, identity frame, isotropic inertia or all-free mask makes the

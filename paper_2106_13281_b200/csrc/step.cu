@@ -687,7 +687,7 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
       }
     }
     if (lean_applies(sys, p, t)) {  // the lean kernel of this plan (same bits)
-      const int lregs = regs >= 128 ? 128 : 96;
+      const int lregs = regs;  // launch_lean maps it onto its 128 / 96 / 80 instantiations
       if (launch_lean(sys, t, p, lregs, stream) != cudaSuccess) {
         cudaGetLastError();
         continue;

@@ -345,16 +345,20 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, 1, H.blob_words, 0, 0, 0);
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(P.smem_bytes);
+  // register budgets as the generic F2 variants: the largest of 128 / 96 / 80 not above `regs`
   if (P.G == 1) {
     if (regs >= 128) return launch_lean_variant<1, 128>(ka, grid, block, smem, stream);
-    return launch_lean_variant<1, 96>(ka, grid, block, smem, stream);
+    if (regs >= 96) return launch_lean_variant<1, 96>(ka, grid, block, smem, stream);
+    return launch_lean_variant<1, 80>(ka, grid, block, smem, stream);
   }
   if (P.G == 2) {
     if (regs >= 128) return launch_lean_variant<2, 128>(ka, grid, block, smem, stream);
-    return launch_lean_variant<2, 96>(ka, grid, block, smem, stream);
+    if (regs >= 96) return launch_lean_variant<2, 96>(ka, grid, block, smem, stream);
+    return launch_lean_variant<2, 80>(ka, grid, block, smem, stream);
   }
   if (regs >= 128) return launch_lean_variant<4, 128>(ka, grid, block, smem, stream);
-  return launch_lean_variant<4, 96>(ka, grid, block, smem, stream);
+  if (regs >= 96) return launch_lean_variant<4, 96>(ka, grid, block, smem, stream);
+  return launch_lean_variant<4, 80>(ka, grid, block, smem, stream);
 }
 
 }  // namespace brax
