@@ -30,10 +30,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def astronaut_text(substeps: int, strength: float) -> str:
-    """humanoid.bxc with gravity, damping and colliders removed, torque actuators of `strength`."""
+def astronaut_text(substeps: int, strength: float, dt: float | None = None) -> str:
+    """humanoid.bxc with gravity, damping and colliders removed, torque actuators of `strength`
+    (and the step length dt, if given)."""
     with open(os.path.join(ROOT, "scenes", "humanoid.bxc")) as f:
         t = f.read()
+    if dt is not None:
+        t = re.sub(r"^dt: *[0-9.]+", f"dt: {dt}", t, flags=re.M)
     t = re.sub(r"gravity \{[^}]*\}", "gravity { }", t)
     t = re.sub(r"angular_damping: [0-9.]+", "angular_damping: 0", t)
     t = re.sub(r"\n  colliders \{[^\n]*\} \}", " }", t)       # each body's one-line collider block
@@ -145,12 +148,74 @@ def run(seeds=128, substeps_list=(2, 4, 8, 16), horizon_s=1.0):
     return out
 
 
+def run_dt_ladder(seeds=16, dts=(0.02, 0.01, 0.005, 0.0025), substeps=4, horizon_s=1.0, engine="gpu"):
+    """The Fig. 5 fidelity axis (steps per second): the same two protocols
+    at a ladder of step lengths dt (substeps fixed), on the GPU kernel or on the fp64 oracle,
+    from identical inputs (brax_reset's Philox noise = oracle.reset; the same NumPy actions and
+    kicks).  Returns one dict per dt with mean drifts over the seeds and the per-seed energy
+    drift."""
+    import oracle
+    import synth
+    out = []
+    for dt in dts:
+        text_mom, text_en = astronaut_text(substeps, 0.5, dt), astronaut_text(substeps, 0.0, dt)
+        o_m, o_e = oracle.Oracle(text_mom), oracle.Oracle(text_en)
+        steps = int(round(horizon_s / dt))
+        acts = synth.actions(300 + int(1e4 * dt), steps, seeds, o_m.act_dim)
+        q0 = o_m.reset(seeds, 7, 0.1, 0.1)
+        e0 = o_e.reset(seeds, 7, 0.0, 0.0)
+        rng = np.random.Generator(np.random.PCG64(400 + int(1e4 * dt)))
+        kick = rng.normal(size=e0["vel"].shape)
+        kick /= np.linalg.norm(kick, axis=-1, keepdims=True)
+        e0["vel"] = kick
+        q0 = synth.to_f32(q0)
+        e0 = synth.to_f32(e0)
+        if engine == "oracle":
+            q1, _ = o_m.rollout(q0, acts, threads=8)
+            e1, _ = o_e.rollout(e0, np.zeros((steps, seeds, o_e.act_dim), np.float32), threads=8)
+        else:
+            import torch
+
+            import paper_2106_13281_b200 as bx
+            sys_m, sys_e = bx.System(text_mom), bx.System(text_en)
+            qd = {k: torch.from_numpy(v).cuda() for k, v in q0.items()}
+            ed = {k: torch.from_numpy(v).cuda() for k, v in e0.items()}
+            ad = torch.from_numpy(acts).cuda()
+            zero = torch.zeros((seeds, sys_e.act_dim), device="cuda")
+            for t in range(steps):
+                sys_m.step(qd, ad[t], qd)
+                sys_e.step(ed, zero, ed)
+            torch.cuda.synchronize()
+            q1 = {k: v.cpu().numpy() for k, v in qd.items()}
+            e1 = {k: v.cpu().numpy() for k, v in ed.items()}
+        P0, L0, _ = invariants(o_m.sys, q0)
+        P1, L1, _ = invariants(o_m.sys, q1)
+        _, _, E0 = invariants(o_e.sys, e0)
+        _, _, E1 = invariants(o_e.sys, e1)
+        out.append({"engine": engine, "dt": dt, "substeps": substeps, "steps": steps, "seeds": seeds,
+                    "linear_momentum_drift": float(np.mean(np.linalg.norm(P1 - P0, axis=-1))),
+                    "angular_momentum_drift": float(np.mean(np.linalg.norm(L1 - L0, axis=-1))),
+                    "energy_drift": float(np.mean(np.abs(E1 - E0))),
+                    "energy_rel_drift": float(np.mean(np.abs(E1 - E0) / np.abs(E0))),
+                    "energy_drift_per_seed": (E1 - E0).tolist(), "energy0_per_seed": E0.tolist()})
+    return out
+
+
 if __name__ == "__main__":
     p = argparse.ArgumentParser()
     p.add_argument("--seeds", type=int, default=128)
     p.add_argument("--json", default=None)
+    p.add_argument("--dt-ladder", action="store_true", help="GPU and oracle over dt in {0.02, 0.01, 0.005, 0.0025}")
     a = p.parse_args()
-    res = run(a.seeds)
+    if a.dt_ladder:
+        res = []
+        for eng in ("oracle", "gpu"):
+            res += run_dt_ladder(min(a.seeds, 16), engine=eng)
+        for r in res:
+            r.pop("energy_drift_per_seed")
+            r.pop("energy0_per_seed")
+    else:
+        res = run(a.seeds)
     for r in res:
         print(json.dumps(r))
     if a.json:
