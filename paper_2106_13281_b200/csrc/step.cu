@@ -664,11 +664,11 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
         cudaGetLastError();
         continue;
       }
-      float ms = 1e30f;  // the fastest of three rounds of five launches (timing noise)
+      float ms = 1e30f;  // the fastest of five rounds of eight launches (timing noise)
       bool ok = true;
-      for (int round = 0; round < 3 && ok; ++round) {
+      for (int round = 0; round < 5 && ok; ++round) {
         cudaEventRecord(e0, stream);
-        for (int r = 0; r < 5; ++r) launch_with(sys, t, p, regs, fx, stream);
+        for (int r = 0; r < 8; ++r) launch_with(sys, t, p, regs, fx, stream);
         cudaEventRecord(e1, stream);
         float m = 0.f;
         if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&m, e0, e1) != cudaSuccess) {
@@ -694,9 +694,9 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
       }
       float ms = 1e30f;
       bool ok = true;
-      for (int round = 0; round < 3 && ok; ++round) {
+      for (int round = 0; round < 5 && ok; ++round) {
         cudaEventRecord(e0, stream);
-        for (int r = 0; r < 5; ++r) launch_lean(sys, t, p, lregs, stream);
+        for (int r = 0; r < 8; ++r) launch_lean(sys, t, p, lregs, stream);
         cudaEventRecord(e1, stream);
         float m = 0.f;
         if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&m, e0, e1) != cudaSuccess) {

@@ -43,12 +43,12 @@ enum : int {
 // body gather shapes with compile-time list lengths (as in the kFixed variant)
 enum : int { kGatherGeneral = 0, kG12 = 1, kG20 = 2, kG22 = 3, kG32 = 4, kG41 = 5 };
 
-template <int G, int R>
+template <class S, int G, int R>
 __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs ka) {
-  using S = F2;
-  constexpr int V = 2, SL = 2, LG = 32 / G, E = 2 * LG, RW = LG * SL;
+  // S = F2: two envs per lane (packed FP32); F1: one env per lane (small batches)
+  constexpr int V = Lanes<S>::V, SL = Lanes<S>::SL, LG = 32 / G, E = V * LG, RW = LG * SL;
   constexpr int LGS = G == 1 ? 5 : G == 2 ? 4 : 3;  // log2(LG)
-  constexpr int QS = kQS2, JS = kJS2, CS = kCS2;
+  constexpr int QS = Lanes<S>::QS, JS = Lanes<S>::JS, CS = Lanes<S>::CS;
   extern __shared__ __align__(16) uint32_t smem[];
   const DHeader& H = ka.hd;
   const DPlan& P = H.plan[ka.plan];
@@ -298,13 +298,13 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   }
 }
 
-template <int G, int R>
+template <class S, int G, int R>
 cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<S, G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kMaxDynSmem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
@@ -319,14 +319,14 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
   attr[0].val.programmaticStreamSerializationAllowed = std::getenv("BRAX_NO_PDL") ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, brax_step_lean<G, R>, ka);
+  return cudaLaunchKernelEx(&cfg, brax_step_lean<S, G, R>, ka);
 }
 
 }  // namespace
 
 bool lean_applies(const System& sys, int plan, const StepArgs& a) {
   const DPlan& P = sys.hd.plan[plan];
-  if (P.V != 2) return false;
+  if (P.V != 2 && P.G == 1) return false;  // one env per lane: the lane-group plans only
   if (a.env || a.act_random || a.contact_dp || sys.trace || a.dpos_out) return false;
   if (!sys.lean_plan_ok[plan]) return false;
   return P.smem_bytes <= kMaxDynSmem;
@@ -342,23 +342,33 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * H.A) % 4 == 0);
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
   if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
-  ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, 1, H.blob_words, 0, 0, 0);
+  ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, P.V == 2 ? 1 : 0, H.blob_words, 0, 0, 0);
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
   const size_t smem = size_t(P.smem_bytes);
-  // register budgets as the generic F2 variants: the largest of 128 / 96 / 80 not above `regs`
-  if (P.G == 1) {
-    if (regs >= 128) return launch_lean_variant<1, 128>(ka, grid, block, smem, stream);
-    if (regs >= 96) return launch_lean_variant<1, 96>(ka, grid, block, smem, stream);
-    return launch_lean_variant<1, 80>(ka, grid, block, smem, stream);
+  // register budgets: the largest instantiation not above `regs` (F2 128 / 96 / 80; F1 128 / 96 / 64)
+  if (P.V == 2) {
+    if (P.G == 1) {
+      if (regs >= 128) return launch_lean_variant<F2, 1, 128>(ka, grid, block, smem, stream);
+      if (regs >= 96) return launch_lean_variant<F2, 1, 96>(ka, grid, block, smem, stream);
+      return launch_lean_variant<F2, 1, 80>(ka, grid, block, smem, stream);
+    }
+    if (P.G == 2) {
+      if (regs >= 128) return launch_lean_variant<F2, 2, 128>(ka, grid, block, smem, stream);
+      if (regs >= 96) return launch_lean_variant<F2, 2, 96>(ka, grid, block, smem, stream);
+      return launch_lean_variant<F2, 2, 80>(ka, grid, block, smem, stream);
+    }
+    if (regs >= 128) return launch_lean_variant<F2, 4, 128>(ka, grid, block, smem, stream);
+    if (regs >= 96) return launch_lean_variant<F2, 4, 96>(ka, grid, block, smem, stream);
+    return launch_lean_variant<F2, 4, 80>(ka, grid, block, smem, stream);
   }
   if (P.G == 2) {
-    if (regs >= 128) return launch_lean_variant<2, 128>(ka, grid, block, smem, stream);
-    if (regs >= 96) return launch_lean_variant<2, 96>(ka, grid, block, smem, stream);
-    return launch_lean_variant<2, 80>(ka, grid, block, smem, stream);
+    if (regs >= 128) return launch_lean_variant<F1, 2, 128>(ka, grid, block, smem, stream);
+    if (regs >= 96) return launch_lean_variant<F1, 2, 96>(ka, grid, block, smem, stream);
+    return launch_lean_variant<F1, 2, 64>(ka, grid, block, smem, stream);
   }
-  if (regs >= 128) return launch_lean_variant<4, 128>(ka, grid, block, smem, stream);
-  if (regs >= 96) return launch_lean_variant<4, 96>(ka, grid, block, smem, stream);
-  return launch_lean_variant<4, 80>(ka, grid, block, smem, stream);
+  if (regs >= 128) return launch_lean_variant<F1, 4, 128>(ka, grid, block, smem, stream);
+  if (regs >= 96) return launch_lean_variant<F1, 4, 96>(ka, grid, block, smem, stream);
+  return launch_lean_variant<F1, 4, 64>(ka, grid, block, smem, stream);
 }
 
 }  // namespace brax
