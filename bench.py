@@ -223,9 +223,14 @@ class Workload:
                 self.sets.append(qp)
             self.acts = torch.from_numpy(synth.actions(17 + rank, self.R, n, A)).to(dev) if A else None
         stream.synchronize()
-        # the launch configuration is measured here, outside any timed region
-        s.tune(self.sets[0], self.act(0), stream=stream)
         self.graph = None
+        self.tuned = False
+
+    def tune(self):
+        """The launch configuration, measured outside any timed region on a state of the
+        workload's own trajectory (after warm-up: contact activity decides between plans)."""
+        self.system.tune(self.sets[0], self.act(0), stream=self.stream)
+        self.tuned = True
 
     def act(self, i):
         return self.acts[i % self.R] if self.acts is not None else None
@@ -238,7 +243,12 @@ class Workload:
         with self.torch.cuda.stream(self.stream):
             for i in range(W):
                 self.launch(i)
+                if i == min(W, 2 * self.R) - 1 and not self.tuned:
+                    self.stream.synchronize()
+                    self.tune()
         self.stream.synchronize()
+        if not self.tuned:
+            self.tune()
 
     def capture(self, K):
         torch = self.torch

@@ -25,7 +25,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <vector>
 #include <cstdlib>
 
 #include "device_rng.cuh"
@@ -639,81 +641,106 @@ LaunchConfig tune(const System& sys, const StepArgs& a, cudaStream_t stream) {
   }
   float* f[4] = {buf, nullptr, nullptr, nullptr};
   for (int k = 1; k < 4; ++k) f[k] = f[k - 1] + fbytes[k - 1] / 4;
-  // every trial steps the caller's (read-only) input into the scratch buffers: all
-  // plans are timed on the same state (in-place trials would let the state drift
-  // between plans, e.g. towards more contacts, and bias the later ones)
+  // the trials step a scratch copy of the caller's state in place (the caller's buffers are
+  // not written): stepping one fixed input out of place ranked the plans differently from a
+  // trajectory (ant 8192: (2,2) chosen, 1 µs slower per step in bench.py than (4,2)); the
+  // candidates are timed in interleaved rounds, so the state's drift reaches all alike
   StepArgs t = a;
-  t.pos_out = f[0];
-  t.rot_out = f[1];
-  t.vel_out = f[2];
-  t.ang_out = f[3];
+  const float* src[4] = {a.pos_in, a.rot_in, a.vel_in, a.ang_in};
+  for (int k = 0; k < 4; ++k) cudaMemcpyAsync(f[k], src[k], fbytes[k], cudaMemcpyDeviceToDevice, stream);
+  t.pos_in = t.pos_out = f[0];
+  t.rot_in = t.rot_out = f[1];
+  t.vel_in = t.vel_out = f[2];
+  t.ang_in = t.ang_out = f[3];
   t.n_steps = 1;
   t.status = nullptr;
   t.contact_active = nullptr;
   t.contact_dp = nullptr;
   t.env = 0;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  float best_ms = 1e30f;
+  // candidates: every plan that fits, its generic / specialised / lean kernels at the plan's
+  // register budget; each warmed up (and checked feasible) once
+  std::vector<LaunchConfig> cands;
+  auto run = [&](const LaunchConfig& c) {
+    return c.lean ? launch_lean(sys, t, c.plan, c.regs, stream) : launch_with(sys, t, c.plan, c.regs, c.fixed, stream);
+  };
   for (int p = 0; p < kNumPlans; ++p) {
     if (!plan_fits(sys, p)) continue;
     const int regs = variant_regs(sys.hd.plan[p].V, choose_regs(sys, sys.hd.plan[p], grid_of(sys, p, n)));
+    std::vector<LaunchConfig> cs;
     for (int fx = 0; fx < (sys.hd.plan[p].V == 2 ? 2 : 1); ++fx) {
-      if (launch_with(sys, t, p, regs, fx, stream) != cudaSuccess) {  // warm-up (and feasibility)
-        cudaGetLastError();
-        continue;
-      }
-      float ms = 1e30f;  // the fastest of five rounds of eight launches (timing noise)
-      bool ok = true;
-      for (int round = 0; round < 5 && ok; ++round) {
-        cudaEventRecord(e0, stream);
-        for (int r = 0; r < 8; ++r) launch_with(sys, t, p, regs, fx, stream);
-        cudaEventRecord(e1, stream);
-        float m = 0.f;
-        if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&m, e0, e1) != cudaSuccess) {
-          cudaGetLastError();
-          ok = false;
-        }
-        ms = m < ms ? m : ms;
-      }
-      if (!ok) continue;
-      if (ms < best_ms) {
-        best_ms = ms;
-        best.plan = p;
-        best.regs = regs;
-        best.fixed = fx != 0;
-        best.lean = false;
-      }
+      LaunchConfig c;
+      c.plan = p;
+      c.regs = regs;
+      c.fixed = fx != 0;
+      cs.push_back(c);
     }
     if (lean_applies(sys, p, t)) {  // the lean kernel of this plan (same bits)
-      const int lregs = regs;  // launch_lean maps it onto its 128 / 96 / 80 instantiations
-      if (launch_lean(sys, t, p, lregs, stream) != cudaSuccess) {
+      LaunchConfig c;
+      c.plan = p;
+      c.regs = regs;  // launch_lean maps it onto its own instantiations
+      c.fixed = true;
+      c.lean = true;
+      cs.push_back(c);
+    }
+    for (const LaunchConfig& c : cs) {
+      if (run(c) != cudaSuccess) {
         cudaGetLastError();
         continue;
       }
-      float ms = 1e30f;
-      bool ok = true;
-      for (int round = 0; round < 5 && ok; ++round) {
-        cudaEventRecord(e0, stream);
-        for (int r = 0; r < 8; ++r) launch_lean(sys, t, p, lregs, stream);
-        cudaEventRecord(e1, stream);
-        float m = 0.f;
-        if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&m, e0, e1) != cudaSuccess) {
-          cudaGetLastError();
-          ok = false;
-        }
-        ms = m < ms ? m : ms;
-      }
-      if (ok && ms < best_ms) {
-        best_ms = ms;
-        best.plan = p;
-        best.regs = lregs;
-        best.fixed = true;
-        best.lean = true;
-      }
+      cands.push_back(c);
     }
   }
+  // interleaved timing of CUDA graphs of 32 launches per candidate (the way a caller replays
+  // steps; long enough that the first launch's missing overlap with a predecessor does not
+  // decide), five rounds, each candidate's fastest round; on a private stream
+  // ordered after the caller's work (graph capture needs a non-legacy stream)
+  cudaEvent_t e0, e1, ready;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  cudaStream_t ts = nullptr;
+  cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking);
+  cudaEventRecord(ready, stream);
+  cudaStreamWaitEvent(ts, ready, 0);
+  std::vector<cudaGraphExec_t> gx(cands.size(), nullptr);
+  for (size_t i = 0; i < cands.size(); ++i) {
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(ts, cudaStreamCaptureModeThreadLocal) != cudaSuccess) break;
+    cudaStream_t keep = stream;
+    stream = ts;  // run() launches on `stream`
+    for (int r = 0; r < 32; ++r) run(cands[i]);
+    stream = keep;
+    if (cudaStreamEndCapture(ts, &g) == cudaSuccess && g) {
+      if (cudaGraphInstantiate(&gx[i], g, 0) != cudaSuccess) gx[i] = nullptr;
+      cudaGraphDestroy(g);
+    }
+    cudaGetLastError();
+  }
+  std::vector<float> best_of(cands.size(), 1e30f);
+  for (int round = 0; round < 5; ++round)
+    for (size_t i = 0; i < cands.size(); ++i) {
+      if (!gx[i]) continue;
+      cudaEventRecord(e0, ts);
+      cudaGraphLaunch(gx[i], ts);
+      cudaEventRecord(e1, ts);
+      float m = 0.f;
+      if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&m, e0, e1) != cudaSuccess) {
+        cudaGetLastError();
+        m = 1e30f;
+      }
+      if (round > 0) best_of[i] = std::min(best_of[i], m);  // round 0 uploads the graphs
+    }
+  for (cudaGraphExec_t x : gx)
+    if (x) cudaGraphExecDestroy(x);
+  cudaStreamSynchronize(ts);
+  cudaStreamDestroy(ts);
+  cudaEventDestroy(ready);
+  float best_ms = 1e30f;
+  for (size_t i = 0; i < cands.size(); ++i)
+    if (best_of[i] < best_ms) {
+      best_ms = best_of[i];
+      best = cands[i];
+    }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFreeAsync(buf, stream);

@@ -49,6 +49,8 @@ for scene in a.scenes.split(","):
             s.reset(qp, 0, 0.1, 0.1)
             T = a.steps
             acts = torch.from_numpy(synth.actions(1, T, n, s.act_dim)).cuda() if s.act_dim else None
+            for t in range(min(T, 20)):  # tune on a state of the trajectory (contact activity matters)
+                s.step(qp, acts[t] if acts is not None else None, qp)
             if G == "0":
                 s.tune(qp, acts[0] if acts is not None else None)
             def run():  # noqa: E306
