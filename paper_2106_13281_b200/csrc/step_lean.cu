@@ -75,6 +75,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   const uint32_t qp_bytes = uint32_t(E * B) * 13u * 4u, act_bytes = uint32_t(E * A) * 4u;
 
 #ifdef BRAX_DIAG  // block timeline (globaltimer, ns): entry, after griddepcontrol.wait, staged, loop end, exit
+  __shared__ long long sDg[kMaxWarps][4];
   long long tl[5] = {0, 0, 0, 0, 0};
   const bool dgb = a.diag_block && tid == 0 && (blockIdx.x % 64) == 0;
   auto gtime = []() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
@@ -194,7 +195,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
       __syncthreads();
 #ifdef BRAX_DIAG  // per-warp clock stamps of substep 3 of step 0 in one block (build with -DBRAX_DIAG)
       const bool dg = a.diag_block && step == 0 && s == 3 && int(blockIdx.x) == a.diag_block - 1 && lane == 0;
-      long long dt0 = dg ? clock64() : 0, dt1 = 0, dt2 = 0;
+      if (dg) sDg[warp][0] = clock64();
 #endif
       if (s == 0 && pf_act) {  // prefetch next step's actions
         mbar_expect_tx(&bars[1], act_bytes);
@@ -221,11 +222,11 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
         }
       }
 #ifdef BRAX_DIAG
-      if (dg) dt1 = clock64();
+      if (dg) sDg[warp][1] = clock64();
 #endif
       __syncthreads();
 #ifdef BRAX_DIAG
-      if (dg) dt2 = clock64();
+      if (dg) sDg[warp][2] = clock64();
 #endif
       // phase 2: this warp's body — gather (S6), potential + collision integrators
       // (S7, S8) fused with the next substep's kinematic integrator (S2)
@@ -250,18 +251,21 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
         else integrate<S>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, nullptr, RW);
       }
 #ifdef BRAX_DIAG
-      if (dg) {  // lane 0 only: no warp-wide synchronisation in here
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        printf("LEAN sm %u warp %d item-class %d body %d gather %d: p1 %lld wait %lld p2 %lld\n", smid, warp, icls,
-               body, gcls, dt1 - dt0, dt2 - dt1, clock64() - dt2);
-      }
+      if (dg) sDg[warp][3] = clock64();  // printed after the substep loop (printf would skew the stamps)
 #endif
     }
   }
   __syncthreads();
 #ifdef BRAX_DIAG
   if (dgb) tl[3] = gtime();
+  if (a.diag_block && int(blockIdx.x) == a.diag_block - 1 && tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    for (int w = 0; w < int(blockDim.x >> 5); ++w)
+      printf("LEAN sm %u warp %d: p1 %lld wait %lld p2 %lld (from substep start: p1 end %lld, p2 end %lld)\n", smid, w,
+             sDg[w][1] - sDg[w][0], sDg[w][2] - sDg[w][1], sDg[w][3] - sDg[w][2], sDg[w][1] - sDg[0][0],
+             sDg[w][3] - sDg[0][0]);
+  }
 #endif
   // S9: status bits, contact counts, and the single write-back of the QP (TMA bulk for full blocks)
   block_extras<V>(a, sQ, sCnt, sStat, B, C, E, LG, e0, nvalid);
@@ -304,8 +308,12 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<S, G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kMaxDynSmem);
+#ifdef BRAX_DIAG
+    const int max_dyn = kMaxDynSmem - 1024;  // the diagnostics' static shared stamps
+#else
+    const int max_dyn = kMaxDynSmem;
+#endif
+    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<S, G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }

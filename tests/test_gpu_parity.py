@@ -101,6 +101,8 @@ def test_full_size_sampled_parity(name, n):
     qp64["ang"] += kick_w * np.array([1 - b.is_static for b in o.sys.bodies])[None, :, None]
     qp = synth.to_f32(qp64)
     act = synth.actions(8, 1, n, o.act_dim)[0]
+    s.tune(dev(qp), torch.from_numpy(act).cuda() if o.act_dim else None)  # the configuration bench.py runs
+    assert s.launch_config(n)["tuned"] == 1
     got, status, ca = gpu_step(s, qp, act)
     rows = synth.sample_envs(9, n, 192)
     ref, ex = o.step({k: v[rows] for k, v in qp.items()}, act[rows], threads=8)
