@@ -10,8 +10,9 @@
 //   * each warp's item and body, their code class (the specialised classes of the
 //     kFixed variant, else the generic code) and their shared-memory record addresses
 //     are resolved once, before the substep loop, instead of once per substep;
-//   * no env epilogue, JVP, tracing, random-action or contact-Δv code is compiled in
-//     (those launches use brax_step_kernel).
+//   * no JVP, tracing or contact-Δv code is compiled in (those launches use
+//     brax_step_kernel); the env epilogue (NEXT-1) is a separate instantiation (kEnv),
+//     with brax_step_kernel's epilogue code in the same order (same bits).
 // Measured on B200 (tools/experiments/ab.sh): see DESIGN.md §5.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -19,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "device_rng.cuh"
 #include "step_device.cuh"
 #include "system.h"
 
@@ -43,7 +45,7 @@ enum : int {
 // body gather shapes with compile-time list lengths (as in the kFixed variant)
 enum : int { kGatherGeneral = 0, kG12 = 1, kG20 = 2, kG22 = 3, kG32 = 4, kG41 = 5 };
 
-template <class S, int G, int R>
+template <class S, int G, int R, bool kEnv>
 __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs ka) {
   // S = F2: two envs per lane (packed FP32); F1: one env per lane (small batches)
   constexpr int V = Lanes<S>::V, SL = Lanes<S>::SL, LG = 32 / G, E = V * LG, RW = LG * SL;
@@ -65,6 +67,16 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   float* sAstg = reinterpret_cast<float*>(smem + L.astg);
   float* sCnt = reinterpret_cast<float*>(smem + L.cnt);
   uint32_t* sStat = smem + L.stat;
+  // env epilogue (kEnv): torso position at the step start, steps / episode / reset flag per
+  // env, contact Δv of the last substep, observation rows (alias U)
+  const DTask& T = H.task;
+  float* sX0 = reinterpret_cast<float*>(smem + L.x0);
+  int32_t* sSteps = reinterpret_cast<int32_t*>(smem + L.steps);
+  uint32_t* sEp = smem + L.ep;
+  int32_t* sRst = reinterpret_cast<int32_t*>(smem + L.rst);
+  float* sCo = reinterpret_cast<float*>(smem + L.co);
+  float* sObs = reinterpret_cast<float*>(smem + L.u);
+  const bool save_co = kEnv && T.contact_obs;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = lane >> LGS, el = lane & (LG - 1);
@@ -117,6 +129,14 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   mbar_wait(&bars[0], 0);
   if (bulk) stg_to_records<V>(stg, sQ, B, E);
   for (int i = tid; i < E; i += blockDim.x) sStat[i] = 0u;
+  if (kEnv) {
+    for (int i = tid; i < E; i += blockDim.x) {
+      sSteps[i] = i < nvalid && a.steps ? a.steps[e0 + i] : 0;
+      sEp[i] = i < nvalid && a.episode ? a.episode[e0 + i] : 0u;
+    }
+    if (save_co)
+      for (int i = tid; i < 6 * B * RW; i += blockDim.x) sCo[i] = 0.f;
+  }
   __syncthreads();
 #ifdef BRAX_DIAG
   if (dgb) tl[2] = gtime();
@@ -177,14 +197,66 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   const float* sJe = sJ + el * JS;  // this lane's record of joint 0 (joint j: + j·LG·JS)
   const float* sCe = sC + el * CS;
 
+  const int od = T.obs_dim;
+  auto save_x0 = [&]() {  // NEXT-1: torso position at the step boundary (before S2)
+    for (int i = tid; i < E; i += blockDim.x)
+      for (int k = 0; k < 3; ++k) sX0[3 * i + k] = sQ[qword<V>(T.torso, i, 0, k, LG)];
+  };
+  auto observe = [&](float* obs_out) {  // NEXT-1: obs rows of the block's envs -> obs_out [nvalid][od]
+    if (icls != kItemNone && icls <= kJointGeneric) {  // joints: angles and rates, by the warps that own them
+      const DJoint& jt = *reinterpret_cast<const DJoint*>(iparams);
+      joint_obs<S>(jt, Row<S>{ip}, Row<S>{ic}, sObs + el * od, LG * od, 5 + jt.obs_off, 11 + T.nq + jt.obs_off);
+    }
+    const int nco = T.contact_obs ? 6 * B : 0;  // torso and contact parts, one thread per (env, word)
+    for (int i = tid; i < E * (11 + nco); i += blockDim.x) {
+      const int env = i / (11 + nco), k = i - env * (11 + nco);
+      float v;
+      int at;
+      if (k < 11) {
+        const int f = k == 0 ? 0 : k < 5 ? 1 : k < 8 ? 2 : 3;
+        const int c = k == 0 ? 2 : k < 5 ? k - 1 : k < 8 ? k - 5 : k - 8;
+        v = sQ[qword<V>(T.torso, env, f, c, LG)];
+        at = k < 5 ? k : 5 + T.nq + (k - 5);
+      } else {
+        const int b = (k - 11) / 6, kk = (k - 11) - 6 * b;
+        v = fminf(fmaxf(sCo[(b * 6 + kk) * RW + eslot<V>(env, LG)], -1.f), 1.f);
+        at = 11 + 2 * T.nq + (k - 11);
+      }
+      sObs[env * od + at] = v;
+    }
+    __syncthreads();
+    for (int i = tid; i < nvalid * od; i += blockDim.x) obs_out[i] = sObs[i];
+    __syncthreads();
+  };
+
   // S2 of the first substep; every later S2 is fused into the previous substep's integrate()
+  // (env mode ends every step at the boundary: its S2 runs at the next step's start)
+  if (kEnv) {
+    save_x0();
+    __syncthreads();
+  }
   if (body >= 0) kinematic<S>(bodies[body], Row<S>{brow}, H.h);
   for (int64_t step = 0; step < a.n_steps; ++step) {
+    if (kEnv && step > 0) {
+      save_x0();
+      __syncthreads();
+      if (body >= 0) kinematic<S>(bodies[body], Row<S>{brow}, H.h);
+    }
     if (act_bulk) {  // this step's actions arrived in sAstg [E][A]; transpose to sA [A][E]
       mbar_wait(&bars[1], uint32_t(step & 1));
       for (int i = tid; i < E * A; i += blockDim.x) {
         const int env = i / A, k = i - env * A;
         sA[k * RW + eslot<V>(env, LG)] = sAstg[i];
+      }
+    } else if (a.act_random) {  // NEXT-2: this step's actions from the counter-based generator
+      const uint2 key = make_uint2(uint32_t(a.act_seed & 0xffffffffu), uint32_t(a.act_seed >> 32));
+      const int A4 = (A + 3) >> 2;
+      const uint32_t t = uint32_t(a.act_step0 + step);
+      for (int i = tid; i < E * A4; i += blockDim.x) {
+        const int env = i / A4, g = i - env * A4;
+        const uint4 x = philox4x32_10(make_uint4(uint32_t(a.act_env_offset + e0 + env), t, uint32_t(g), kActTag), key);
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        for (int j = 0; j < 4 && 4 * g + j < A; ++j) sA[(4 * g + j) * RW + eslot<V>(env, LG)] = u_pm1(xs[j]);
       }
     } else {
       load_actions<V>(a, sA, A, E, LG, step, e0, nvalid);
@@ -231,7 +303,9 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
       // phase 2: this warp's body — gather (S6), potential + collision integrators
       // (S7, S8) fused with the next substep's kinematic integrator (S2)
       if (body >= 0) {
-        const bool kin = !(s + 1 == H.S && step + 1 == a.n_steps);
+        const bool last = s + 1 == H.S;
+        const bool kin = !(last && (kEnv || step + 1 == a.n_steps));
+        float* const co = save_co && last ? sCo + body * 6 * RW + el * SL : nullptr;
         const int32_t* jl = reinterpret_cast<const int32_t*>(sBlob + H.off_jinc) + j0;
         const int32_t* cl = reinterpret_cast<const int32_t*>(sBlob + H.off_cinc) + c0;
         Acc<S> acc{typename Acc<S>::NoInit{}};
@@ -247,14 +321,65 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
             if (nc > 0) acc.template gather<true>(cl, nc, sCe, LG * CS);
             else acc.zero_slots();
         }
-        if (free_body) integrate<S, true>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, nullptr, RW);
-        else integrate<S>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, nullptr, RW);
+        if (free_body) integrate<S, true>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, co, RW);
+        else integrate<S>(bodies[body], Row<S>{brow}, acc, H.h, H.g, kin, co, RW);
       }
 #ifdef BRAX_DIAG
       if (dg) sDg[warp][3] = clock64();  // printed after the substep loop (printf would skew the stamps)
 #endif
     }
+    if (kEnv) {  // NEXT-1 epilogue of this step (R30-R34), brax_step_kernel's code and order
+      __syncthreads();
+      for (int i = tid; i < E; i += blockDim.x) {  // reward, done, step / episode counters
+        float x1[3];
+        for (int k = 0; k < 3; ++k) x1[k] = sQ[qword<V>(T.torso, i, 0, k, LG)];
+        float fwd = __fmul_rn(__fadd_rn(x1[0], -sX0[3 * i]), T.fwd[0]);
+        fwd = __fmaf_rn(__fadd_rn(x1[1], -sX0[3 * i + 1]), T.fwd[1], fwd);
+        fwd = __fmaf_rn(__fadd_rn(x1[2], -sX0[3 * i + 2]), T.fwd[2], fwd);
+        float ctrl = 0.f;
+        for (int k = 0; k < A; ++k) {
+          const float u = sA[k * RW + eslot<V>(i, LG)];
+          ctrl = __fmaf_rn(u, u, ctrl);
+        }
+        const float reward = __fadd_rn(__fadd_rn(__fdiv_rn(fwd, T.dt), T.survive), -__fmul_rn(T.ctrl_cost, ctrl));
+        const int32_t st1 = sSteps[i] + 1;
+        bool done = st1 >= T.episode_length;
+        if (T.has_healthy) done = done || x1[2] < T.z_lo || x1[2] > T.z_hi;
+        sRst[i] = done ? 1 : 0;
+        sSteps[i] = done ? 0 : st1;
+        if (done) sEp[i] += 1u;
+        if (i < nvalid) {
+          if (a.reward) a.reward[step * a.n_envs + e0 + i] = reward;
+          if (a.done) a.done[step * a.n_envs + e0 + i] = done ? 1 : 0;
+        }
+      }
+      __syncthreads();
+      // auto-reset of done envs (R34): default_qp + noise, Philox counter (env, b, f, episode)
+      const uint2 key = make_uint2(uint32_t(a.seed & 0xffffffffu), uint32_t(a.seed >> 32));
+      for (int i = tid; i < E * B; i += blockDim.x) {
+        const int env = i / B, b = i - env * B;
+        if (!sRst[env]) continue;
+        float x[3], q[4], v[3], w[3];
+        reset_body(a.dqp, a.masks, B, b, uint32_t(a.env_offset + e0 + env), sEp[env], key, T.noise_vel,
+                   T.noise_ang, x, q, v, w);
+        for (int k = 0; k < 3; ++k) {
+          sQ[qword<V>(b, env, 0, k, LG)] = x[k];
+          sQ[qword<V>(b, env, 2, k, LG)] = v[k];
+          sQ[qword<V>(b, env, 3, k, LG)] = w[k];
+        }
+        for (int k = 0; k < 4; ++k) sQ[qword<V>(b, env, 1, k, LG)] = q[k];
+        if (save_co)
+          for (int k = 0; k < 6; ++k) sCo[(b * 6 + k) * RW + eslot<V>(env, LG)] = 0.f;
+      }
+      __syncthreads();
+      if (a.obs) observe(a.obs + (step * a.n_envs + e0) * od);
+    }
   }
+  if (kEnv)
+    for (int i = tid; i < nvalid; i += blockDim.x) {
+      if (a.steps) a.steps[e0 + i] = sSteps[i];
+      if (a.episode) a.episode[e0 + i] = sEp[i];
+    }
   __syncthreads();
 #ifdef BRAX_DIAG
   if (dgb) tl[3] = gtime();
@@ -302,7 +427,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   }
 }
 
-template <class S, int G, int R>
+template <class S, int G, int R, bool kEnv = false>
 cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
@@ -313,7 +438,7 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
 #else
     const int max_dyn = kMaxDynSmem;
 #endif
-    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<S, G, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<S, G, R, kEnv>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
@@ -327,7 +452,7 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
   attr[0].val.programmaticStreamSerializationAllowed = std::getenv("BRAX_NO_PDL") ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, brax_step_lean<S, G, R>, ka);
+  return cudaLaunchKernelEx(&cfg, brax_step_lean<S, G, R, kEnv>, ka);
 }
 
 }  // namespace
@@ -335,9 +460,10 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
 bool lean_applies(const System& sys, int plan, const StepArgs& a) {
   const DPlan& P = sys.hd.plan[plan];
   if (P.V != 2 && P.G == 1) return false;  // one env per lane: the lane-group plans only
-  if (a.env || a.act_random || a.contact_dp || sys.trace || a.dpos_out) return false;
+  if ((a.env && a.n_steps == 0) || a.contact_dp || sys.trace || a.dpos_out) return false;  // observe-only: generic
+  if (a.env && P.G == 1) return false;  // env instantiations: the lane-group plans
   if (!sys.lean_plan_ok[plan]) return false;
-  return P.smem_bytes <= kMaxDynSmem;
+  return (a.env ? P.smem_bytes_env : P.smem_bytes) <= kMaxDynSmem;
 }
 
 cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream) {
@@ -350,9 +476,26 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * H.A) % 4 == 0);
   if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
   if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
-  ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, P.V == 2 ? 1 : 0, H.blob_words, 0, 0, 0);
+  ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, P.V == 2 ? 1 : 0, H.blob_words,
+                     a.env ? H.task.obs_dim : 0, a.env ? H.task.contact_obs : 0, 0);
   dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
-  const size_t smem = size_t(P.smem_bytes);
+  const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);
+  if (a.env) {  // env-epilogue instantiations (register budgets 128 / 96)
+    if (P.V == 2) {
+      if (P.G == 2) {
+        if (regs >= 128) return launch_lean_variant<F2, 2, 128, true>(ka, grid, block, smem, stream);
+        return launch_lean_variant<F2, 2, 96, true>(ka, grid, block, smem, stream);
+      }
+      if (regs >= 128) return launch_lean_variant<F2, 4, 128, true>(ka, grid, block, smem, stream);
+      return launch_lean_variant<F2, 4, 96, true>(ka, grid, block, smem, stream);
+    }
+    if (P.G == 2) {
+      if (regs >= 128) return launch_lean_variant<F1, 2, 128, true>(ka, grid, block, smem, stream);
+      return launch_lean_variant<F1, 2, 96, true>(ka, grid, block, smem, stream);
+    }
+    if (regs >= 128) return launch_lean_variant<F1, 4, 128, true>(ka, grid, block, smem, stream);
+    return launch_lean_variant<F1, 4, 96, true>(ka, grid, block, smem, stream);
+  }
   // register budgets: the largest instantiation not above `regs` (F2 128 / 96 / 80; F1 128 / 96 / 64)
   if (P.V == 2) {
     if (P.G == 1) {

@@ -158,3 +158,38 @@ def test_env_errors():
     s.env_reset(st)
     with pytest.raises(bx.BraxError):
         bx.brax_env_step(s.handle, st["qp"], None, 1, st["qp"], 4, None, None, None, None, None)
+
+
+@pytest.mark.parametrize("name", ["ant", "humanoid", "halfcheetah"])
+def test_lean_kernel_env_and_random_actions_bit_identical(name):
+    """The lean kernel's env-epilogue and on-device-action paths give brax_step_kernel's bits
+    (same device code in the same order) for every plan it applies to."""
+    import os
+    o = oracle.Oracle(oracle.load_scene(name))
+    s = bx.System(oracle.load_scene(name))
+    n, T = 300, 3
+    acts = torch.from_numpy(synth.actions(31, T, n, o.act_dim)).cuda()
+    q0 = o.reset(n, 32, 0.1, 0.1)
+
+    def run(plan, lean):
+        os.environ.update({"BRAX_PLAN": plan, "BRAX_LEAN": lean, "BRAX_FIXED_GATHER": "1"})
+        try:
+            st = s.env_state(n)
+            s.env_reset(st, seed=4)
+            out = s.env_step(st, acts, seed=4)
+            qr = {k: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).cuda() for k, v in q0.items()}
+            s.rollout_random(qr, T, seed=9, env_offset=3, step0=2)
+            torch.cuda.synchronize()
+            return out, st, qr
+        finally:
+            for k in ("BRAX_PLAN", "BRAX_LEAN", "BRAX_FIXED_GATHER"):
+                os.environ.pop(k, None)
+    for plan in ("2,2", "4,2", "2,1", "4,1"):
+        ref, st_ref, qr_ref = run(plan, "0")
+        got, st_got, qr_got = run(plan, "1")
+        for key in ("obs", "reward", "done"):
+            assert torch.equal(got[key], ref[key]), (plan, key)
+        for k in ("pos", "rot", "vel", "ang"):
+            assert torch.equal(st_got["qp"][k], st_ref["qp"][k]), (plan, k)
+            assert torch.equal(qr_got[k], qr_ref[k]), (plan, k)
+        assert torch.equal(st_got["steps"], st_ref["steps"]) and torch.equal(st_got["episode"], st_ref["episode"])
