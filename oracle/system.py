@@ -146,6 +146,18 @@ class Actuator:
 
 
 @dataclass
+class Goal:
+    """Goal-directed task (grasp / fetch; R36): bring
+    `obj` within `radius` of the frozen marker body `target`; the marker is then
+    placed again."""
+    obj: int
+    target: int
+    radius: float
+    bonus: float
+    range: np.ndarray               # marker placement half-extents around its default position
+
+
+@dataclass
 class Task:
     """Locomotion env epilogue (NEXT-1; R30-R35)."""
     torso: int
@@ -157,6 +169,7 @@ class Task:
     contact_obs: bool               # append clipped per-body contact Δv, Δω
     reset_vel_noise: float
     reset_ang_noise: float
+    goal: Goal | None = None
 
 
 @dataclass
@@ -189,10 +202,12 @@ class System:
 
     @property
     def obs_dim(self) -> int:
-        """torso z, quat (5) | joint angles (Σdof) | torso v, ω (6) | joint rates (Σdof) | contacts (6B)."""
+        """torso z, quat (5) | joint angles (Σdof) | torso v, ω (6) | joint rates (Σdof) |
+        goal (9, R36) | contacts (6B)."""
         if self.task is None:
             return 0
-        return 11 + 2 * self.n_joint_dofs + (6 * len(self.bodies) if self.task.contact_obs else 0)
+        return (11 + 2 * self.n_joint_dofs + (9 if self.task.goal is not None else 0)
+                + (6 * len(self.bodies) if self.task.contact_obs else 0))
 
     def slot_table(self) -> np.ndarray:
         """Integer contact-slot table [C, 7] (pair, type, bodyA, bodyB, colA, colB, point)."""
@@ -457,19 +472,46 @@ def parse_system(text: str) -> System:
     if len(slots) > 255:
         raise ValidationError("config", "more than 255 contact slots")
 
-    task = _parse_task(_one(top, "task", "config", "msg", None), bodies, names)
+    task = _parse_task(_one(top, "task", "config", "msg", None), bodies, names, colliders)
     return System(dt=dt, substeps=int(substeps), gravity=gravity, friction=friction,
                   elasticity=elasticity, baumgarte=beta, bodies=bodies, joints=joints,
                   actuators=actuators, colliders=colliders, pairs=pairs, slots=slots, task=task)
 
 
-def _parse_task(node, bodies, names):
-    """task { torso forward survive_reward ctrl_cost healthy_z episode_length contact_obs reset_noise }."""
+def _parse_goal(node, bodies, names, colliders, path):
+    """goal { object target radius bonus range { x y z } } (R36)."""
+    gf = _fields(node, path, {"object", "target", "radius", "bonus", "range"})
+    ix = {}
+    for key in ("object", "target"):
+        nm = _one(gf, key, path, "str")
+        if nm is None:
+            raise ValidationError(f"{path}.{key}", "required")
+        if nm not in names:
+            raise ValidationError(f"{path}.{key}", f"unknown body '{nm}'")
+        ix[key] = names[nm]
+    if bodies[ix["object"]].is_static:
+        raise ValidationError(f"{path}.object", "must not be a static body")
+    if not bodies[ix["target"]].is_static:
+        raise ValidationError(f"{path}.target", "must be a frozen { all: true } marker body")
+    if any(c.body == ix["target"] for c in colliders):
+        raise ValidationError(f"{path}.target", "must have no colliders")
+    radius = _one(gf, "radius", path, "num", None)
+    if radius is None or not radius > 0:
+        raise ValidationError(f"{path}.radius", "must be > 0")
+    rng = _vec3(_one(gf, "range", path, "msg", []), f"{path}.range")
+    if np.any(rng < 0):
+        raise ValidationError(f"{path}.range", "must be >= 0")
+    return Goal(obj=ix["object"], target=ix["target"], radius=radius, bonus=_one(gf, "bonus", path, "num", 0.0),
+                range=rng)
+
+
+def _parse_task(node, bodies, names, colliders):
+    """task { torso forward survive_reward ctrl_cost healthy_z episode_length contact_obs reset_noise goal }."""
     if node is None:
         return None
     path = "config.task"
     tf = _fields(node, path, {"torso", "forward", "survive_reward", "ctrl_cost", "healthy_z", "episode_length",
-                              "contact_obs", "reset_noise"})
+                              "contact_obs", "reset_noise", "goal"})
     tn = _one(tf, "torso", path, "str")
     if tn is None:
         raise ValidationError(f"{path}.torso", "required")
@@ -505,9 +547,11 @@ def _parse_task(node, bodies, names):
     sw = _one(rf, "ang", f"{path}.reset_noise", "num", 0.1)
     if sv < 0 or sw < 0:
         raise ValidationError(f"{path}.reset_noise", "must be >= 0")
+    gn = _one(tf, "goal", path, "msg", None)
+    goal = None if gn is None else _parse_goal(gn, bodies, names, colliders, f"{path}.goal")
     return Task(torso=torso, forward=fwd, survive_reward=_one(tf, "survive_reward", path, "num", 1.0),
                 ctrl_cost=ctrl, healthy_z=healthy, episode_length=int(L), contact_obs=bool(co),
-                reset_vel_noise=sv, reset_ang_noise=sw)
+                reset_vel_noise=sv, reset_ang_noise=sw, goal=goal)
 
 
 def _orient(colliders, i, j):

@@ -536,7 +536,7 @@ Config parse_config(const std::string& text) {
   if (const std::vector<Node>* tn = top.msg("task")) {
     const std::string path = "config.task";
     Fields tf(*tn, path, {"torso", "forward", "survive_reward", "ctrl_cost", "healthy_z", "episode_length",
-                          "contact_obs", "reset_noise"});
+                          "contact_obs", "reset_noise", "goal"});
     Task& t = c.task;
     t.present = true;
     bool has = false;
@@ -575,6 +575,32 @@ Config parse_config(const std::string& text) {
       t.noise_ang = rf.num("ang", 0.1);
     }
     if (t.noise_vel < 0 || t.noise_ang < 0) invalid(path + ".reset_noise", "must be >= 0");
+    if (const std::vector<Node>* gn = tf.msg("goal")) {  // R36
+      const std::string gp = path + ".goal";
+      Fields gf(*gn, gp, {"object", "target", "radius", "bonus", "range"});
+      int ix[2];
+      const char* keys[2] = {"object", "target"};
+      for (int k = 0; k < 2; ++k) {
+        bool has_k = false;
+        const std::string nm = gf.str(keys[k], &has_k);
+        if (!has_k) invalid(gp + "." + keys[k], "required");
+        if (!body_ix.count(nm)) invalid(gp + "." + keys[k], "unknown body '" + nm + "'");
+        ix[k] = body_ix[nm];
+      }
+      t.has_goal = true;
+      t.obj = ix[0];
+      t.target = ix[1];
+      if (c.bodies[t.obj].is_static()) invalid(gp + ".object", "must not be a static body");
+      if (!c.bodies[t.target].is_static()) invalid(gp + ".target", "must be a frozen { all: true } marker body");
+      for (const Collider& col : c.colliders)
+        if (col.body == t.target) invalid(gp + ".target", "must have no colliders");
+      if (!gf.has("radius")) invalid(gp + ".radius", "must be > 0");
+      t.radius = gf.num("radius", 0);
+      if (!(t.radius > 0)) invalid(gp + ".radius", "must be > 0");
+      t.bonus = gf.num("bonus", 0);
+      if (const std::vector<Node>* rg = gf.msg("range")) vec3(rg, gp + ".range", t.range);
+      if (t.range[0] < 0 || t.range[1] < 0 || t.range[2] < 0) invalid(gp + ".range", "must be >= 0");
+    }
   }
   return c;
 }

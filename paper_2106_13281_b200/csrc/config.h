@@ -83,6 +83,11 @@ struct Task {
   int episode_length = 1000;
   bool contact_obs = false;
   double noise_vel = 0.1, noise_ang = 0.1;
+  // goal-directed task (grasp / fetch, R36): bring `obj` within `radius` of the
+  // frozen, collider-free marker body `target`, which is then placed again
+  bool has_goal = false;
+  int obj = 0, target = 0;
+  double radius = 0, bonus = 0, range[3] = {0, 0, 0};
 };
 
 struct Config {
@@ -103,10 +108,10 @@ struct Config {
     for (const Joint& j : joints) n += j.dof;
     return n;
   }
-  // z, quat | joint angles | v, ω | joint rates | per-body contact Δv, Δω (R32)
+  // z, quat | joint angles | v, ω | joint rates | goal (R36) | per-body contact Δv, Δω (R32)
   int obs_dim() const {
     if (!task.present) return 0;
-    return 11 + 2 * n_joint_dofs() + (task.contact_obs ? 6 * int(bodies.size()) : 0);
+    return 11 + 2 * n_joint_dofs() + (task.has_goal ? 9 : 0) + (task.contact_obs ? 6 * int(bodies.size()) : 0);
   }
 };
 

@@ -88,6 +88,40 @@ def test_validation_errors(text, status):
     assert le.value.detail.startswith(oe.value.path + ":")
 
 
+GOAL_BASE = ('bodies { name: "Ball" colliders { sphere { radius: 0.1 } } } '
+             'bodies { name: "T" frozen { all: true } } bodies { name: "W" } ')
+
+
+@pytest.mark.parametrize("goal", [
+    'goal { object: "Ball" target: "W" radius: 0.1 }',
+    'goal { object: "T" target: "T" radius: 0.1 }',
+    'goal { object: "Ball" target: "Ghost" radius: 0.1 }',
+    'goal { object: "Ball" target: "T" }',
+    'goal { object: "Ball" target: "T" radius: -1 }',
+    'goal { object: "Ball" target: "T" radius: 0.1 range { y: -0.5 } }',
+    'goal { target: "T" radius: 0.1 }',
+    'goal { object: "Ball" target: "T" radius: 0.1 size: 1 }',
+])
+def test_goal_validation_errors_agree_with_oracle(goal):
+    """The goal block (R36) is checked identically by both parsers (same field path)."""
+    text = GOAL_BASE + 'task { torso: "Ball" ' + goal + " }"
+    with pytest.raises(oracle.ValidationError) as oe:
+        oracle.parse_system(text)
+    with pytest.raises(bx.BraxError) as le:
+        bx.brax_config_parse(text)
+    assert le.value.name == "BRAX_E_VALIDATION"
+    assert le.value.detail.startswith(oe.value.path + ":"), (le.value.detail, oe.value.path)
+
+
+def test_goal_marker_with_collider_rejected_by_both():
+    text = ('bodies { name: "Ball" } bodies { name: "T" frozen { all: true } colliders { sphere { radius: 1 } } } '
+            'task { torso: "Ball" goal { object: "Ball" target: "T" radius: 0.1 } }')
+    with pytest.raises(oracle.ValidationError, match="collider"):
+        oracle.parse_system(text)
+    with pytest.raises(bx.BraxError, match="collider"):
+        bx.brax_config_parse(text)
+
+
 def test_random_scenes_tables_match_oracle():
     """Randomly generated small scenes: both builders produce identical integer tables."""
     rng = np.random.default_rng(0)

@@ -9,7 +9,7 @@ import synth
 STRUCT = {  # scene: (B, J, A, C, substeps)
     "ball": (2, 0, 0, 1, 1), "pendulum": (2, 1, 1, 0, 1), "chain2": (3, 2, 2, 0, 2),
     "ant": (10, 8, 8, 9, 10), "humanoid": (12, 10, 17, 22, 8), "halfcheetah": (9, 7, 7, 16, 10),
-    "grasp": (16, 13, 19, 27, 4), "fetch": (12, 9, 10, 16, 4), "coverage": (7, 3, 6, 16, 5),
+    "grasp": (17, 13, 19, 27, 4), "fetch": (12, 9, 10, 16, 4), "coverage": (7, 3, 6, 16, 5),
 }
 
 
