@@ -444,7 +444,8 @@ brax_status brax_env_reset(const brax_system* sys, brax_qp out, int64_t n_envs, 
   DeviceGuard dg(s.device);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = brax::launch_reset(s, out.pos, out.rot, out.vel, out.ang, n_envs, io->seed,
-                                     float(s.cfg.task.noise_vel), float(s.cfg.task.noise_ang), cs, io->env_offset);
+                                     float(s.cfg.task.noise_vel), float(s.cfg.task.noise_ang), cs, io->env_offset,
+                                     true);
   if (e == cudaSuccess) e = cudaMemsetAsync(io->steps, 0, size_t(n_envs) * 4, cs);
   if (e == cudaSuccess) e = cudaMemsetAsync(io->episode, 0, size_t(n_envs) * 4, cs);
   if (e != cudaSuccess) return cuda_status(e, "brax_env_reset");

@@ -43,5 +43,15 @@ __device__ __forceinline__ void reset_body(const float* dqp, const float* masks,
   for (int k = 0; k < 4; ++k) q[k] = dqp[3 * B + 4 * b + k];
 }
 
+// Goal-task marker placement (R36): x = x̄_T + range ⊙ u(env, T, field, episode);
+// field 2 at a reset of episode k, 2 + steps' at a hit (steps' ≥ 1: steps after the step).
+__device__ __forceinline__ void place_target(const float* dqp, int tb, const float* range, uint32_t env,
+                                             uint32_t field, uint32_t episode, uint2 key, float* x) {
+  const uint4 r = philox4x32_10(make_uint4(env, uint32_t(tb), field, episode), key);
+  const uint32_t rr[3] = {r.x, r.y, r.z};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) x[k] = __fadd_rn(dqp[3 * tb + k], __fmul_rn(range[k], u_pm1(rr[k])));
+}
+
 }  // namespace dev
 }  // namespace brax

@@ -150,10 +150,12 @@ BRAX_HD inline SmemLayout smem_layout(int32_t B, int32_t J, int32_t C, int32_t A
 // Env epilogue parameters (NEXT-1, R30-R35); present == 0: no task.
 struct DTask {
   int32_t present, torso, episode_length, contact_obs;
-  int32_t nq, obs_dim, has_healthy, pad0;
+  int32_t nq, obs_dim, has_healthy, has_goal;
   float fwd[3], dt;
   float survive, ctrl_cost, z_lo, z_hi;
-  float noise_vel, noise_ang, pad1, pad2;
+  float noise_vel, noise_ang, radius, bonus;
+  int32_t obj, target, pad0, pad1;  // goal task (R36): object body, frozen marker body
+  float range[3], pad2;             // marker placement half-extents
 };
 
 // Arguments of one step launch (device pointers; see include/brax_b200.h).

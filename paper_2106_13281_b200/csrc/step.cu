@@ -195,7 +195,7 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   // ---- NEXT-1 env epilogue pieces (R30-R35; per-env scalar code spells out its rounding) ----
   auto save_x0 = [&]() {  // torso position at the step boundary (before S2)
     for (int i = tid; i < E; i += blockDim.x)
-      for (int k = 0; k < 3; ++k) sX0[3 * i + k] = sQ[qword<V>(T.torso, i, 0, k, LG)];
+      for (int k = 0; k < 3; ++k) sX0[3 * i + k] = sQ[qword<V>(T.obj, i, 0, k, LG)];
   };
   auto observe = [&](float* obs_out) {  // obs rows of the block's envs -> obs_out [nvalid][od]
     // joints: angles and rates, by the warps that own them
@@ -207,9 +207,9 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
                    sObs + el * od, LG * od, 5 + jt.obs_off, 11 + T.nq + jt.obs_off);
     }
     // torso and contact parts, one thread per (env, word)
-    const int nco = T.contact_obs ? 6 * B : 0;
-    for (int i = tid; i < E * (11 + nco); i += blockDim.x) {
-      const int env = i / (11 + nco), k = i - env * (11 + nco);
+    const int nco = T.contact_obs ? 6 * B : 0, ng = T.has_goal ? 9 : 0, nw = 11 + ng + nco;
+    for (int i = tid; i < E * nw; i += blockDim.x) {
+      const int env = i / nw, k = i - env * nw;
       float v;
       int at;
       if (k < 11) {
@@ -217,8 +217,15 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
         const int c = k == 0 ? 2 : k < 5 ? k - 1 : k < 8 ? k - 5 : k - 8;
         v = sQ[qword<V>(T.torso, env, f, c, LG)];
         at = k < 5 ? k : 5 + T.nq + (k - 5);
+      } else if (k < 11 + ng) {  // goal block (R36): x_T − x_O, x_O − x_torso, v_O
+        const int g = (k - 11) / 3, c = (k - 11) - 3 * g;
+        const float xo = sQ[qword<V>(T.obj, env, 0, c, LG)];
+        v = g == 0 ? __fadd_rn(sQ[qword<V>(T.target, env, 0, c, LG)], -xo)
+          : g == 1 ? __fadd_rn(xo, -sQ[qword<V>(T.torso, env, 0, c, LG)])
+                   : sQ[qword<V>(T.obj, env, 2, c, LG)];
+        at = 11 + 2 * T.nq + (k - 11);
       } else {
-        const int b = (k - 11) / 6, kk = (k - 11) - 6 * b;
+        const int b = (k - 11 - ng) / 6, kk = (k - 11 - ng) - 6 * b;
         v = fminf(fmaxf(sCo[(b * 6 + kk) * RW + eslot<V>(env, LG)], -1.f), 1.f);
         at = 11 + 2 * T.nq + (k - 11);
       }
@@ -392,23 +399,44 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
 #endif
     }
     if (envm) {
+      const uint2 key = make_uint2(uint32_t(a.seed & 0xffffffffu), uint32_t(a.seed >> 32));  // reset / marker draws
       __syncthreads();
-      // reward, done, step / episode counters (one thread per env)
+      // reward, done, step / episode counters (one thread per env; goal tasks R36)
       for (int i = tid; i < E; i += blockDim.x) {
-        float x1[3];
-        for (int k = 0; k < 3; ++k) x1[k] = sQ[qword<V>(T.torso, i, 0, k, LG)];
-        float fwd = __fmul_rn(__fadd_rn(x1[0], -sX0[3 * i]), T.fwd[0]);
-        fwd = __fmaf_rn(__fadd_rn(x1[1], -sX0[3 * i + 1]), T.fwd[1], fwd);
-        fwd = __fmaf_rn(__fadd_rn(x1[2], -sX0[3 * i + 2]), T.fwd[2], fwd);
+        float x1[3];  // the torso's (goal tasks: the object's) position after the step
+        for (int k = 0; k < 3; ++k) x1[k] = sQ[qword<V>(T.obj, i, 0, k, LG)];
+        const int32_t st1 = sSteps[i] + 1;
+        float prog;
+        if (T.has_goal) {  // R36: progress towards the marker (+ bonus and a new marker on a hit)
+          float xt[3], s0 = 0.f, s1 = 0.f;
+          for (int k = 0; k < 3; ++k) {
+            xt[k] = sQ[qword<V>(T.target, i, 0, k, LG)];
+            const float e0k = __fadd_rn(sX0[3 * i + k], -xt[k]), e1k = __fadd_rn(x1[k], -xt[k]);
+            s0 = __fmaf_rn(e0k, e0k, s0);
+            s1 = __fmaf_rn(e1k, e1k, s1);
+          }
+          const float d1 = __fsqrt_rn(s1);
+          prog = __fdiv_rn(__fadd_rn(__fsqrt_rn(s0), -d1), T.dt);
+          if (d1 < T.radius) {
+            prog = __fadd_rn(prog, T.bonus);
+            place_target(a.dqp, T.target, T.range, uint32_t(a.env_offset + e0 + i), uint32_t(2 + st1), sEp[i], key, xt);
+            for (int k = 0; k < 3; ++k) sQ[qword<V>(T.target, i, 0, k, LG)] = xt[k];
+          }
+        } else {
+          float fwd = __fmul_rn(__fadd_rn(x1[0], -sX0[3 * i]), T.fwd[0]);
+          fwd = __fmaf_rn(__fadd_rn(x1[1], -sX0[3 * i + 1]), T.fwd[1], fwd);
+          fwd = __fmaf_rn(__fadd_rn(x1[2], -sX0[3 * i + 2]), T.fwd[2], fwd);
+          prog = __fdiv_rn(fwd, T.dt);
+        }
         float ctrl = 0.f;
         for (int k = 0; k < A; ++k) {
           const float u = sA[k * RW + eslot<V>(i, LG)];
           ctrl = __fmaf_rn(u, u, ctrl);
         }
-        const float reward = __fadd_rn(__fadd_rn(__fdiv_rn(fwd, T.dt), T.survive), -__fmul_rn(T.ctrl_cost, ctrl));
-        const int32_t st1 = sSteps[i] + 1;
+        const float reward = __fadd_rn(__fadd_rn(prog, T.survive), -__fmul_rn(T.ctrl_cost, ctrl));
         bool done = st1 >= T.episode_length;
-        if (T.has_healthy) done = done || x1[2] < T.z_lo || x1[2] > T.z_hi;
+        const float tz = sQ[qword<V>(T.torso, i, 0, 2, LG)];
+        if (T.has_healthy) done = done || tz < T.z_lo || tz > T.z_hi;
         sRst[i] = done ? 1 : 0;
         sSteps[i] = done ? 0 : st1;
         if (done) sEp[i] += 1u;
@@ -419,13 +447,14 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       }
       __syncthreads();
       // auto-reset of done envs (R34): default_qp + noise, Philox counter (env, b, f, episode)
-      const uint2 key = make_uint2(uint32_t(a.seed & 0xffffffffu), uint32_t(a.seed >> 32));
       for (int i = tid; i < E * B; i += blockDim.x) {
         const int env = i / B, b = i - env * B;
         if (!sRst[env]) continue;
         float x[3], q[4], v[3], w[3];
         reset_body(a.dqp, a.masks, B, b, uint32_t(a.env_offset + e0 + env), sEp[env], key, T.noise_vel,
                    T.noise_ang, x, q, v, w);
+        if (T.has_goal && b == T.target)  // R36: the new episode's marker placement
+          place_target(a.dqp, b, T.range, uint32_t(a.env_offset + e0 + env), 2u, sEp[env], key, x);
         for (int k = 0; k < 3; ++k) {
           sQ[qword<V>(b, env, 0, k, LG)] = x[k];
           sQ[qword<V>(b, env, 2, k, LG)] = v[k];

@@ -172,6 +172,12 @@ System* build_host(const Config& cfg) {
     t.z_hi = float(src.z_hi);
     t.noise_vel = float(src.noise_vel);
     t.noise_ang = float(src.noise_ang);
+    t.has_goal = src.has_goal ? 1 : 0;
+    t.obj = src.has_goal ? src.obj : src.torso;  // the body whose start position the epilogue keeps
+    t.target = src.target;
+    t.radius = float(src.radius);
+    t.bonus = float(src.bonus);
+    for (int k = 0; k < 3; ++k) t.range[k] = float(src.range[k]);
   }
 
   std::vector<DBody> bodies(B);

@@ -77,7 +77,7 @@ cudaError_t launch_step_vjp(const System& sys, const StepArgs& primal, const flo
                             float* const g_in[4], float* g_action, cudaStream_t stream);
 cudaError_t launch_reset(const System& sys, float* pos, float* rot, float* vel, float* ang, int64_t n,
                          uint64_t seed, float vel_noise, float ang_noise, cudaStream_t stream,
-                         int64_t env_offset = 0);
+                         int64_t env_offset = 0, bool goal = false);  // goal: brax_env_reset's marker placement (R36)
 
 }  // namespace brax
 

@@ -21,7 +21,7 @@ import paper_2106_13281_b200 as bx  # noqa: E402
 
 TOL = 1e-4
 FIELDS = ("pos", "rot", "vel", "ang")
-ENV_SCENES = ["ant", "humanoid", "halfcheetah"]
+ENV_SCENES = ["ant", "humanoid", "halfcheetah", "grasp", "fetch"]
 _cache = {}
 
 
@@ -55,11 +55,31 @@ def start_states(e, n, seed):
     return qp, steps, episode
 
 
-def near_threshold(e, z):
-    if e.task.healthy_z is None:
-        return np.zeros_like(z, dtype=bool)
-    lo, hi = e.task.healthy_z
-    return (np.abs(z - lo) < TOL) | (np.abs(z - hi) < TOL)
+def near_threshold(e, z, d1=None):
+    """Envs whose fp32 decision (height limits; goal tasks: the marker radius, R36) lies
+    within the step tolerance of its threshold."""
+    out = np.zeros_like(z, dtype=bool)
+    if e.task.healthy_z is not None:
+        lo, hi = e.task.healthy_z
+        out |= (np.abs(z - lo) < TOL) | (np.abs(z - hi) < TOL)
+    if d1 is not None:
+        out |= np.abs(d1 - e.task.goal.radius) < 2 * TOL
+    return out
+
+
+def near_marker(e, qp, seed, frac=0.4):
+    """Goal tasks: put the marker within about the radius of the object in a fraction
+    of the envs, so that hits (bonus + new marker) occur in the step."""
+    g = e.task.goal
+    if g is None:
+        return qp
+    rng = np.random.default_rng(seed)
+    n = qp["pos"].shape[0]
+    m = rng.random(n) < frac
+    d = rng.normal(size=(n, 3))
+    d *= (g.radius * rng.uniform(0.3, 1.3, size=(n, 1))) / np.linalg.norm(d, axis=1, keepdims=True)
+    qp["pos"][m, g.target] = (qp["pos"][m, g.obj] + d[m]).astype(qp["pos"].dtype)
+    return qp
 
 
 @pytest.mark.parametrize("name", ENV_SCENES)
@@ -87,19 +107,25 @@ def test_env_step_matches_oracle(name):
     e, s = scene(name)
     n = 1000
     qp, steps, ep = start_states(e, n, seed=31)
+    qp = near_marker(e, qp, seed=33)
     act = synth.actions(32, 1, n, e.sys.act_dim)[0]
     ref = e.step(qp, steps, ep, act, seed=9, env_offset=50, threads=8)
     st = {"qp": {k: dev(qp[k]) for k in FIELDS}, "steps": dev(steps, torch.int32),
           "episode": dev(ep.view(np.int32), torch.int32)}
     out = s.env_step(st, dev(act), seed=9, env_offset=50)
-    keep = ~ref["ambiguous"] & ~near_threshold(e, ref["x1_z"])
+    keep = ~ref["ambiguous"] & ~near_threshold(e, ref["x1_z"], ref["d1"])
     assert keep.mean() > 0.9
     done = out["done"][0].cpu().numpy().astype(bool)
     assert np.array_equal(done[keep], ref["done"][keep])
     assert ref["done"].sum() >= 0.1 * n  # the truncation envs at least
     assert np.array_equal(st["steps"].cpu().numpy()[keep], ref["steps"][keep])
     assert np.array_equal(st["episode"].cpu().numpy().view(np.uint32)[keep], ref["episode"][keep])
-    tol_r = 2 * TOL * np.linalg.norm(e.task.forward, 1) / e.sys.dt + 1e-5
+    if e.task.goal is None:
+        tol_r = 2 * TOL * np.linalg.norm(e.task.forward, 1) / e.sys.dt + 1e-5
+    else:  # |Δd1| ≤ |Δx'| plus fp32 rounding of the distances (R36)
+        hits = ref["d1"] < e.task.goal.radius
+        assert hits[keep].sum() >= 0.1 * n, hits.sum()
+        tol_r = (2 * TOL + 4e-7 * (1 + np.max(ref["d1"]))) / e.sys.dt + 1e-5
     r = out["reward"][0].cpu().numpy()
     assert np.max(np.abs(r[keep] - ref["reward"][keep])) < tol_r
     for k in FIELDS:
@@ -109,12 +135,14 @@ def test_env_step_matches_oracle(name):
     assert np.max(np.abs(obs[keep] - ref["obs"][keep])) < TOL
 
 
-def test_env_rollout_equals_single_steps_and_plans_agree():
+@pytest.mark.parametrize("name", ["ant", "grasp"])
+def test_env_rollout_equals_single_steps_and_plans_agree(name):
     """T steps in one launch give the same bits as T single-step launches, and
-    every launch plan gives the same bits (auto-resets included)."""
-    e, s = scene("ant")
+    every launch plan gives the same bits (auto-resets and marker hits included)."""
+    e, s = scene(name)
     n = 500
     qp, steps, ep = start_states(e, n, seed=41)
+    qp = near_marker(e, qp, seed=43)
     T = 6
     acts = dev(synth.actions(42, T, n, e.sys.act_dim))
 
@@ -160,7 +188,7 @@ def test_env_errors():
         bx.brax_env_step(s.handle, st["qp"], None, 1, st["qp"], 4, None, None, None, None, None)
 
 
-@pytest.mark.parametrize("name", ["ant", "humanoid", "halfcheetah"])
+@pytest.mark.parametrize("name", ENV_SCENES)
 def test_lean_kernel_env_and_random_actions_bit_identical(name):
     """The lean kernel's env-epilogue and on-device-action paths give brax_step_kernel's bits
     (same device code in the same order) for every plan it applies to."""
