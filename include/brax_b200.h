@@ -305,6 +305,11 @@ brax_status brax_step_vjp(const brax_system *sys, brax_qp in, const float *actio
  * text.  Per step and env, after the last substep and while the bodies are still
  * in shared memory:
  *   reward = ((x'_torso − x_torso)·forward)/dt + survive_reward − ctrl_cost·Σ a²
+ *   (goal tasks, R36 — grasp / fetch: the forward term is
+ *   (|x_O − x_T| − |x'_O − x_T|)/dt + bonus·[|x'_O − x_T| < radius] for the object O and
+ *   the frozen marker body T; a hit moves T to x̄_T + range ⊙ u(env, T, 2 + steps', episode),
+ *   a reset of episode k to x̄_T + range ⊙ u(env, T, 2, k); obs gains x_T − x_O, x_O − x_torso,
+ *   v_O before the contact terms)
  *   done   = torso z' outside healthy_z, or steps + 1 >= episode_length
  *   done envs auto-reset: default_qp + the task's reset noise with Philox counter
  *   (env_offset + env, body, field, episode + 1); steps = 0, episode += 1
@@ -329,7 +334,7 @@ brax_status brax_env_step(const brax_system *sys, brax_qp in, const float *actio
 /* brax_env_step with on-device random actions (NEXT-2; ctrl cost uses them). */
 brax_status brax_env_step_random(const brax_system *sys, brax_qp in, int64_t n_steps, brax_qp out, int64_t n_envs,
                                  const brax_random_actions *ra, const brax_env_io *io, void *stream);
-/* Episode-0 reset (the task's reset noise, Philox counter (env_offset + env, b, f, 0)),
+/* Episode-0 reset (the task's reset noise, Philox counter (env_offset + env, b, f, 0); goal tasks: the marker at x̄_T + range ⊙ u(env, T, 2, 0)),
  * steps = episode = 0, and io->obs (if not NULL). */
 brax_status brax_env_reset(const brax_system *sys, brax_qp out, int64_t n_envs, const brax_env_io *io,
                            void *stream);
