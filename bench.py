@@ -49,6 +49,7 @@ def parse(argv=None):
     p.add_argument("--scene", default="ant")
     p.add_argument("--envs", type=int, default=None, help="envs per GPU")
     p.add_argument("--no-env", action="store_true", help="skip the brax_env_step (NEXT-1) measurement")
+    p.add_argument("--no-rollout", action="store_true", help="skip the fused-rollout (NEXT-2) measurement")
     p.add_argument("--no-vjp", action="store_true", help="skip the brax_step_vjp (NEXT-4) measurement")
     p.add_argument("--no-scenes", action="store_true", help="skip the other scenes' lines")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -483,6 +484,31 @@ def run_b200(args):
                     "steps": Kv, "obs_dim": od,
                     "api": "brax_env_step: physics + reward/done/auto-reset/observation epilogue, one launch"}
 
+    # ---- NEXT-2: T steps of the same workload in ONE launch (brax_rollout_random: the QP
+    # stays in shared memory for all T·S substeps, actions drawn in the kernel), on a copy
+    # of one batch; device-timed like the step
+    roll_line = None
+    if not args.no_rollout:
+        Tr, reps = 100, 3
+        with torch.cuda.stream(stream):
+            rq = {k: v.clone() for k, v in wl.sets[0].items()}
+            system.rollout_random(rq, Tr, seed=rank + 5, env_offset=rank * n, stream=stream)
+            stream.synchronize()
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record(stream)
+            for j in range(reps):
+                system.rollout_random(rq, Tr, seed=rank + 5, env_offset=rank * n, step0=(j + 1) * Tr, stream=stream)
+            r1.record(stream)
+            r1.synchronize()
+        r_ms = bd.allreduce_max(r0.elapsed_time(r1), device=dev)
+        bad = int((~torch.isfinite(rq["pos"]).all(dim=(1, 2))).sum().item())
+        rrf = roofline(load_counts(args.scene), n, (r_ms / 1e3) / (reps * Tr), *load_peaks(), clocks)
+        roll_line = {"value": n * world * reps * Tr / (r_ms / 1e3), "unit": "env-steps/s",
+                     "ms_per_step": r_ms / (reps * Tr), "steps_per_launch": Tr, "launches": reps,
+                     "frac": rrf["frac"], "frac_lean": rrf.get("frac_lean"), "blowups": bad,
+                     "api": "brax_rollout_random: T steps in one launch, actions from the in-kernel Philox stream"}
+        del rq
+
     # ---- NEXT-4: reverse mode of the same step (brax_step_vjp: g_in = Jᵀ·g_out and
     # g_action, one launch) on one batch of the workload; device-timed like the step
     vjp_line = None
@@ -547,7 +573,7 @@ def run_b200(args):
                    "kernel_config": system.launch_config(n),
                    "comm": {"backend": ranks.backend, "nranks": ranks.nranks}},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K, "clocks": clocks,
-        "scenes": scene_lines, "env_epilogue": env_line, "vjp": vjp_line,
+        "scenes": scene_lines, "env_epilogue": env_line, "rollout": roll_line, "vjp": vjp_line,
         "blowups": total_blowups, "substeps_per_s": value * system.substeps,
     }
     print(json.dumps(line), flush=True)

@@ -41,5 +41,7 @@ def test_bench_json_line():
         line = d["scenes"][sc]
         assert line["value"] > 0 and 0.0 < line["frac"] < 1.0 and line["blowups"] == 0, (sc, line)
     assert d["blowups"] == 0
+    roll = d["rollout"]
+    assert roll["value"] > 0 and roll["blowups"] == 0 and 0.0 < roll["frac"] < 1.0
     if d.get("vjp"):
         assert d["vjp"]["value"] > 0 and d["vjp"]["over_step"] > 1.0
