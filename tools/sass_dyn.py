@@ -56,13 +56,18 @@ def main():
     info = {}
     frames = []
     sass = sass_of(a.kernel, "step_lean", "brax_step_lean") if a.lean else sass_of(a.kernel)
+    fresh = True  # nvdisasm -gi writes an inline chain as consecutive //## lines, innermost first
     for line in sass.splitlines():
         if "//## File" in line:
-            frames = re.findall(r'"([^"]+)", line (\d+)', line)
+            if fresh:
+                frames = []
+                fresh = False
+            frames += re.findall(r'"([^"]+)", line (\d+)', line)
             continue
         m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", line)
         if not m:
             continue
+        fresh = True
         sc = [(os.path.basename(f), int(n)) for f, n in frames if os.path.basename(f) in src]
         info[int(m.group(1), 16)] = (sc[-1] if sc else ("?", 0), sc[0] if sc else ("?", 0), m.group(3).split(".")[0])
     rep = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source", "sass"],
