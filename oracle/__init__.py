@@ -10,6 +10,9 @@ Pieces:
   system.py      schema, validation, contact-slot table (R19), default_qp, lint
   philox.py      Philox4x32-10 counter-based generator + brax_reset semantics
   brax_oracle.cpp the step itself (fp64 scalar C++, plus an op-counting twin)
+  env.py         the NEXT-1 env epilogue: observation, reward, done, auto-reset,
+                 goal tasks (R30-R36)
+  diff.py        central finite differences of the step and of rollouts (NEXT-4 checks)
 
 Parity unpinned: whole-scene trajectories of ant/humanoid/halfcheetah/grasp/
 fetch have no closed form; they are pinned only by the invariants in
