@@ -67,7 +67,8 @@ class Ranks:
 
 def init_ranks(backend: str) -> Ranks:
     """Read RANK / WORLD_SIZE / LOCAL_RANK (torchrun), bind the local GPU for "nccl", and
-    create the process group for world > 1.  Logs the communicator size to stderr."""
+    create the process group for world > 1 or any torchrun launch (a one-rank communicator
+    at N = 1, so the launcher's path is the one exercised).  Logs the communicator size."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -75,7 +76,7 @@ def init_ranks(backend: str) -> Ranks:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if backend == "nccl":
         torch.cuda.set_device(local)
-    if world == 1:
+    if world == 1 and "TORCHELASTIC_RUN_ID" not in os.environ:
         return Ranks(rank, 1, local, None, 1)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     if backend == "nccl":
@@ -90,7 +91,7 @@ def init_ranks(backend: str) -> Ranks:
 
 
 def barrier(r: Ranks) -> None:
-    if r.world > 1:
+    if r.backend is not None:
         import torch.distributed as dist
         dist.barrier()
 
@@ -103,7 +104,7 @@ def allreduce_stats(env_steps: float, blowups: float, elapsed_ms: float, return_
     import torch.distributed as dist
     s = torch.tensor([env_steps, blowups, return_sum], dtype=torch.float64, device=device)
     m = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
     return float(s[0]), float(s[1]), float(s[2]), float(m[0])
@@ -115,6 +116,6 @@ def allreduce_max(x: float, device=None) -> float:
 
 
 def finalize(r: Ranks) -> None:
-    if r.world > 1:
+    if r.backend is not None:
         import torch.distributed as dist
         dist.destroy_process_group()

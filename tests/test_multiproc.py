@@ -108,3 +108,21 @@ def test_bench_gpus2_starts_two_ranks_and_reduces_stats():
 def test_bench_rejects_a_world_size_mismatch():
     r = _bench(["--gpus", "2", "--dist-selftest"], env={"WORLD_SIZE": "3", "RANK": "0", "LOCAL_RANK": "0"})
     assert r.returncode != 0 and "WORLD_SIZE=3" in (r.stderr + r.stdout)
+
+
+def test_torchrun_one_rank_builds_a_communicator():
+    """Under the driver's launcher at N = 1 (torch.distributed.run, WORLD_SIZE = 1) the rank
+    still builds its one-rank communicator and reduces through it (the launcher's path)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                        "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(root, "bench.py"),
+                        "--gpus", "1", "--dist-selftest"], capture_output=True, text=True, env=e, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["n_gpus"] == 1 and d["nranks"] == 1 and d["backend"] == "gloo"
+    assert d["env_steps"] == 100.0 and d["ms_max"] == 10.0
+    assert "gloo communicator: nranks=1" in r.stderr
