@@ -29,6 +29,11 @@ constexpr int kEnvsPerBlock = 32;  // lane = env; warp = work item
 // shared memory (the tracing sums)
 constexpr int kMaxDynSmem = 227 * 1024 - 128;
 constexpr int kMaxWarps = 16;      // 512 threads per block at most
+// Cross-launch env-granule dependencies of the lean kernel (DESIGN.md §5 "Launch
+// overlap"): per granule of kGranule envs, how many launches have started on it and
+// how many have finished; kMaxGranules granules per system (2^22 envs).
+constexpr int kGranule = 8;
+constexpr int kMaxGranules = 1 << 19;
 
 // Flag bits (precomputed on the host; warp-uniform tests in the kernel).  An
 // exact-zero offset, identity frame, isotropic inertia or all-free mask makes the

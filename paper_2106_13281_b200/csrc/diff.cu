@@ -64,6 +64,7 @@ cudaError_t launch_step_vjp(const System& sys, const StepArgs& primal, const flo
                             float* const g_in[4], float* g_action, cudaStream_t stream) {
   const int64_t n = primal.n_envs;
   if (n <= 0) return cudaSuccess;
+  note_other_launch(sys, stream);
   const int B = sys.hd.B, A = sys.hd.A;
   const int64_t qf = n * B * 13, K = int64_t(13) * B + A;
   float* buf = nullptr;

@@ -41,6 +41,7 @@ cudaError_t launch_reset(const System& sys, float* pos, float* rot, float* vel, 
                          uint64_t seed, float vel_noise, float ang_noise, cudaStream_t stream, int64_t env_offset,
                          bool goal) {
   if (n <= 0) return cudaSuccess;
+  note_other_launch(sys, stream);
   const int B = sys.hd.B;
   int64_t total = n * B;
   unsigned blocks = unsigned((total + 255) / 256);

@@ -585,6 +585,8 @@ cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, 
 }
 
 cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs, bool fixed, cudaStream_t stream) {
+  auto order = launch_order_lock();
+  note_other_launch(sys, stream);  // triggers its dependents early without the granule protocol
   KArgs ka{a, sys.d_blob, sys.hd, plan};
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
@@ -788,6 +790,8 @@ cudaError_t launch_step_jvp(const System& sys, const StepArgs& a, cudaStream_t s
   DPlan P = sys.hd.plan[p];
   if (P.smem_bytes_jvp > kMaxDynSmem) return cudaErrorInvalidValue;
   P.smem_bytes = P.smem_bytes_jvp;
+  auto order = launch_order_lock();
+  note_other_launch(sys, stream);
   KArgs ka{a, sys.d_blob, sys.hd, p};
   ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
   ka.a.phase_cycles = nullptr;

@@ -1051,6 +1051,18 @@ __device__ __forceinline__ void tma_store_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// waits until the bulk stores have WRITTEN global memory (a later launch may read them
+// before this grid completes: the lean kernel's granule protocol)
+__device__ __forceinline__ void tma_store_commit_wait_all() {
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+}
+// orders this thread's generic-proxy accesses with async-proxy (TMA) accesses to global memory
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // Staging area layout (words): the block's contiguous global chunks
 // pos [E][B][3] | rot [E][B][4] | vel [E][B][3] | ang [E][B][3].  Full blocks only.

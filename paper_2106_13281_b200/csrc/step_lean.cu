@@ -19,6 +19,10 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "device_rng.cuh"
 #include "step_device.cuh"
@@ -35,6 +39,11 @@ struct LeanArgs {
   DHeader hd;
   int32_t plan;
   SmemLayout L;
+  // launch overlap: per env granule, launches started (gs) / finished (gd)
+  uint32_t* gs;
+  uint32_t* gd;
+  int32_t reg;       // this launch registers on the granule counters
+  int32_t overlap;   // skip griddepcontrol.wait: wait for the granules' earlier launches instead
 };
 
 // item classes (warp-uniform: the items sharing a warp step share a class)
@@ -104,8 +113,25 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
     mbar_expect_tx(&bars[0], uint32_t(H.blob_words) * 4u + (bulk ? qp_bytes : 0u));
     tma_load(sBlob, ka.blob, uint32_t(H.blob_words) * 4u, &bars[0]);
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the QP may be the previous kernel's output
+  // The QP may be the previous launch's output.  Default: PDL's grid-wide wait.  Overlapped
+  // launches (host-checked: the previous kernel on this stream was a lean launch of this
+  // system whose buffers are this launch's, env for env, or disjoint from them): register as
+  // the next launch of each of the block's env granules, let the next launch be scheduled,
+  // and wait only until every earlier launch on these granules has finished.
+  if (!ka.overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int g0 = int(e0 / kGranule), ng = (nvalid + kGranule - 1) / kGranule;
+  uint32_t gprev = 0;
+  if (ka.reg && tid < ng) gprev = atomicAdd(ka.gs + g0 + tid, 1u);
+  if (ka.reg) __syncthreads();  // every registration performed before the trigger
   asm volatile("griddepcontrol.launch_dependents;");
+  if (ka.reg) {
+#ifndef BRAX_OVERLAP_NO_SPIN  // (negative control for tests/test_gpu_overlap.py only: races on purpose)
+    if (tid < ng)
+      while (int32_t(ld_acquire_gpu(ka.gd + g0 + tid) - gprev) < 0) __nanosleep(64);
+#endif
+    __syncthreads();
+    if (tid == 0) fence_proxy_async_global();  // the TMA loads below read what the acquire made visible
+  }
 #ifdef BRAX_DIAG
   if (dgb) tl[1] = gtime();
 #endif
@@ -437,7 +463,8 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
       tma_store(a.rot_out + e0 * B * 4, sr, uint32_t(E * B) * 16u);
       tma_store(a.vel_out + e0 * B * 3, sv, uint32_t(E * B) * 12u);
       tma_store(a.ang_out + e0 * B * 3, sw, uint32_t(E * B) * 12u);
-      tma_store_commit_wait();
+      if (ka.reg) tma_store_commit_wait_all();  // written, not just read: a later launch may run now
+      else tma_store_commit_wait();
 #ifdef BRAX_DIAG
       if (dgb) {
         tl[4] = gtime();
@@ -454,6 +481,14 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   if (a.status) {
     __syncthreads();
     for (int i = tid; i < nvalid; i += blockDim.x) a.status[e0 + i] = sStat[i];
+  }
+  if (ka.reg) {  // this launch is done with its granules: release them to the next launch
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async_global();
+      __threadfence();
+      for (int k = 0; k < ng; ++k) atomicAdd(ka.gd + g0 + k, 1u);
+    }
   }
 }
 
@@ -485,7 +520,98 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
   return cudaLaunchKernelEx(&cfg, brax_step_lean<S, G, R, kEnv>, ka);
 }
 
+// ---- launch-order bookkeeping for overlapped launches (DESIGN.md §5 "Launch overlap") ----
+// Per (device, stream): the window of lean launches that may still be in flight — every
+// launch since the last one that waited for its predecessor in full (griddepcontrol.wait).
+// A launch may skip that wait only if the stream's last kernel is the window's last member,
+// it belongs to the same system and batch size, and every buffer it touches is, for every
+// window member, either disjoint from that member's buffers or the same array of the same
+// field (env i <-> env i): then the per-granule counters order every dependency, and a
+// later full-waiting launch that waits for the window's last member waits, transitively
+// through the granule counters, for all of them.  Kernels of other code on the stream do
+// not trigger their dependents early, so they serialise as usual; this library's other
+// kernels reset the window (note_other_launch).
+struct Span {
+  uintptr_t lo, hi;
+  int kind;
+  bool operator==(const Span& o) const { return lo == o.lo && hi == o.hi && kind == o.kind; }
+};
+struct LaunchRecord {
+  std::vector<Span> reads, writes;
+  bool operator==(const LaunchRecord& o) const { return reads == o.reads && writes == o.writes; }
+};
+struct StreamWindow {
+  const System* sys = nullptr;
+  int64_t n = -1;
+  bool valid = false;               // the stream's last kernel is the window's last member
+  std::vector<LaunchRecord> members;  // distinct buffer sets of the launches in the window
+};
+constexpr size_t kMaxWindow = 64;
+std::recursive_mutex g_track_mu;  // held across each launch: recorded order = stream order
+std::map<std::pair<int, cudaStream_t>, StreamWindow> g_track;
+
+void spans_of(const System& sys, const StepArgs& a, std::vector<Span>& rd, std::vector<Span>& wr) {
+  const int64_t n = a.n_envs, B = sys.hd.B, T = a.n_steps > 0 ? a.n_steps : 1;
+  auto add = [](std::vector<Span>& v, const void* p, int64_t bytes, int kind) {
+    if (p && bytes > 0) v.push_back({reinterpret_cast<uintptr_t>(p), reinterpret_cast<uintptr_t>(p) + uintptr_t(bytes), kind});
+  };
+  const int w[4] = {3, 4, 3, 3};
+  const void* in[4] = {a.pos_in, a.rot_in, a.vel_in, a.ang_in};
+  const void* out[4] = {a.pos_out, a.rot_out, a.vel_out, a.ang_out};
+  for (int f = 0; f < 4; ++f) {
+    add(rd, in[f], n * B * w[f] * 4, f);
+    add(wr, out[f], n * B * w[f] * 4, f);
+  }
+  add(rd, a.actions, T * n * sys.hd.A * 4, 4);
+  add(wr, a.status, n * 4, 5);
+  add(wr, a.contact_active, n * sys.hd.C, 6);
+  if (a.env) {
+    add(rd, a.steps, n * 4, 7);
+    add(wr, a.steps, n * 4, 7);
+    add(rd, a.episode, n * 4, 8);
+    add(wr, a.episode, n * 4, 8);
+    add(wr, a.obs, T * n * sys.hd.task.obs_dim * 4, 9);
+    add(wr, a.reward, T * n * 4, 10);
+    add(wr, a.done, T * n, 11);
+  }
+}
+
+bool compatible(const LaunchRecord& cur, const LaunchRecord& prev) {
+  auto ok = [](const Span& x, const Span& y) {
+    return x.hi <= y.lo || y.hi <= x.lo || (x.lo == y.lo && x.hi == y.hi && x.kind == y.kind);
+  };
+  for (const Span& y : prev.writes) {
+    for (const Span& x : cur.reads)
+      if (!ok(x, y)) return false;
+    for (const Span& x : cur.writes)
+      if (!ok(x, y)) return false;
+  }
+  for (const Span& y : prev.reads)
+    for (const Span& x : cur.writes)
+      if (!ok(x, y)) return false;
+  return true;
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
 }  // namespace
+
+std::unique_lock<std::recursive_mutex> launch_order_lock() { return std::unique_lock<std::recursive_mutex>(g_track_mu); }
+
+void note_other_launch(const System&, cudaStream_t stream) {
+  std::lock_guard<std::recursive_mutex> g(g_track_mu);
+  g_track[{current_device(), stream}] = StreamWindow{};
+}
+
+void forget_system(const System* sys) {
+  std::lock_guard<std::recursive_mutex> g(g_track_mu);
+  for (auto it = g_track.begin(); it != g_track.end();)
+    it = it->second.sys == sys ? g_track.erase(it) : std::next(it);
+}
 
 bool lean_applies(const System& sys, int plan, const StepArgs& a) {
   const DPlan& P = sys.hd.plan[plan];
@@ -496,21 +622,10 @@ bool lean_applies(const System& sys, int plan, const StepArgs& a) {
   return (a.env ? P.smem_bytes_env : P.smem_bytes) <= kMaxDynSmem;
 }
 
-cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream) {
-  const DPlan& P = sys.hd.plan[plan];
-  const DHeader& H = sys.hd;
-  LeanArgs ka{a, sys.d_blob, sys.hd, plan, {}};
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
-                 al16(a.rot_out) && al16(a.vel_out) && al16(a.ang_out);
-  ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * H.A) % 4 == 0);
-  if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
-  if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
-  ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, P.V == 2 ? 1 : 0, H.blob_words,
-                     a.env ? H.task.obs_dim : 0, a.env ? H.task.contact_obs : 0, 0);
-  dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
-  const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);
-  if (a.env) {  // env-epilogue instantiations (register budgets 128 / 96)
+namespace {
+cudaError_t dispatch_lean(const LeanArgs& ka, const DPlan& P, bool env, int regs, dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t stream) {
+  if (env) {  // env-epilogue instantiations (register budgets 128 / 96)
     if (P.V == 2) {
       if (P.G == 2) {
         if (regs >= 128) return launch_lean_variant<F2, 2, 128, true>(ka, grid, block, smem, stream);
@@ -550,6 +665,55 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   if (regs >= 128) return launch_lean_variant<F1, 4, 128>(ka, grid, block, smem, stream);
   if (regs >= 96) return launch_lean_variant<F1, 4, 96>(ka, grid, block, smem, stream);
   return launch_lean_variant<F1, 4, 64>(ka, grid, block, smem, stream);
+}
+}  // namespace
+
+cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs, cudaStream_t stream) {
+  const DPlan& P = sys.hd.plan[plan];
+  const DHeader& H = sys.hd;
+  LeanArgs ka{a, sys.d_blob, sys.hd, plan, {}};
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
+                 al16(a.rot_out) && al16(a.vel_out) && al16(a.ang_out);
+  ka.a.act_bulk_ok = a.actions && al16(a.actions) && ((a.n_envs * H.A) % 4 == 0);
+  if (std::getenv("BRAX_NO_BULK")) ka.a.bulk_ok = ka.a.act_bulk_ok = 0;
+  if (const char* e = std::getenv("BRAX_DIAG_BLOCK")) ka.a.diag_block = std::atoi(e);
+  ka.L = smem_layout(H.B, H.J, H.C, H.A, P.E, 32 / P.G, P.V == 2 ? 1 : 0, H.blob_words,
+                     a.env ? H.task.obs_dim : 0, a.env ? H.task.contact_obs : 0, 0);
+  dim3 grid(unsigned((a.n_envs + P.E - 1) / P.E)), block(unsigned(P.W * 32));
+  const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);
+  // granule registration and launch overlap (DESIGN.md §5 "Launch overlap"); the record and
+  // the launch happen under one lock, so the recorded order is the stream order
+  LaunchRecord cur;
+  spans_of(sys, a, cur.reads, cur.writes);
+  const bool reg = sys.d_gran != nullptr && a.n_envs <= int64_t(kMaxGranules) * kGranule;
+  const bool no_overlap = std::getenv("BRAX_NO_OVERLAP") != nullptr;
+  std::lock_guard<std::recursive_mutex> g(g_track_mu);
+  StreamWindow& w = g_track[{current_device(), stream}];
+  bool overlap = reg && !no_overlap && w.valid && w.sys == &sys && w.n == a.n_envs;
+  bool known = false;
+  for (size_t i = 0; overlap && i < w.members.size(); ++i) {
+    overlap = compatible(cur, w.members[i]);
+    known = known || cur == w.members[i];
+  }
+  if (overlap && !known && w.members.size() >= kMaxWindow) overlap = false;  // start a new window
+  ka.gs = sys.d_gran;
+  ka.gd = sys.d_gran + kMaxGranules;
+  ka.reg = reg ? 1 : 0;
+  ka.overlap = overlap ? 1 : 0;
+  const cudaError_t e = dispatch_lean(ka, P, a.env != 0, regs, grid, block, smem, stream);
+  if (e != cudaSuccess) {
+    w = StreamWindow{};  // nothing known about the stream's last kernel: the next launch waits in full
+  } else if (overlap) {
+    if (!known) w.members.push_back(std::move(cur));
+  } else {  // this launch waited in full: it opens the window
+    w = StreamWindow{};
+    w.sys = &sys;
+    w.n = a.n_envs;
+    w.valid = reg;
+    w.members.push_back(std::move(cur));
+  }
+  return e;
 }
 
 }  // namespace brax

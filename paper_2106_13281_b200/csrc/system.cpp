@@ -56,10 +56,12 @@ void cuda_check(cudaError_t e, const char* what) {
 }  // namespace
 
 System::~System() {
+  forget_system(this);
   if (d_blob) cudaFree(d_blob);
   if (d_default_qp) cudaFree(d_default_qp);
   if (d_masks) cudaFree(d_masks);
   if (d_phase_cycles) cudaFree(d_phase_cycles);
+  if (d_gran) cudaFree(d_gran);
 }
 
 void default_qp(const Config& cfg, std::vector<double>& pos, std::vector<double>& rot) {
@@ -507,6 +509,8 @@ System* build_system(const Config& cfg, int device) {
   }
   cuda_check(cudaMalloc(&s->d_phase_cycles, 4 * sizeof(unsigned long long)), "cudaMalloc(phase_cycles)");
   cuda_check(cudaMemset(s->d_phase_cycles, 0, 4 * sizeof(unsigned long long)), "cudaMemset");
+  cuda_check(cudaMalloc(&s->d_gran, 2 * size_t(kMaxGranules) * 4), "cudaMalloc(granule counters)");
+  cuda_check(cudaMemset(s->d_gran, 0, 2 * size_t(kMaxGranules) * 4), "cudaMemset(granule counters)");
   cuda_check(cudaMalloc(&s->d_masks, s->d_masks_host.size() * 4), "cudaMalloc(masks)");
   cuda_check(cudaMemcpy(s->d_masks, s->d_masks_host.data(), s->d_masks_host.size() * 4, cudaMemcpyHostToDevice),
              "cudaMemcpy(masks)");

@@ -36,6 +36,7 @@ struct System {
   int num_sms = 0;                     // of `device` (launch heuristics)
   bool trace = false;                  // per-phase cycle tracing (brax_system_set_tracing)
   unsigned long long* d_phase_cycles = nullptr;  // device [4]
+  uint32_t* d_gran = nullptr;          // device [2][kMaxGranules]: launches started / finished per env granule
   size_t smem_bytes = 0;
   bool lean_plan_ok[kNumPlans] = {};   // plan gives every warp at most one item step and one body step
   // launch configuration per batch size, measured by brax_system_tune
@@ -75,6 +76,14 @@ cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, con
 // The same from the JVP columns (diff.cu), 13B + A JVP launches: the cross-check.
 cudaError_t launch_step_vjp(const System& sys, const StepArgs& primal, const float* const g_out[4],
                             float* const g_in[4], float* g_action, cudaStream_t stream);
+// Launch-order bookkeeping for the lean kernel's overlapped launches (step_lean.cu):
+// every kernel launch on `stream` that is not a lean step launch records itself here,
+// so the next lean launch waits for it in full (griddepcontrol.wait).
+void note_other_launch(const System& sys, cudaStream_t stream);
+// Held across a launch that calls note_other_launch, so the record order is the stream order.
+std::unique_lock<std::recursive_mutex> launch_order_lock();
+// Drops the records of a system being destroyed.
+void forget_system(const System* sys);
 cudaError_t launch_reset(const System& sys, float* pos, float* rot, float* vel, float* ang, int64_t n,
                          uint64_t seed, float vel_noise, float ang_noise, cudaStream_t stream,
                          int64_t env_offset = 0, bool goal = false);  // goal: brax_env_reset's marker placement (R36)

@@ -855,6 +855,7 @@ cudaError_t launch_step_vjp_fused(const System& sys, const StepArgs& primal, con
                                   float* const g_in[4], float* g_action, cudaStream_t stream) {
   const int64_t n = primal.n_envs;
   if (n <= 0) return cudaSuccess;
+  note_other_launch(sys, stream);
   const DHeader& H = sys.hd;
   int p = -1;  // the largest one-env-per-lane block whose layout fits
   for (int q : {0, 1, 2}) {
