@@ -569,7 +569,8 @@ def run_b200(args):
                    "l2": f"inputs larger than L2: {wl.R} rotating batches x {2 * wl.qp_bytes / 1e6:.1f} MB "
                          f"(> 126 MB L2)",
                    "launch": f"one CUDA graph of exactly {K} brax_step launches, replayed once untimed, "
-                             f"then timed",
+                             f"then timed; consecutive launches overlap, ordered per env granule "
+                             f"(DESIGN.md §5 'Launch overlap')",
                    "kernel_config": system.launch_config(n),
                    "comm": {"backend": ranks.backend, "nranks": ranks.nranks}},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K, "clocks": clocks,
