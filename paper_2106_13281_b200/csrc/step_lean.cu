@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -548,7 +549,23 @@ struct StreamWindow {
 };
 constexpr size_t kMaxWindow = 64;
 std::recursive_mutex g_track_mu;  // held across each launch: recorded order = stream order
-std::map<std::pair<int, cudaStream_t>, StreamWindow> g_track;
+// keyed by (device, stream, capture sequence id or 0): a stream capture tracks its own
+// launch order (its first node has no in-graph predecessor; the graph launch serialises
+// with the stream's earlier work) and leaves the stream's eager record alone
+using TrackKey = std::tuple<int, cudaStream_t, unsigned long long>;
+std::map<TrackKey, StreamWindow> g_track;
+
+TrackKey track_key(cudaStream_t stream) {
+  int d = 0;
+  cudaGetDevice(&d);
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(stream, &st, &id) != cudaSuccess) {
+    cudaGetLastError();
+    id = 0;
+  }
+  return TrackKey{d, stream, st == cudaStreamCaptureStatusActive ? id : 0ull};
+}
 
 void spans_of(const System& sys, const StepArgs& a, std::vector<Span>& rd, std::vector<Span>& wr) {
   const int64_t n = a.n_envs, B = sys.hd.B, T = a.n_steps > 0 ? a.n_steps : 1;
@@ -592,19 +609,13 @@ bool compatible(const LaunchRecord& cur, const LaunchRecord& prev) {
   return true;
 }
 
-int current_device() {
-  int d = 0;
-  cudaGetDevice(&d);
-  return d;
-}
-
 }  // namespace
 
 std::unique_lock<std::recursive_mutex> launch_order_lock() { return std::unique_lock<std::recursive_mutex>(g_track_mu); }
 
 void note_other_launch(const System&, cudaStream_t stream) {
   std::lock_guard<std::recursive_mutex> g(g_track_mu);
-  g_track[{current_device(), stream}] = StreamWindow{};
+  g_track[track_key(stream)] = StreamWindow{};
 }
 
 void forget_system(const System* sys) {
@@ -689,7 +700,7 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   const bool reg = sys.d_gran != nullptr && a.n_envs <= int64_t(kMaxGranules) * kGranule;
   const bool no_overlap = std::getenv("BRAX_NO_OVERLAP") != nullptr;
   std::lock_guard<std::recursive_mutex> g(g_track_mu);
-  StreamWindow& w = g_track[{current_device(), stream}];
+  StreamWindow& w = g_track[track_key(stream)];
   bool overlap = reg && !no_overlap && w.valid && w.sys == &sys && w.n == a.n_envs;
   bool known = false;
   for (size_t i = 0; overlap && i < w.members.size(); ++i) {

@@ -201,3 +201,36 @@ def test_env_chain_matches_serialised_launches():
     for x, y in zip(oa, ob):
         for key in ("obs", "reward", "done"):
             assert torch.equal(x[key], y[key]), key
+
+
+def test_eager_launches_right_after_a_graph_replay():
+    """A replayed graph of in-place launches, then eager launches on the same buffers and
+    stream with no synchronisation: the eager launches' record predates the capture (a
+    capture tracks its own order), and the graph launch serialises with them."""
+    o = oracle.Oracle(oracle.load_scene("ant"))
+    s = bx.System(oracle.load_scene("ant"))
+    n = 8192
+    q0 = start(o, n, 31)
+    acts = torch.from_numpy(synth.actions(32, 16, n, o.act_dim)).cuda()
+    X = clone(q0)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        s.step(X, acts[0], X)  # the stream's eager record: an in-place launch on X
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for t in range(1, 9):
+            s.step(X, acts[t], X)
+    for k in FIELDS:
+        X[k].copy_(q0[k])
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        s.step(X, acts[0], X)
+        g.replay()
+        for t in range(9, 16):
+            s.step(X, acts[t], X)
+    torch.cuda.synchronize()
+    R = clone(q0)
+    run(s, [lambda s, t=t: s.step(R, acts[t], R) for t in range(16)], sync=True)
+    for k in FIELDS:
+        assert torch.equal(X[k], R[k]), k
