@@ -48,6 +48,11 @@ struct KArgs {
   const uint32_t* blob;
   DHeader hd;
   int32_t plan;  // index into hd.plan (G = 1 << plan lane groups per warp)
+  // launch overlap (as in step_lean.cu): env-granule counters
+  uint32_t* gs;
+  uint32_t* gd;
+  int32_t reg;
+  int32_t overlap;
 };
 
 // Register budget: 80 per thread keeps 2 blocks of up to 12 warps resident per SM.
@@ -136,9 +141,20 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
     tma_load(sBlob, ka.blob, uint32_t(H.blob_words) * 4u, &bars[0]);
   }
   // programmatic dependent launch: everything above overlapped the previous kernel's
-  // tail; the QP and actions may be its outputs, so wait for it to complete here
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // tail; the QP and actions may be its outputs, so wait for it to complete here — or,
+  // for an overlapped launch, only for the earlier launches on this block's env granules
+  if (!ka.overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int g0 = int(e0 / kGranule), ng = (nvalid + kGranule - 1) / kGranule;
+  uint32_t gprev = 0;
+  if (ka.reg && tid < ng) gprev = atomicAdd(ka.gs + g0 + tid, 1u);
+  if (ka.reg) __syncthreads();  // every registration performed before the trigger
   asm volatile("griddepcontrol.launch_dependents;");
+  if (ka.reg) {
+    if (tid < ng)
+      while (int32_t(ld_acquire_gpu(ka.gd + g0 + tid) - gprev) < 0) __nanosleep(64);
+    __syncthreads();
+    if (tid == 0) fence_proxy_async_global();
+  }
   if (tid == 0) {
     if (bulk) {
       float* sp = stg;
@@ -238,6 +254,10 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
 
   if (envm && a.n_steps == 0) {  // observe only (brax_env_observe / brax_env_reset): QP not written
     observe(a.obs + e0 * od);
+    if (ka.reg && tid == 0) {  // (the host does not register these launches; never leave a granule open)
+      __threadfence();
+      for (int k = 0; k < ng; ++k) atomicAdd(ka.gd + g0 + k, 1u);
+    }
     return;
   }
   // S2 of the first substep; every later S2 is fused into the previous substep's integrate()
@@ -496,7 +516,8 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
       tma_store(a.rot_out + e0 * B * 4, sr, uint32_t(E * B) * 16u);
       tma_store(a.vel_out + e0 * B * 3, sv, uint32_t(E * B) * 12u);
       tma_store(a.ang_out + e0 * B * 3, sw, uint32_t(E * B) * 12u);
-      tma_store_commit_wait();
+      if (ka.reg) tma_store_commit_wait_all();
+      else tma_store_commit_wait();
     }
   } else if constexpr (kJvp) {
     store_block_d(a, sQ, B, E, e0, nvalid);
@@ -510,6 +531,14 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   if (trace) {
     lap(3);
     for (int k = 0; k < 4; ++k) atomicAdd(&a.phase_cycles[k], (unsigned long long)sTr[k]);
+  }
+  if (ka.reg) {  // release this block's granules to the next launch
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async_global();
+      __threadfence();
+      for (int k = 0; k < ng; ++k) atomicAdd(ka.gd + g0 + k, 1u);
+    }
   }
 }
 
@@ -584,10 +613,21 @@ cudaError_t launch_variant(const KArgs& ka, dim3 grid, dim3 block, size_t smem, 
   return cudaLaunchKernelEx(&cfg, brax_step_kernel<S, R, kEnv, kFixed>, ka);
 }
 
+cudaError_t launch_with_args(const System& sys, KArgs& ka, int regs, bool fixed, cudaStream_t stream);
+
 cudaError_t launch_with(const System& sys, const StepArgs& a, int plan, int regs, bool fixed, cudaStream_t stream) {
-  auto order = launch_order_lock();
-  note_other_launch(sys, stream);  // triggers its dependents early without the granule protocol
-  KArgs ka{a, sys.d_blob, sys.hd, plan};
+  auto order = launch_order_lock();  // held across the launch: recorded order = stream order
+  // observe-only env launches return early and do not take part in the granule protocol
+  const OverlapDecision d = overlap_decide(sys, a, stream, !(a.env && a.n_steps == 0));
+  KArgs ka{a, sys.d_blob, sys.hd, plan, sys.d_gran, sys.d_gran + kMaxGranules, d.reg ? 1 : 0, d.overlap ? 1 : 0};
+  const cudaError_t e = launch_with_args(sys, ka, regs, fixed, stream);
+  overlap_commit(sys, a, stream, d, e);
+  return e;
+}
+
+cudaError_t launch_with_args(const System& sys, KArgs& ka, int regs, bool fixed, cudaStream_t stream) {
+  const StepArgs& a = ka.a;
+  const int plan = ka.plan;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   ka.a.bulk_ok = al16(a.pos_in) && al16(a.rot_in) && al16(a.vel_in) && al16(a.ang_in) && al16(a.pos_out) &&
                  al16(a.rot_out) && al16(a.vel_out) && al16(a.ang_out);

@@ -582,6 +582,7 @@ void spans_of(const System& sys, const StepArgs& a, std::vector<Span>& rd, std::
   add(rd, a.actions, T * n * sys.hd.A * 4, 4);
   add(wr, a.status, n * 4, 5);
   add(wr, a.contact_active, n * sys.hd.C, 6);
+  add(wr, a.contact_dp, n * B * 6 * 4, 12);
   if (a.env) {
     add(rd, a.steps, n * 4, 7);
     add(wr, a.steps, n * 4, 7);
@@ -612,6 +613,48 @@ bool compatible(const LaunchRecord& cur, const LaunchRecord& prev) {
 }  // namespace
 
 std::unique_lock<std::recursive_mutex> launch_order_lock() { return std::unique_lock<std::recursive_mutex>(g_track_mu); }
+
+OverlapDecision overlap_decide(const System& sys, const StepArgs& a, cudaStream_t stream, bool participant) {
+  std::lock_guard<std::recursive_mutex> g(g_track_mu);
+  OverlapDecision d;
+  d.reg = participant && sys.d_gran != nullptr && a.n_envs <= int64_t(kMaxGranules) * kGranule;
+  if (!d.reg || std::getenv("BRAX_NO_OVERLAP")) return d;
+  const StreamWindow& w = g_track[track_key(stream)];
+  if (!w.valid || w.sys != &sys || w.n != a.n_envs) return d;
+  LaunchRecord cur;
+  spans_of(sys, a, cur.reads, cur.writes);
+  bool known = false;
+  for (const LaunchRecord& m : w.members) {
+    if (!compatible(cur, m)) return d;
+    known = known || cur == m;
+  }
+  if (!known && w.members.size() >= kMaxWindow) return d;  // start a new window
+  d.overlap = true;
+  return d;
+}
+
+void overlap_commit(const System& sys, const StepArgs& a, cudaStream_t stream, const OverlapDecision& d,
+                    cudaError_t launched) {
+  std::lock_guard<std::recursive_mutex> g(g_track_mu);
+  StreamWindow& w = g_track[track_key(stream)];
+  if (launched != cudaSuccess || !d.reg) {  // nothing to order by counters: the next launch waits in full
+    w = StreamWindow{};
+    return;
+  }
+  LaunchRecord cur;
+  spans_of(sys, a, cur.reads, cur.writes);
+  if (d.overlap) {
+    for (const LaunchRecord& m : w.members)
+      if (cur == m) return;
+    w.members.push_back(std::move(cur));
+    return;
+  }
+  w = StreamWindow{};  // this launch waited in full: it opens the window
+  w.sys = &sys;
+  w.n = a.n_envs;
+  w.valid = true;
+  w.members.push_back(std::move(cur));
+}
 
 void note_other_launch(const System&, cudaStream_t stream) {
   std::lock_guard<std::recursive_mutex> g(g_track_mu);
@@ -695,35 +738,14 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   const size_t smem = size_t(a.env ? P.smem_bytes_env : P.smem_bytes);
   // granule registration and launch overlap (DESIGN.md §5 "Launch overlap"); the record and
   // the launch happen under one lock, so the recorded order is the stream order
-  LaunchRecord cur;
-  spans_of(sys, a, cur.reads, cur.writes);
-  const bool reg = sys.d_gran != nullptr && a.n_envs <= int64_t(kMaxGranules) * kGranule;
-  const bool no_overlap = std::getenv("BRAX_NO_OVERLAP") != nullptr;
-  std::lock_guard<std::recursive_mutex> g(g_track_mu);
-  StreamWindow& w = g_track[track_key(stream)];
-  bool overlap = reg && !no_overlap && w.valid && w.sys == &sys && w.n == a.n_envs;
-  bool known = false;
-  for (size_t i = 0; overlap && i < w.members.size(); ++i) {
-    overlap = compatible(cur, w.members[i]);
-    known = known || cur == w.members[i];
-  }
-  if (overlap && !known && w.members.size() >= kMaxWindow) overlap = false;  // start a new window
+  auto order = launch_order_lock();
+  const OverlapDecision d = overlap_decide(sys, a, stream, true);
   ka.gs = sys.d_gran;
   ka.gd = sys.d_gran + kMaxGranules;
-  ka.reg = reg ? 1 : 0;
-  ka.overlap = overlap ? 1 : 0;
+  ka.reg = d.reg ? 1 : 0;
+  ka.overlap = d.overlap ? 1 : 0;
   const cudaError_t e = dispatch_lean(ka, P, a.env != 0, regs, grid, block, smem, stream);
-  if (e != cudaSuccess) {
-    w = StreamWindow{};  // nothing known about the stream's last kernel: the next launch waits in full
-  } else if (overlap) {
-    if (!known) w.members.push_back(std::move(cur));
-  } else {  // this launch waited in full: it opens the window
-    w = StreamWindow{};
-    w.sys = &sys;
-    w.n = a.n_envs;
-    w.valid = reg;
-    w.members.push_back(std::move(cur));
-  }
+  overlap_commit(sys, a, stream, d, e);
   return e;
 }
 

@@ -82,6 +82,16 @@ cudaError_t launch_step_vjp(const System& sys, const StepArgs& primal, const flo
 void note_other_launch(const System& sys, cudaStream_t stream);
 // Held across a launch that calls note_other_launch, so the record order is the stream order.
 std::unique_lock<std::recursive_mutex> launch_order_lock();
+// Launch overlap (step_lean.cu): under launch_order_lock(), whether a step
+// launch registers on the env-granule counters (participant, batch within their range)
+// and whether it may skip the grid-wide dependent-launch wait; then record the launch.
+struct OverlapDecision {
+  bool reg = false;
+  bool overlap = false;
+};
+OverlapDecision overlap_decide(const System& sys, const StepArgs& a, cudaStream_t stream, bool participant);
+void overlap_commit(const System& sys, const StepArgs& a, cudaStream_t stream, const OverlapDecision& d,
+                    cudaError_t launched);
 // Drops the records of a system being destroyed.
 void forget_system(const System* sys);
 cudaError_t launch_reset(const System& sys, float* pos, float* rot, float* vel, float* ang, int64_t n,
