@@ -445,6 +445,24 @@ def run_b200(args):
             del w2
             torch.cuda.empty_cache()
 
+    # ---- the M6 N-sweep's large end: the same scene at 65536 envs per GPU,
+    # same protocol, a graph of min(K, 200) launches
+    large_line = None
+    if not args.no_scenes and args.envs is None:
+        m, Kl = 65536, max(1, min(K, 200))
+        w3 = Workload(bx, synth, torch, args.scene, m, rank, stream)
+        w3.warmup(max(3, min(W, 20)))
+        w3.capture(Kl)
+        ms3 = bd.allreduce_max(w3.timed_replay(ranks, bd), device=dev)
+        peaks, peak_src = load_peaks()
+        rf = roofline(load_counts(args.scene), m, (ms3 / 1e3) / Kl, peaks, peak_src, {})
+        large_line = {"envs_per_gpu": m, "value": m * world * Kl / (ms3 / 1e3), "unit": "env-steps/s",
+                      "ms_per_step": ms3 / Kl, "steps": Kl, "frac": rf["frac"], "frac_lean": rf.get("frac_lean"),
+                      "kernel_config": w3.system.launch_config(m), "blowups": w3.blowups(),
+                      "l2": f"{w3.R} rotating batches"}
+        del w3
+        torch.cuda.empty_cache()
+
     # ---- NEXT-1: the same workload through brax_env_step (reward, done, auto-reset and
     # observations fused into the step), when the scene has a task block
     env_line = None
@@ -574,7 +592,8 @@ def run_b200(args):
                    "kernel_config": system.launch_config(n),
                    "comm": {"backend": ranks.backend, "nranks": ranks.nranks}},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K, "clocks": clocks,
-        "scenes": scene_lines, "env_epilogue": env_line, "rollout": roll_line, "vjp": vjp_line,
+        "scenes": scene_lines, "large_batch": large_line, "env_epilogue": env_line, "rollout": roll_line,
+        "vjp": vjp_line,
         "blowups": total_blowups, "substeps_per_s": value * system.substeps,
     }
     print(json.dumps(line), flush=True)

@@ -41,6 +41,8 @@ def test_bench_json_line():
         line = d["scenes"][sc]
         assert line["value"] > 0 and 0.0 < line["frac"] < 1.0 and line["blowups"] == 0, (sc, line)
     assert d["blowups"] == 0
+    big = d["large_batch"]
+    assert big["envs_per_gpu"] == 65536 and big["blowups"] == 0 and 0.0 < big["frac"] < 1.0
     roll = d["rollout"]
     assert roll["value"] > 0 and roll["blowups"] == 0 and 0.0 < roll["frac"] < 1.0
     if d.get("vjp"):
