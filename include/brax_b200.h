@@ -209,6 +209,18 @@ brax_status brax_system_phase_cycles(brax_system *sys, uint64_t out[4]);
 brax_status brax_system_set_autotune(brax_system *sys, int enable);
 brax_status brax_system_launch_config(const brax_system *sys, int64_t n_envs, int32_t out[6]);
 
+/* Launch overlap (DESIGN.md §5 "Launch overlap").  The step launches of a system
+ * (brax_step, brax_step_ex, brax_rollout*, brax_env_step*) register per group of 8 envs
+ * on device counters the system owns (2 x 2^19 words, allocated by brax_system_create);
+ * consecutive such launches on one stream, of the same system and n_envs, whose
+ * buffers are identical array for array or disjoint, start each block as soon as the
+ * earlier launches on its envs have finished instead of after the whole previous
+ * grid.  Results are bit-identical either way.  The library tracks its own launches
+ * per stream (and per stream capture); a kernel of OTHER code that uses programmatic
+ * dependent launch and triggers early, placed between two step launches on the same
+ * stream and writing their buffers, is not seen — separate such work with an event or
+ * set BRAX_NO_OVERLAP=1 (every launch then waits for the previous grid). */
+
 /* Lint warning i (0 <= i < n_lint_warnings) as text; NULL if out of range. */
 const char *brax_system_lint_warning(const brax_system *sys, int32_t i);
 
