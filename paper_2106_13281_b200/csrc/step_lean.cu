@@ -564,7 +564,11 @@ TrackKey track_key(cudaStream_t stream) {
     cudaGetLastError();
     id = 0;
   }
-  return TrackKey{d, stream, st == cudaStreamCaptureStatusActive ? id : 0ull};
+  const TrackKey key{d, stream, st == cudaStreamCaptureStatusActive ? id : 0ull};
+  if (std::get<2>(key) != 0 && g_track.size() > 1024 && !g_track.count(key))
+    for (auto it = g_track.begin(); it != g_track.end();)  // finished captures' windows
+      it = std::get<2>(it->first) != 0 ? g_track.erase(it) : std::next(it);
+  return key;
 }
 
 void spans_of(const System& sys, const StepArgs& a, std::vector<Span>& rd, std::vector<Span>& wr) {
