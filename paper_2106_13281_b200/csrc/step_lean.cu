@@ -3,9 +3,10 @@
 // the identical order, so identical bits) with the per-substep scaffolding cut down
 // for the common launch shape (DESIGN.md §5 "Lean kernel").
 //
-// Applies to the two-envs-per-lane plans with G = 2 or 4 lane groups whose work plan
-// gives every warp at most one item step and at most one body step (the planner's
-// G > 1 rule W = max(item steps, body steps) does, up to 16 warps).  Then:
+// Applies to the plans whose work plan gives every warp at most one body step and at
+// most one item step (the planner's G > 1 rule W = max(item steps, body steps) does, up
+// to 16 warps) or, for the one-lane-group two-envs-per-lane plans of large batches
+// (W = ⌈item steps / 2⌉), two item steps (kItems = 2, physics launches).  Then:
 //   * G, the lanes per group, E and every record stride are compile-time constants;
 //   * each warp's item and body, their code class (the specialised classes of the
 //     kFixed variant, else the generic code) and their shared-memory record addresses
@@ -55,7 +56,9 @@ enum : int {
 // body gather shapes with compile-time list lengths (as in the kFixed variant)
 enum : int { kGatherGeneral = 0, kG12 = 1, kG20 = 2, kG22 = 3, kG32 = 4, kG41 = 5 };
 
-template <class S, int G, int R, bool kEnv>
+// kItems: the most item steps a warp of the plan has (2: the one-lane-group plans of large
+// batches, W = ⌈item steps / 2⌉; physics launches only)
+template <class S, int G, int R, bool kEnv, int kItems = 1>
 __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs ka) {
   // S = F2: two envs per lane (packed FP32); F1: one env per lane (small batches)
   constexpr int V = Lanes<S>::V, SL = Lanes<S>::SL, LG = 32 / G, E = V * LG, RW = LG * SL;
@@ -169,42 +172,52 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   if (dgb) tl[2] = gtime();
 #endif
 
-  // ---- this warp's program, resolved once: at most one item and one body ----
+  // ---- this warp's program, resolved once: at most kItems items and one body ----
   const DBody* bodies = reinterpret_cast<const DBody*>(sBlob + H.off_bodies);
   const int32_t* item_begin = reinterpret_cast<const int32_t*>(sBlob + P.off_item_begin);
   const int32_t* body_begin = reinterpret_cast<const int32_t*>(sBlob + P.off_body_begin);
-  const int it0 = item_begin[warp];
-  const int item = it0 < item_begin[warp + 1] ? reinterpret_cast<const int32_t*>(sBlob + P.off_items)[it0 * G + grp]
-                                              : -1;
+  const int it0 = item_begin[warp], nit = item_begin[warp + 1] - it0;
   const int bw0 = body_begin[warp];
   const int body = bw0 < body_begin[warp + 1]
                        ? reinterpret_cast<const int32_t*>(sBlob + P.off_bodies_of_warp)[bw0 * G + grp]
                        : -1;
-  int icls = kItemNone;
-  const uint32_t* iparams = nullptr;  // the item's parameter record (DJoint / DSlot) in shared memory
-  float *ip = nullptr, *ic = nullptr, *irec = nullptr, *icnt = nullptr;  // record addresses
-  if (item >= 0 && item < J) {
-    const DJoint& jt = reinterpret_cast<const DJoint*>(sBlob + H.off_joints)[item];
-    const int4 h0 = *reinterpret_cast<const int4*>(&jt);
-    icls = h0.w == 0 ? (h0.z == 1 ? kJointHinge : h0.z == 2 ? kJoint2 : h0.z == 3 ? kJoint3 : kJointGeneric)
-                     : kJointGeneric;
-    iparams = reinterpret_cast<const uint32_t*>(&jt);
-    ip = sQ + ((h0.x << LGS) + el) * QS;
-    ic = sQ + ((h0.y << LGS) + el) * QS;
-    irec = sJ + ((item << LGS) + el) * JS;
-  } else if (item >= J) {
-    const int c = item - J;
-    const DSlot& sl = reinterpret_cast<const DSlot*>(sBlob + H.off_slots)[c];
-    const int4 h0 = *reinterpret_cast<const int4*>(&sl), h1 = reinterpret_cast<const int4*>(&sl)[1];
-    const bool ground = h1.x == 0 && h1.y == 1 && (h1.z & kCapsuleOnGroundFlags) == kCapsuleOnGroundFlags;
-    icls = !ground ? kContactGeneric : h0.x == 1 ? kCapsuleGround : h0.x == 0 ? kSphereGround
-                                   : h0.x == 2 ? kBoxGround : kContactGeneric;
-    iparams = reinterpret_cast<const uint32_t*>(&sl);
-    ip = sQ + ((h0.y << LGS) + el) * QS;
-    ic = sQ + ((h0.z << LGS) + el) * QS;
-    irec = sC + ((c << LGS) + el) * CS;
-    icnt = sCnt + c * RW + el * SL;
-  }
+  struct ItemProg {
+    int cls = kItemNone;
+    const uint32_t* params = nullptr;  // the item's parameter record (DJoint / DSlot) in shared memory
+    float *p = nullptr, *c = nullptr, *rec = nullptr, *cnt = nullptr;  // record addresses
+  };
+  auto resolve = [&](int k) {
+    ItemProg r;
+    const int item = k < nit ? reinterpret_cast<const int32_t*>(sBlob + P.off_items)[(it0 + k) * G + grp] : -1;
+    if (item >= 0 && item < J) {
+      const DJoint& jt = reinterpret_cast<const DJoint*>(sBlob + H.off_joints)[item];
+      const int4 h0 = *reinterpret_cast<const int4*>(&jt);
+      r.cls = h0.w == 0 ? (h0.z == 1 ? kJointHinge : h0.z == 2 ? kJoint2 : h0.z == 3 ? kJoint3 : kJointGeneric)
+                        : kJointGeneric;
+      r.params = reinterpret_cast<const uint32_t*>(&jt);
+      r.p = sQ + ((h0.x << LGS) + el) * QS;
+      r.c = sQ + ((h0.y << LGS) + el) * QS;
+      r.rec = sJ + ((item << LGS) + el) * JS;
+    } else if (item >= J) {
+      const int c = item - J;
+      const DSlot& sl = reinterpret_cast<const DSlot*>(sBlob + H.off_slots)[c];
+      const int4 h0 = *reinterpret_cast<const int4*>(&sl), h1 = reinterpret_cast<const int4*>(&sl)[1];
+      const bool ground = h1.x == 0 && h1.y == 1 && (h1.z & kCapsuleOnGroundFlags) == kCapsuleOnGroundFlags;
+      r.cls = !ground ? kContactGeneric : h0.x == 1 ? kCapsuleGround : h0.x == 0 ? kSphereGround
+                                        : h0.x == 2 ? kBoxGround : kContactGeneric;
+      r.params = reinterpret_cast<const uint32_t*>(&sl);
+      r.p = sQ + ((h0.y << LGS) + el) * QS;
+      r.c = sQ + ((h0.z << LGS) + el) * QS;
+      r.rec = sC + ((c << LGS) + el) * CS;
+      r.cnt = sCnt + c * RW + el * SL;
+    }
+    return r;
+  };
+  const ItemProg it_a = resolve(0);
+  const ItemProg it_b = kItems > 1 ? resolve(1) : ItemProg{};
+  const int icls = it_a.cls;
+  const uint32_t* iparams = it_a.params;
+  float *ip = it_a.p, *ic = it_a.c;
   int gcls = kGatherGeneral, j0 = 0, nj = 0, c0 = 0, nc = 0;
   bool free_body = false;
   float* brow = nullptr;
@@ -296,7 +309,8 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
     } else {
       load_actions<V>(a, sA, A, E, LG, step, e0, nvalid);
     }  // sA is read after the next barrier
-    if (icnt) Lanes<S>::st(icnt, bc<S>(0.f));
+    if (it_a.cnt) Lanes<S>::st(it_a.cnt, bc<S>(0.f));
+    if (kItems > 1 && it_b.cnt) Lanes<S>::st(it_b.cnt, bc<S>(0.f));
     const bool pf_act = act_bulk && tid == 0 && step + 1 < a.n_steps;
     for (int s = 0; s < H.S; ++s) {
       __syncthreads();
@@ -308,22 +322,29 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
         mbar_expect_tx(&bars[1], act_bytes);
         tma_load(sAstg, a.actions + ((step + 1) * a.n_envs + e0) * A, act_bytes, &bars[1]);
       }
-      // phase 1: this warp's joint (with its actuator) or contact slot (S3-S5)
-      if (icls != kItemNone) {
-        const Row<S> rp{ip}, rc{ic};
-        if (icls <= kJointGeneric) {
-          const DJoint& jt = *reinterpret_cast<const DJoint*>(iparams);
+      // phase 1: this warp's joint (with its actuator) or contact slot (S3-S5); kItems = 2:
+      // the second one after it (one call site per class: the loop is not unrolled)
+#pragma unroll 1
+      for (int k = 0; k < kItems; ++k) {
+        const ItemProg& it = k == 0 ? it_a : it_b;
+        const int cls = it.cls;
+        if (cls == kItemNone) break;
+        const Row<S> rp{it.p}, rc{it.c};
+        float* const irec = it.rec;
+        if (cls <= kJointGeneric) {
+          const DJoint& jt = *reinterpret_cast<const DJoint*>(it.params);
           const float* act = sA + el * SL;
-          if (icls == kJointHinge) joint<S, 1, 0>(jt, rp, rc, act, RW, irec);
-          else if (icls == kJoint2) joint<S, 2, 0>(jt, rp, rc, act, RW, irec);
-          else if (icls == kJoint3) joint<S, 3, 0>(jt, rp, rc, act, RW, irec);
+          if (cls == kJointHinge) joint<S, 1, 0>(jt, rp, rc, act, RW, irec);
+          else if (cls == kJoint2) joint<S, 2, 0>(jt, rp, rc, act, RW, irec);
+          else if (cls == kJoint3) joint<S, 3, 0>(jt, rp, rc, act, RW, irec);
           else joint<S>(jt, rp, rc, act, RW, irec);
         } else {
-          const DSlot& sl = *reinterpret_cast<const DSlot*>(iparams);
+          const DSlot& sl = *reinterpret_cast<const DSlot*>(it.params);
+          float* const icnt = it.cnt;
           S cnt = Lanes<S>::ld(icnt);
-          if (icls == kCapsuleGround) contact<S, 1>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
-          else if (icls == kSphereGround) contact<S, 2>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
-          else if (icls == kBoxGround) contact<S, 3>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
+          if (cls == kCapsuleGround) contact<S, 1>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
+          else if (cls == kSphereGround) contact<S, 2>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
+          else if (cls == kBoxGround) contact<S, 3>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
           else contact<S>(sl, rp, rc, 1.f + H.e, H.beta_over_h, H.mu, irec, cnt);
           Lanes<S>::st(icnt, cnt);
         }
@@ -493,7 +514,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   }
 }
 
-template <class S, int G, int R, bool kEnv = false>
+template <class S, int G, int R, bool kEnv = false, int kItems = 1>
 cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_t smem, cudaStream_t stream) {
   static bool attr_set[64] = {};
   int dev = 0;
@@ -504,7 +525,8 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
 #else
     const int max_dyn = kMaxDynSmem;
 #endif
-    cudaError_t e = cudaFuncSetAttribute(brax_step_lean<S, G, R, kEnv>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    cudaError_t e =
+        cudaFuncSetAttribute(brax_step_lean<S, G, R, kEnv, kItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
@@ -518,7 +540,7 @@ cudaError_t launch_lean_variant(const LeanArgs& ka, dim3 grid, dim3 block, size_
   attr[0].val.programmaticStreamSerializationAllowed = std::getenv("BRAX_NO_PDL") ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, brax_step_lean<S, G, R, kEnv>, ka);
+  return cudaLaunchKernelEx(&cfg, brax_step_lean<S, G, R, kEnv, kItems>, ka);
 }
 
 // ---- launch-order bookkeeping for overlapped launches (DESIGN.md §5 "Launch overlap") ----
@@ -676,13 +698,14 @@ bool lean_applies(const System& sys, int plan, const StepArgs& a) {
   if (P.V != 2 && P.G == 1) return false;  // one env per lane: the lane-group plans only
   if ((a.env && a.n_steps == 0) || a.contact_dp || sys.trace || a.dpos_out) return false;  // observe-only: generic
   if (a.env && P.G == 1) return false;  // env instantiations: the lane-group plans
-  if (!sys.lean_plan_ok[plan]) return false;
+  const int items = sys.lean_items[plan];
+  if (items == 0 || (items == 2 && (a.env || P.G != 1 || P.V != 2))) return false;  // kItems = 2: G = 1, F2, physics
   return (a.env ? P.smem_bytes_env : P.smem_bytes) <= kMaxDynSmem;
 }
 
 namespace {
-cudaError_t dispatch_lean(const LeanArgs& ka, const DPlan& P, bool env, int regs, dim3 grid, dim3 block, size_t smem,
-                          cudaStream_t stream) {
+cudaError_t dispatch_lean(const LeanArgs& ka, const DPlan& P, bool env, int items, int regs, dim3 grid, dim3 block,
+                          size_t smem, cudaStream_t stream) {
   if (env) {  // env-epilogue instantiations (register budgets 128 / 96)
     if (P.V == 2) {
       if (P.G == 2) {
@@ -701,6 +724,11 @@ cudaError_t dispatch_lean(const LeanArgs& ka, const DPlan& P, bool env, int regs
   }
   // register budgets: the largest instantiation not above `regs` (F2 128 / 96 / 80; F1 128 / 96 / 64)
   if (P.V == 2) {
+    if (P.G == 1 && items == 2) {
+      if (regs >= 128) return launch_lean_variant<F2, 1, 128, false, 2>(ka, grid, block, smem, stream);
+      if (regs >= 96) return launch_lean_variant<F2, 1, 96, false, 2>(ka, grid, block, smem, stream);
+      return launch_lean_variant<F2, 1, 80, false, 2>(ka, grid, block, smem, stream);
+    }
     if (P.G == 1) {
       if (regs >= 128) return launch_lean_variant<F2, 1, 128>(ka, grid, block, smem, stream);
       if (regs >= 96) return launch_lean_variant<F2, 1, 96>(ka, grid, block, smem, stream);
@@ -748,7 +776,7 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
   ka.gd = sys.d_gran + kMaxGranules;
   ka.reg = d.reg ? 1 : 0;
   ka.overlap = d.overlap ? 1 : 0;
-  const cudaError_t e = dispatch_lean(ka, P, a.env != 0, regs, grid, block, smem, stream);
+  const cudaError_t e = dispatch_lean(ka, P, a.env != 0, sys.lean_items[plan], regs, grid, block, smem, stream);
   overlap_commit(sys, a, stream, d, e);
   return e;
 }

@@ -413,7 +413,7 @@ System* build_host(const Config& cfg) {
         max_items = std::max(max_items, per_warp[w].size());
         max_bodies = std::max(max_bodies, wb[w].size());
       }
-      s->lean_plan_ok[pi] = max_items <= 1 && max_bodies <= 1;
+      s->lean_items[pi] = max_bodies <= 1 && max_items <= 2 ? std::max<int>(1, int(max_items)) : 0;
     }
     P.off_bodies_of_warp = int32_t(blob.size());
     for (int w = 0; w < W; ++w)

@@ -38,7 +38,9 @@ struct System {
   unsigned long long* d_phase_cycles = nullptr;  // device [4]
   uint32_t* d_gran = nullptr;          // device [2][kMaxGranules]: launches started / finished per env granule
   size_t smem_bytes = 0;
-  bool lean_plan_ok[kNumPlans] = {};   // plan gives every warp at most one item step and one body step
+  // the lean kernel's reach per plan: the most item steps any warp has (1 or 2; 0 = more,
+  // or a warp with more than one body step)
+  int lean_items[kNumPlans] = {};
   // launch configuration per batch size, measured by brax_system_tune
   // (every plan gives the same bits, so the choice only affects speed)
   bool autotune = true;

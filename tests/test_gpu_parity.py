@@ -277,7 +277,7 @@ def test_every_launch_plan_matches_oracle(name):
         for plan, fixed, lean in (("1,1", "0", "0"), ("2,1", "0", "0"), ("4,1", "0", "0"), ("1,2", "0", "0"),
                                   ("2,2", "0", "0"), ("4,2", "0", "0"), ("1,2", "1", "0"), ("2,2", "1", "0"),
                                   ("4,2", "1", "0"), ("2,2", "1", "1"), ("4,2", "1", "1"), ("2,1", "0", "1"),
-                                  ("4,1", "0", "1")):
+                                  ("4,1", "0", "1"), ("1,2", "1", "1")):
             for regs in ("56", "96", "128"):
                 os.environ["BRAX_PLAN"] = plan
                 os.environ["BRAX_MAXREG"] = regs
