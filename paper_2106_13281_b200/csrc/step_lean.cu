@@ -48,6 +48,13 @@ struct LeanArgs {
   int32_t overlap;   // skip griddepcontrol.wait: wait for the granules' earlier launches instead
 };
 
+#ifdef BRAX_DIAG
+// block timelines (tools/experiments/overlap_timeline.sh): [launch tag][block][entry, after
+// the wait, staged, loop end, stored, smid, overlap, exit] in globaltimer ns
+constexpr int kDiagLaunches = 16, kDiagBlocks = 4096;
+__device__ long long g_diag_tl[kDiagLaunches * kDiagBlocks * 8];
+#endif
+
 // item classes (warp-uniform: the items sharing a warp step share a class)
 enum : int {
   kItemNone = 0, kJointHinge = 1, kJoint2 = 2, kJoint3 = 3, kJointGeneric = 4,
@@ -102,7 +109,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
 #ifdef BRAX_DIAG  // block timeline (globaltimer, ns): entry, after griddepcontrol.wait, staged, loop end, exit
   __shared__ long long sDg[kMaxWarps][4];
   long long tl[5] = {0, 0, 0, 0, 0};
-  const bool dgb = a.diag_block && tid == 0 && (blockIdx.x % 64) == 0;
+  const bool dgb = a.diag_block && tid == 0 && (a.diag_block >= 1000 || (blockIdx.x % 64) == 0);
   auto gtime = []() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
   if (dgb) tl[0] = gtime();
 #endif
@@ -488,13 +495,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
       if (ka.reg) tma_store_commit_wait_all();  // written, not just read: a later launch may run now
       else tma_store_commit_wait();
 #ifdef BRAX_DIAG
-      if (dgb) {
-        tl[4] = gtime();
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        printf("BLOCK %u sm %u t0 %lld wait %lld stage %lld loop %lld store %lld\n", blockIdx.x, smid, tl[0] % 100000000,
-               tl[1] - tl[0], tl[2] - tl[1], tl[3] - tl[2], tl[4] - tl[3]);
-      }
+      if (dgb) tl[4] = gtime();
 #endif
     }
   } else {
@@ -512,6 +513,17 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
       for (int k = 0; k < ng; ++k) atomicAdd(ka.gd + g0 + k, 1u);
     }
   }
+#ifdef BRAX_DIAG  // block timeline of launch tag (diag_block - 1000) into g_diag_tl, no printf in the way
+  if (dgb && tl[4] && a.diag_block >= 1000 && a.diag_block < 1000 + kDiagLaunches && blockIdx.x < kDiagBlocks) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    long long* r = g_diag_tl + (size_t(a.diag_block - 1000) * kDiagBlocks + blockIdx.x) * 8;
+    for (int k = 0; k < 5; ++k) r[k] = tl[k];
+    r[5] = smid;
+    r[6] = ka.overlap;
+    r[7] = gtime();
+  }
+#endif
 }
 
 template <class S, int G, int R, bool kEnv = false, int kItems = 1>
@@ -782,3 +794,11 @@ cudaError_t launch_lean(const System& sys, const StepArgs& a, int plan, int regs
 }
 
 }  // namespace brax
+
+#ifdef BRAX_DIAG
+extern "C" int brax_diag_timeline(long long* out, long long n) {  // diagnostic builds only
+  const long long total = (long long)brax::kDiagLaunches * brax::kDiagBlocks * 8;
+  return cudaMemcpyFromSymbol(out, brax::g_diag_tl, size_t(n < total ? n : total) * sizeof(long long)) == cudaSuccess
+             ? 0 : 1;
+}
+#endif
