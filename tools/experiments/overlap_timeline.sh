@@ -35,6 +35,9 @@ for k in range(K):
     w = (r[:, 1] - r[:, 0]) / 1e3
     print(f"{k:6d} {int(r[0, 6]):7d}  {st0.min():7.1f} {np.median(st0):7.1f} {st0.max():7.1f}   {np.median(ready):7.1f}"
           f"   {end.min():7.1f} {np.median(end):7.1f} {end.max():7.1f}   {np.median(w):6.1f} {w.max():6.1f}")
+ph = np.concatenate([tl[k] for k in range(1, K)])
+print("median per block (us): wait %.2f  stage %.2f  loop %.2f  store %.2f  release+exit %.2f" % tuple(
+    np.median((ph[:, b] - ph[:, a]) / 1e3) for a, b in ((0, 1), (1, 2), (2, 3), (3, 4), (4, 7))))
 tot = (tl[K - 1, :, 7].max() - t0) / 1e3
 print(f"{K} launches in {tot:.1f} us: {tot / K:.2f} us per launch")
 PY
