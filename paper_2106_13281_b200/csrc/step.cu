@@ -145,13 +145,21 @@ __global__ void __maxnreg__(R) brax_step_kernel(const __grid_constant__ KArgs ka
   // for an overlapped launch, only for the earlier launches on this block's env granules
   if (!ka.overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int g0 = int(e0 / kGranule), ng = (nvalid + kGranule - 1) / kGranule;
-  uint32_t gprev = 0;
-  if (ka.reg && tid < ng) gprev = atomicAdd(ka.gs + g0 + tid, 1u);
+  uint32_t gprev = 0, gdone = 0;
+  if (ka.reg && tid < ng) {
+    // register, and read the finished count in the same round trip: completions counted
+    // before our registration are all of earlier launches (a later one waits for us)
+    gprev = atomicAdd(ka.gs + g0 + tid, 1u);
+    gdone = ld_acquire_gpu(ka.gd + g0 + tid);
+  }
   if (ka.reg) __syncthreads();  // every registration performed before the trigger
   asm volatile("griddepcontrol.launch_dependents;");
   if (ka.reg) {
     if (tid < ng)
-      while (int32_t(ld_acquire_gpu(ka.gd + g0 + tid) - gprev) < 0) __nanosleep(64);
+      while (int32_t(gdone - gprev) < 0) {
+        __nanosleep(64);
+        gdone = ld_acquire_gpu(ka.gd + g0 + tid);
+      }
     __syncthreads();
     if (tid == 0) fence_proxy_async_global();
   }
