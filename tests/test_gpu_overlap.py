@@ -178,13 +178,21 @@ def test_two_streams_share_a_system():
         assert torch.equal(P[k], RP[k]) and torch.equal(Q[k], RQ[k]), k
 
 
-def test_env_chain_matches_serialised_launches():
-    o = oracle.Oracle(oracle.load_scene("ant"))
-    s = bx.System(oracle.load_scene("ant"))
+@pytest.mark.parametrize("scene,plan,lean", [("ant", None, None), ("ant", "4,2", "0"), ("ant", "1,2", "0"),
+                                             ("ant", "2,1", "1"), ("grasp", None, None)])
+def test_env_chain_matches_serialised_launches(scene, plan, lean):
+    """Env launches (reward / done / auto-reset / observations; grasp: goal markers) overlapped,
+    lean and generic kernels, against the same launches serialised."""
+    o = oracle.Oracle(oracle.load_scene(scene))
+    s = bx.System(oracle.load_scene(scene))
     n = 2000
     acts = torch.from_numpy(synth.actions(21, 40, n, o.act_dim)).cuda()
+    env = {} if plan is None else {"BRAX_PLAN": plan, "BRAX_LEAN": lean, "BRAX_FIXED_GATHER": "1"}
 
     def go(sync):
+        return with_env(env, lambda: go_(sync))
+
+    def go_(sync):
         st = s.env_state(n)
         s.env_reset(st, seed=5)
         outs = []
