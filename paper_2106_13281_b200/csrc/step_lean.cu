@@ -253,9 +253,21 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
   const float* sCe = sC + el * CS;
 
   const int od = T.obs_dim;
-  auto save_x0 = [&]() {  // NEXT-1: torso (goal: object) position at the step boundary (before S2)
-    for (int i = tid; i < E; i += blockDim.x)
-      for (int k = 0; k < 3; ++k) sX0[3 * i + k] = sQ[qword<V>(T.obj, i, 0, k, LG)];
+  // NEXT-1: the torso's (goal tasks: the object's) position at the step boundary, before S2,
+  // saved by the lane group that integrates that body (program order: no barrier needed)
+  auto save_x0 = [&]() {
+    if (body != T.obj) return;
+    const V3T<S> x = Row<S>{brow}.pos();
+    if constexpr (V == 2) {
+      const float a0[3] = {x.x.x, x.y.x, x.z.x}, a1[3] = {x.x.y, x.y.y, x.z.y};
+      for (int k = 0; k < 3; ++k) {
+        sX0[3 * el + k] = a0[k];
+        sX0[3 * (el + LG) + k] = a1[k];
+      }
+    } else {
+      const float a0[3] = {x.x.x, x.y.x, x.z.x};
+      for (int k = 0; k < 3; ++k) sX0[3 * el + k] = a0[k];
+    }
   };
   auto observe = [&](float* obs_out) {  // NEXT-1: obs rows of the block's envs -> obs_out [nvalid][od]
     if (icls != kItemNone && icls <= kJointGeneric) {  // joints: angles and rates, by the warps that own them
@@ -265,7 +277,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
     // torso, goal and contact parts, one thread per (env, word)
     const int nco = T.contact_obs ? 6 * B : 0, ng = T.has_goal ? 9 : 0, nw = 11 + ng + nco;
     for (int i = tid; i < E * nw; i += blockDim.x) {
-      const int env = i / nw, k = i - env * nw;
+      const int k = i / E, env = i - k * E;  // E is a compile-time power of two: shifts, not a division
       float v;
       int at;
       if (k < 11) {
@@ -294,15 +306,11 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
 
   // S2 of the first substep; every later S2 is fused into the previous substep's integrate()
   // (env mode ends every step at the boundary: its S2 runs at the next step's start)
-  if (kEnv) {
-    save_x0();
-    __syncthreads();
-  }
+  if (kEnv) save_x0();
   if (body >= 0) kinematic<S>(bodies[body], Row<S>{brow}, H.h);
   for (int64_t step = 0; step < a.n_steps; ++step) {
     if (kEnv && step > 0) {
       save_x0();
-      __syncthreads();
       if (body >= 0) kinematic<S>(bodies[body], Row<S>{brow}, H.h);
     }
     if (act_bulk) {  // this step's actions arrived in sAstg [E][A]; transpose to sA [A][E]
@@ -448,7 +456,7 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
       __syncthreads();
       // auto-reset of done envs (R34): default_qp + noise, Philox counter (env, b, f, episode)
       for (int i = tid; i < E * B; i += blockDim.x) {
-        const int env = i / B, b = i - env * B;
+        const int b = i / E, env = i - b * E;
         if (!sRst[env]) continue;
         float x[3], q[4], v[3], w[3];
         reset_body(a.dqp, a.masks, B, b, uint32_t(a.env_offset + e0 + env), sEp[env], key, T.noise_vel,

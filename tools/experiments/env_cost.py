@@ -24,6 +24,7 @@ for r in range(R):
                 "episode": torch.zeros(n, dtype=torch.int32, device="cuda"),
                 "obs": torch.empty((n, od), device="cuda"), "reward": torch.empty(n, device="cuda"),
                 "done": torch.empty(n, dtype=torch.uint8, device="cuda")})
+s.tune(sets[0], acts[0])
 res = {"cfg": s.launch_config(n)}
 
 
