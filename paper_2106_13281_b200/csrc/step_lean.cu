@@ -125,8 +125,8 @@ __global__ void __maxnreg__(R) brax_step_lean(const __grid_constant__ LeanArgs k
     tma_load(sBlob, ka.blob, uint32_t(H.blob_words) * 4u, &bars[0]);
   }
   // The QP may be the previous launch's output.  Default: PDL's grid-wide wait.  Overlapped
-  // launches (host-checked: the previous kernel on this stream was a lean launch of this
-  // system whose buffers are this launch's, env for env, or disjoint from them): register as
+  // launches (host-checked: the launches of this system still in flight on this stream use
+  // buffers that are this launch's, env for env, or disjoint from them): register as
   // the next launch of each of the block's env granules, let the next launch be scheduled,
   // and wait only until every earlier launch on these granules has finished.
   if (!ka.overlap) asm volatile("griddepcontrol.wait;" ::: "memory");
