@@ -41,4 +41,4 @@ print("median per block (us): wait %.2f  stage %.2f  loop %.2f  store %.2f  rele
 tot = (tl[K - 1, :, 7].max() - t0) / 1e3
 print(f"{K} launches in {tot:.1f} us: {tot / K:.2f} us per launch")
 PY
-BRAX_LIB_PATH=$PWD/_ab/libdiag.so BRAX_PLAN=4,2 BRAX_MAXREG=96 BRAX_FIXED_GATHER=1 BRAX_LEAN=1 timeout 120 python /tmp/otl.py > gpurun_out/overlap_timeline.txt 2>&1
+BRAX_LIB_PATH=$PWD/_ab/${DIAGLIB:-libdiag.so} BRAX_PLAN=4,2 BRAX_MAXREG=96 BRAX_FIXED_GATHER=1 BRAX_LEAN=1 timeout 120 python /tmp/otl.py > gpurun_out/overlap_timeline.txt 2>&1
