@@ -122,12 +122,15 @@ def r24_qualifies(o, qp, acts, T):
 
 
 @pytest.mark.parametrize("name,n,zero_action", [("ball", 1, True), ("pendulum", 1024, False),
-                                                ("chain2", 1024, False), ("ant", 512, True)])
+                                                ("chain2", 1024, False), ("ant", 512, True),
+                                                ("fetch", 512, True), ("grasp", 512, True)])
 def test_100_step_parity(name, n, zero_action):
     """Free-running GPU vs oracle trajectories, 100 steps, ≤ 1e-3 (R24-qualified configs).
     Envs are excluded only by the standard R23 band (|d| < 1e-5, j_n·k(n) < 1e-5 in some
     substep), evaluated along the oracle's own trajectory; at least 95 % must remain
-    (ant: 16 of 512 excluded, measured on B200, tools/parity100.py)."""
+    (ant: 16 of 512 excluded, measured on B200, tools/parity100.py; fetch 23 and grasp 1
+    of 512, settling with zero actions — humanoid and halfcheetah do not qualify: R24
+    fails or the R23 band takes most envs of a resting capsule body)."""
     o, s = scene(name)
     T = 100
     qp = synth.to_f32(o.reset(n, 11, 0.1, 0.1))
